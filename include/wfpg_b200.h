@@ -1,0 +1,342 @@
+/*
+ * wfpg_b200.h — C ABI of the B200-native guided wavefront render path.
+ *
+ * Drop-in boundary for the reference package `wfpg` (arXiv 2405.06997 CPU
+ * reference, /root/reference/pkg).  The reference crosses Python -> native
+ * code at the Cython `def *_kernel` functions of src/wfpg/_kernels.pyx and
+ * at the numpy-level SVO / guiding / wavefront functions; every entry point
+ * below names the reference interface it replaces (file:line, paths relative
+ * to /root/reference/pkg/src/wfpg/).
+ *
+ * Conventions
+ *  - Plain C types only.  Every pointer inside a struct or argument is a
+ *    DEVICE pointer unless the field comment says "host".
+ *  - The caller owns every buffer.  Functions never allocate device memory;
+ *    entry points that need scratch take a caller-provided workspace whose
+ *    size is returned by the matching *_workspace_bytes() query.
+ *  - All work is enqueued on `stream` (a cudaStream_t passed as void*).
+ *    Functions that must report a device-side count to the host say so.
+ *  - Return value: WFPG_OK (0) or a WFPG_ERR_* code; wfpg_last_error()
+ *    returns a human-readable message for the last failure on this thread.
+ *  - Index width: triangle ids, node ids and path ids are int32 on the
+ *    device (the reference uses int64; the Python layer widens on export).
+ *  - Floating point: fp64 throughout, like the reference.
+ */
+#ifndef WFPG_B200_H
+#define WFPG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WFPG_ABI_VERSION 1
+
+enum wfpg_status {
+  WFPG_OK = 0,
+  WFPG_ERR_ARG = 1,        /* invalid argument (reference: ValueError) */
+  WFPG_ERR_CUDA = 2,       /* CUDA runtime error */
+  WFPG_ERR_WORKSPACE = 3,  /* workspace too small */
+  WFPG_ERR_CAPACITY = 4    /* a device-side count exceeded the caller's capacity */
+};
+
+/* ------------------------------------------------------------------------ */
+/* Data contracts                                                            */
+/* ------------------------------------------------------------------------ */
+
+/* Scene arrays: scene.py:85-131 (Scene.__init__) + bvh.py:33-119 (Bvh). */
+typedef struct wfpg_scene {
+  int32_t n_tris;
+  const double* v0;          /* (T,3) */
+  const double* v1;          /* (T,3) original vertices (voxelize uses them, svo.py:110) */
+  const double* v2;          /* (T,3) */
+  const double* e1;          /* (T,3) v1 - v0 */
+  const double* e2;          /* (T,3) v2 - v0 */
+  const double* normals;     /* (T,3) unit geometric normals, bit-exact host copy */
+  const int32_t* tri_mat;    /* (T,)  material id */
+  const int32_t* mat_kind;   /* (M,)  0 lambert, 1 mirror, 2 emitter (scene.py:18) */
+  const double* mat_rgb;     /* (M,3) */
+  int32_t n_mats;
+  int32_t n_emit;
+  const double* emitter_cdf; /* (E,) area CDF */
+  const int32_t* emitter_tris; /* (E,) */
+  double emitter_area;
+  double ray_eps;            /* 1e-4 * scene diagonal (scene.py:22,108) */
+  double bbox_lo[3];         /* host values */
+  double bbox_hi[3];
+  int32_t bvh_nodes;
+  const double* bvh_lo;      /* (N,3) */
+  const double* bvh_hi;      /* (N,3) */
+  const int32_t* bvh_left;   /* (N,) */
+  const int32_t* bvh_right;  /* (N,) */
+  const int32_t* bvh_count;  /* (N,) 0 = inner node */
+  const int32_t* bvh_order;  /* (T,) */
+  int32_t brute;             /* 1 when T <= 512: nearest-hit queries use the brute
+                                force path (_kernelshim.py:13-21) */
+} wfpg_scene;
+
+/* Pinhole camera: scene.py:29-61 (Camera). Host values. */
+typedef struct wfpg_camera {
+  double position[3];
+  double forward[3];
+  double right[3];
+  double up[3];              /* Camera.up_ortho */
+  double tan_half;
+  int32_t width;
+  int32_t height;
+} wfpg_camera;
+
+/* Sparse voxel octree: svo.py:176-224 (SvoCache).  Level-grouped flat node
+ * arrays, level 0 = root, node id = flat index. */
+typedef struct wfpg_svo {
+  int32_t depth;
+  int32_t resolution;
+  int64_t n_nodes;
+  double lo[3];              /* host: cube_lo */
+  double size;               /* host: cube_size */
+  int64_t level_off[32];     /* host: depth+2 entries used */
+  uint64_t* codes;           /* (n,) morton code at the node's level */
+  int32_t* child_base;       /* (n,) first child, -1 for leaves */
+  uint8_t* child_mask;       /* (n,) */
+  int32_t* parent;           /* (n,) -1 for the root */
+  uint32_t* node_desc;       /* (n,2) packed {child_base, child_mask} for descents */
+  double* normal;            /* (n,3) normal_a (normal_b = -normal_a) */
+  double* sum_a;             /* (n,3) */
+  double* sum_b;             /* (n,3) */
+  double* weight_a;          /* (n,)  */
+  double* weight_b;          /* (n,)  */
+  double* mean_a;            /* (n,3) */
+  double* mean_b;            /* (n,3) */
+  int32_t* counter;          /* (n,)  Alg. 2 ray counters, zero between calls */
+} wfpg_svo;
+
+/* Wavefront path state: wavefront.py:53-71 (PathState), SoA. */
+typedef struct wfpg_paths {
+  int64_t n;
+  int32_t max_depth;         /* rec arrays have max_depth+1 slots per path */
+  double* ray_o;             /* (P,3) */
+  double* ray_d;             /* (P,3) */
+  double* beta;              /* (P,3) */
+  double* radiance;          /* (P,3) */
+  uint64_t* key;             /* (P,) */
+  uint64_t* ctr;             /* (P,) */
+  uint8_t* alive;            /* (P,) */
+  double* prev_pdf;          /* (P,) */
+  double* rec_pos;           /* (P,D+1,3) */
+  double* rec_T;             /* (P,D+1,3) */
+  double* emit_le;           /* (P,3) */
+  int32_t* emit_depth;       /* (P,) */
+} wfpg_paths;
+
+/* Per-depth guide tables: guiding.py:254-309 (GuideTables).  The B200 layout
+ * keeps the floored field values plus their row sums, marginal CDF and
+ * totals; conditional CDFs, pdf tables and product block CDFs are evaluated
+ * on the fly by the samplers with the same arithmetic as fill_batch. */
+typedef struct wfpg_guide {
+  int32_t mode;              /* 0 off, 1 plain, 2 product */
+  int32_t n;                 /* field resolution */
+  int32_t capacity;          /* bin slots allocated */
+  double eps;                /* guiding.EPSILON_FLOOR */
+  double* vals;              /* (B,n,n) */
+  double* row_sum;           /* (B,n)   values.sum(axis=2) */
+  double* marg;              /* (B,n)   cumsum(row_sums)/totals */
+  double* total;             /* (B,)    */
+  double* block_sums;        /* (B,8,8) product mode (else may be NULL) */
+  const int32_t* n_bins;     /* device count of valid slots */
+} wfpg_guide;
+
+/* Knobs of one render pass: wavefront.py:21-50 (GuidingConfig). */
+typedef struct wfpg_pass_config {
+  int32_t l_min;
+  int32_t c_ray;
+  int32_t field_res;
+  int32_t guided_depths;
+  int32_t max_depth;
+  int32_t product;
+  int32_t jitter;
+  double blur_sigma;
+  double epsilon;
+  int32_t russian_roulette;
+  int32_t rr_depth;
+  uint64_t seed;
+  int64_t sample_index;      /* first sample index of the pass */
+  int32_t n_samples;         /* samples per pixel in this pass */
+  int32_t deterministic;     /* 1: exitance splat in path order (np.add.at) */
+  int32_t blur_radius;       /* core._blur_kernel radius (0: no blur) */
+  double blur_w[33];         /* normalised blur taps, computed by numpy on the host */
+} wfpg_pass_config;
+
+/* Per-pass statistics returned to the host: wavefront.py:81-85 (PassStats). */
+typedef struct wfpg_pass_stats {
+  int32_t depths_run;
+  int32_t bins_per_depth[32];
+  int32_t rays_per_depth[32];
+  int32_t live_per_depth[32];
+  int32_t deposits;
+  int32_t mat_groups[32][16]; /* per depth, per material id (first 16 ids) */
+} wfpg_pass_stats;
+
+/* ------------------------------------------------------------------------ */
+/* Library                                                                   */
+/* ------------------------------------------------------------------------ */
+
+int wfpg_abi_version(void);
+const char* wfpg_last_error(void);
+/* Number of kernel launches issued by this library since load (process-wide). */
+uint64_t wfpg_launch_count(void);
+
+/* ------------------------------------------------------------------------ */
+/* Device primitives (scan, stable radix sort)                               */
+/* ------------------------------------------------------------------------ */
+
+size_t wfpg_scan_workspace_bytes(int64_t n);
+/* Exclusive prefix sum of n uint32 values; writes the total to *total (device). */
+int wfpg_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* total,
+                  void* workspace, size_t ws_bytes, void* stream);
+
+size_t wfpg_sort_workspace_bytes(int64_t n);
+/* Stable LSD radix sort of (key, value) pairs on the low `key_bits` bits.
+ * n_dev (optional, device int32) overrides n with a device-side count <= n. */
+int wfpg_sort_pairs_u64(uint64_t* keys, uint32_t* vals, int64_t n, const int32_t* n_dev,
+                        int32_t key_bits, void* workspace, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Item 1 — SVO builder                                                      */
+/* ------------------------------------------------------------------------ */
+
+/* svo.py:94-136 (voxelize).  Pass 1: candidate counts -> upper bound of the
+ * fragment count (host, synchronous). */
+size_t wfpg_voxelize_workspace_bytes(int32_t n_tris, int64_t n_candidates);
+/* Pass 1: number of candidate voxels (sum of triangle bbox voxel ranges),
+ * host value, synchronous.  Workspace: wfpg_voxelize_workspace_bytes(T, 0). */
+int wfpg_voxelize_count(const wfpg_scene* scene, const double* cube_lo, double side,
+                        int32_t resolution, int64_t* n_candidates,
+                        void* workspace, size_t ws_bytes, void* stream);
+/* Pass 2: SAT-test every candidate and emit fragments in (tri, x, y, z)
+ * order: coords (F,3) int32, tris (F,) int32.  *n_fragments (host) is set
+ * even when capacity is too small (then WFPG_ERR_CAPACITY and nothing is
+ * written).  Workspace: wfpg_voxelize_workspace_bytes(T, n_candidates). */
+int wfpg_voxelize_emit(const wfpg_scene* scene, const double* cube_lo, double side,
+                       int32_t resolution, int64_t n_candidates, int32_t* out_coords,
+                       int32_t* out_tris, int64_t capacity, int64_t* n_fragments,
+                       void* workspace, size_t ws_bytes, void* stream);
+
+/* svo.py:416-500 (build_octree).  Phase A sorts/uniques fragments and sizes
+ * the tree (host, synchronous: returns node count and level offsets in
+ * svo->level_off).  Phase B fills the caller-allocated node arrays and fits
+ * the dual normals (svo.py:139-173 cluster_normals, bit-exact). */
+size_t wfpg_svo_build_workspace_bytes(int64_t n_fragments, int32_t depth);
+int wfpg_svo_build_structure(wfpg_svo* svo, const int32_t* frag_coords, int64_t n_fragments,
+                             void* workspace, size_t ws_bytes, void* stream);
+int wfpg_svo_build_fill(wfpg_svo* svo, const int32_t* frag_tris, const double* tri_normals,
+                        int64_t n_fragments, uint64_t seed,
+                        void* workspace, size_t ws_bytes, void* stream);
+/* Debug/golden access to phase-A intermediates kept in the workspace. */
+int wfpg_svo_build_sorted(const void* workspace, int64_t n_fragments,
+                          const uint64_t** sorted_codes, const uint32_t** sort_perm);
+
+/* ------------------------------------------------------------------------ */
+/* Item 2 — exitance accumulation                                            */
+/* ------------------------------------------------------------------------ */
+
+/* _kernels.pyx:591-658 (descend_point/descend_kernel) -> node, present, deepest. */
+int wfpg_descend(const wfpg_svo* svo, const double* points, int64_t n,
+                 int32_t* out_node, uint8_t* out_present, int32_t* out_deepest, void* stream);
+
+/* svo.py:254-263 (accumulate_batch): deposits applied in input order.
+ * deterministic=1 reproduces np.add.at's sequential order (sort + segmented
+ * sum); 0 uses fp64 atomics. */
+size_t wfpg_accumulate_workspace_bytes(int64_t n);
+int wfpg_svo_accumulate(wfpg_svo* svo, const int32_t* leaf, const double* dirs,
+                        const double* rad, int64_t n, const int32_t* n_dev, int32_t deterministic,
+                        void* workspace, size_t ws_bytes, void* stream);
+
+/* svo.py:265-313 (propagate_up): full bottom-up recompute of mean_a/mean_b,
+ * bitwise equal to the reference's dirty-only update. */
+int wfpg_svo_propagate(wfpg_svo* svo, void* stream);
+
+/* wavefront.py:286-332 (update_exitance) over a finished pass. */
+size_t wfpg_update_exitance_workspace_bytes(int64_t n_paths, int32_t max_depth);
+int wfpg_update_exitance(wfpg_svo* svo, const wfpg_paths* paths, int32_t deterministic,
+                         int32_t* n_deposits_dev, void* workspace, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Item 3 — cone tracer                                                      */
+/* ------------------------------------------------------------------------ */
+
+/* _kernels.pyx:661-757 (trace_one/trace_kernel), _kernelshim.py:79-98.
+ * origin_stride = 0 broadcasts a single origin. out (n,3) RGB. */
+int wfpg_trace_cones(const wfpg_scene* scene, const wfpg_svo* svo, const double* origins,
+                     int32_t origin_stride, const double* dirs, int64_t n, double omega,
+                     double* out, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Item 4 — field / PDF generation, guided + product sampling, MIS           */
+/* ------------------------------------------------------------------------ */
+
+/* guiding.py:231-251 (generate_fields_batch) fused with guiding.py:293-309
+ * (GuideTables.fill_batch): one CTA per bin cone-traces the n x n octahedral
+ * grid, takes luminance, blurs (core.py:170-195), floors at epsilon and
+ * writes vals/row_sum/marg/total (+ block_sums in product mode).
+ * origins (B,3), jitters (B,2). n_bins_dev optional device count <= n_bins.
+ * blur_w: 2*blur_radius+1 taps (host), core._blur_kernel(sigma). */
+int wfpg_generate_fields(const wfpg_scene* scene, const wfpg_svo* svo, const double* origins,
+                         const double* jitters, int64_t n_bins, const int32_t* n_bins_dev,
+                         int32_t n, int32_t blur_radius, const double* blur_w /* host */,
+                         wfpg_guide* guide, void* stream);
+
+/* Materialise the reference's full GuideTables arrays (cond, pdftab and the
+ * product block CDFs) from a B200 guide, for parity checks. */
+int wfpg_guide_expand(const wfpg_guide* guide, int64_t n_bins, double* cond, double* pdftab,
+                      double* blk_marg, double* blk_cond, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Item 5 — wavefront stages                                                 */
+/* ------------------------------------------------------------------------ */
+
+/* _kernels.pyx:764-795 (camera_kernel). */
+int wfpg_camera_rays(const wfpg_camera* cam, const uint64_t* keys, const int64_t* pixels,
+                     int64_t n, double* out_o, double* out_d, void* stream);
+
+/* _kernels.pyx:502-527 (intersect_kernel); misses: t = +inf, tri = -1. */
+int wfpg_intersect(const wfpg_scene* scene, const double* origins, const double* dirs,
+                   int64_t n, double t_min, double* out_t, int32_t* out_tri, void* stream);
+
+/* _kernels.pyx:530-555 (occluded_kernel). */
+int wfpg_occluded(const wfpg_scene* scene, const double* origins, const double* dirs,
+                  int64_t n, double t_min, const double* t_max, uint8_t* out, void* stream);
+
+/* _kernels.pyx:905-1253 (shade_one/shade_kernel), _kernelshim.py:113-151.
+ * active (n_active,) path ids; bin_slot (P,) or NULL; guide may be NULL. */
+int wfpg_shade_depth(const wfpg_scene* scene, wfpg_paths* paths, int32_t depth,
+                     const int32_t* active, int64_t n_active, const int32_t* n_active_dev,
+                     const double* hit_t, const int32_t* hit_tri, const wfpg_guide* guide,
+                     const int32_t* bin_slot, int32_t rr_enabled, int32_t rr_depth, void* stream);
+
+/* wavefront.py:98-157 (partition_spatial, Alg. 2).  positions (n,3) of the
+ * lambert hits, path_idx (n,) ascending.  Outputs bins ordered by node id:
+ * bin_node (B,), bin_start (B,), bin_count (B,), members (n,) path ids
+ * grouped by bin, ascending within a bin; *n_bins_dev (device). */
+size_t wfpg_partition_workspace_bytes(int64_t n, int64_t n_nodes);
+int wfpg_partition_spatial(wfpg_svo* svo, const double* positions, const int32_t* path_idx,
+                           int64_t n, const int32_t* n_dev, int32_t l_min, int32_t c_ray,
+                           int32_t* bin_node, int32_t* bin_start, int32_t* bin_count,
+                           int32_t* members, int32_t* n_bins_dev, int64_t bin_capacity,
+                           void* workspace, size_t ws_bytes, void* stream);
+
+/* wavefront.py:198-277 (render_pass): the whole pass on the device.
+ * frame (H*W,3) receives the mean radiance of the pass; stats (host) is
+ * filled after the pass (one synchronisation). */
+size_t wfpg_render_workspace_bytes(const wfpg_scene* scene, const wfpg_svo* svo,
+                                   const wfpg_camera* cam, const wfpg_pass_config* cfg);
+int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camera* cam,
+                     const wfpg_pass_config* cfg, wfpg_paths* paths, double* frame,
+                     wfpg_pass_stats* stats, void* workspace, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WFPG_B200_H */

@@ -1,0 +1,289 @@
+// Ray casting device functions: brute-force nearest hit over a shared-memory
+// triangle pack (wfpg_brute_nearest, _kernels.pyx:40-97) and the BVH
+// traversals (bvh_nearest / bvh_occluded / tri_hit / box_near / box_hit,
+// _kernels.pyx:319-478).  Same acceptance tests and tie rules as the
+// reference: brute force keeps the minimum t with the lowest triangle id on
+// ties; BVH traversal visits children nearest-first with the same stacks.
+#pragma once
+#include "common.cuh"
+
+namespace wfpg {
+
+struct SceneView {
+  const double* v0;
+  const double* e1;
+  const double* e2;
+  const double* normals;
+  const int32_t* tri_mat;
+  const int32_t* mat_kind;
+  const double* mat_rgb;
+  const double* em_cdf;
+  const int32_t* em_tris;
+  int32_t n_emit;
+  double em_area;
+  double ray_eps;
+  int32_t n_tris;
+  int32_t brute;
+  const double* blo;
+  const double* bhi;
+  const int32_t* bleft;
+  const int32_t* bright;
+  const int32_t* bcount;
+  const int32_t* border;
+};
+
+inline SceneView make_scene_view(const wfpg_scene* s) {
+  SceneView v;
+  v.v0 = s->v0;
+  v.e1 = s->e1;
+  v.e2 = s->e2;
+  v.normals = s->normals;
+  v.tri_mat = s->tri_mat;
+  v.mat_kind = s->mat_kind;
+  v.mat_rgb = s->mat_rgb;
+  v.em_cdf = s->emitter_cdf;
+  v.em_tris = s->emitter_tris;
+  v.n_emit = s->n_emit;
+  v.em_area = s->emitter_area;
+  v.ray_eps = s->ray_eps;
+  v.n_tris = s->n_tris;
+  v.brute = s->brute;
+  v.blo = s->bvh_lo;
+  v.bhi = s->bvh_hi;
+  v.bleft = s->bvh_left;
+  v.bright = s->bvh_right;
+  v.bcount = s->bvh_count;
+  v.border = s->bvh_order;
+  return v;
+}
+
+// Triangle record in shared memory (9 doubles).
+struct TriRec {
+  double v0x, v0y, v0z, e1x, e1y, e1z, e2x, e2y, e2z;
+};
+
+constexpr int kMaxBruteTris = 512;
+
+// Cooperative load of the triangle pack into shared memory.
+__device__ __forceinline__ void load_tris_smem(const SceneView& s, TriRec* sm) {
+  for (int t = threadIdx.x; t < s.n_tris; t += blockDim.x) {
+    TriRec r;
+    r.v0x = s.v0[3 * t];
+    r.v0y = s.v0[3 * t + 1];
+    r.v0z = s.v0[3 * t + 2];
+    r.e1x = s.e1[3 * t];
+    r.e1y = s.e1[3 * t + 1];
+    r.e1z = s.e1[3 * t + 2];
+    r.e2x = s.e2[3 * t];
+    r.e2y = s.e2[3 * t + 1];
+    r.e2z = s.e2[3 * t + 2];
+    sm[t] = r;
+  }
+}
+
+// _kernels.pyx:63-81 for one triangle.  Returns t (>0) when accepted, else -1.
+__device__ __forceinline__ double mt_brute(const TriRec& T, double ox, double oy, double oz,
+                                           double dx, double dy, double dz, double tmin) {
+  double px = dy * T.e2z - dz * T.e2y;
+  double py = dz * T.e2x - dx * T.e2z;
+  double pz = dx * T.e2y - dy * T.e2x;
+  double det = T.e1x * px + T.e1y * py + T.e1z * pz;
+  double s = det > 0.0 ? 1.0 : -1.0;
+  double ad = det * s;
+  double tx = ox - T.v0x, ty = oy - T.v0y, tz = oz - T.v0z;
+  double us = (tx * px + ty * py + tz * pz) * s;
+  double qx = ty * T.e1z - tz * T.e1y;
+  double qy = tz * T.e1x - tx * T.e1z;
+  double qz = tx * T.e1y - ty * T.e1x;
+  double vs = (dx * qx + dy * qy + dz * qz) * s;
+  double ts = (T.e2x * qx + T.e2y * qy + T.e2z * qz) * s;
+  bool ok = (ad > 1e-300) & (us >= 0.0) & (vs >= 0.0) & (us + vs <= ad) & (ts > tmin * ad);
+  return ok ? ts / ad : -1.0;
+}
+
+__device__ __forceinline__ void brute_nearest(const TriRec* __restrict__ tris, int n, double ox,
+                                              double oy, double oz, double dx, double dy,
+                                              double dz, double tmin, double* bt, int32_t* bid) {
+  double best = 1e300;
+  int32_t id = -1;
+  for (int t = 0; t < n; ++t) {
+    double h = mt_brute(tris[t], ox, oy, oz, dx, dy, dz, tmin);
+    if (h > 0.0 && h < best) {  // accepted hits have ts/ad > tmin > 0
+      best = h;
+      id = t;
+    }
+  }
+  *bt = best;
+  *bid = id;
+}
+
+// _kernels.pyx:339-372
+__device__ __forceinline__ double tri_hit(const double* v0, const double* e1, const double* e2,
+                                          double ox, double oy, double oz, double dx, double dy,
+                                          double dz, double tmin, double tmax) {
+  double px = dy * e2[2] - dz * e2[1];
+  double py = dz * e2[0] - dx * e2[2];
+  double pz = dx * e2[1] - dy * e2[0];
+  double det = e1[0] * px + e1[1] * py + e1[2] * pz;
+  double ad = fabs(det);
+  if (ad <= 1e-300) return -1.0;
+  double s = det > 0.0 ? 1.0 : -1.0;
+  double tx = ox - v0[0], ty = oy - v0[1], tz = oz - v0[2];
+  double us = (tx * px + ty * py + tz * pz) * s;
+  if (us < 0.0 || us > ad) return -1.0;
+  double qx = ty * e1[2] - tz * e1[1];
+  double qy = tz * e1[0] - tx * e1[2];
+  double qz = tx * e1[1] - ty * e1[0];
+  double vs = (dx * qx + dy * qy + dz * qz) * s;
+  if (vs < 0.0 || us + vs > ad) return -1.0;
+  double ts = (e2[0] * qx + e2[1] * qy + e2[2] * qz) * s;
+  if (ts > tmin * ad && ts < tmax * ad) return ts / ad;
+  return -1.0;
+}
+
+__device__ __forceinline__ void slab(const double* lo, const double* hi, double ox, double oy,
+                                     double oz, double ix, double iy, double iz, double* tn,
+                                     double* tf) {
+  double t0 = (lo[0] - ox) * ix, t1 = (hi[0] - ox) * ix;
+  double n = fmin(t0, t1), f = fmax(t0, t1);
+  t0 = (lo[1] - oy) * iy;
+  t1 = (hi[1] - oy) * iy;
+  n = fmax(n, fmin(t0, t1));
+  f = fmin(f, fmax(t0, t1));
+  t0 = (lo[2] - oz) * iz;
+  t1 = (hi[2] - oz) * iz;
+  n = fmax(n, fmin(t0, t1));
+  f = fmin(f, fmax(t0, t1));
+  *tn = n;
+  *tf = f;
+}
+
+// _kernels.pyx:398-445
+__device__ __forceinline__ void bvh_nearest(const SceneView& b, double ox, double oy, double oz,
+                                            double dx, double dy, double dz, double tmin,
+                                            double* best_t, int32_t* best_tri) {
+  int32_t stack[64];
+  double dstack[64];
+  double ix = 1.0 / dx, iy = 1.0 / dy, iz = 1.0 / dz;
+  double bt = 1e300;
+  int32_t bid = -1;
+  stack[0] = 0;
+  dstack[0] = 0.0;
+  int sp = 1;
+  while (sp > 0) {
+    --sp;
+    if (dstack[sp] >= bt) continue;
+    int32_t node = stack[sp];
+    int32_t cnt = b.bcount[node];
+    if (cnt > 0) {
+      int32_t first = b.bleft[node];
+      for (int32_t k = first; k < first + cnt; ++k) {
+        int32_t tri = b.border[k];
+        double t = tri_hit(b.v0 + 3 * tri, b.e1 + 3 * tri, b.e2 + 3 * tri, ox, oy, oz, dx, dy, dz,
+                           tmin, bt);
+        if (t > 0.0) {
+          bt = t;
+          bid = tri;
+        }
+      }
+    } else {
+      int32_t c0 = b.bleft[node], c1 = b.bright[node];
+      double n0, f0, n1, f1;
+      slab(b.blo + 3 * c0, b.bhi + 3 * c0, ox, oy, oz, ix, iy, iz, &n0, &f0);
+      slab(b.blo + 3 * c1, b.bhi + 3 * c1, ox, oy, oz, ix, iy, iz, &n1, &f1);
+      double d0 = (f0 >= n0 && n0 <= bt && f0 >= tmin) ? n0 : 1e301;
+      double d1 = (f1 >= n1 && n1 <= bt && f1 >= tmin) ? n1 : 1e301;
+      if (d0 > d1) {
+        int32_t tn = c0;
+        c0 = c1;
+        c1 = tn;
+        double td = d0;
+        d0 = d1;
+        d1 = td;
+      }
+      if (d1 < 1e301 && sp < 64) {
+        stack[sp] = c1;
+        dstack[sp] = d1;
+        ++sp;
+      }
+      if (d0 < 1e301 && sp < 64) {
+        stack[sp] = c0;
+        dstack[sp] = d0;
+        ++sp;
+      }
+    }
+  }
+  *best_t = bt;
+  *best_tri = bid;
+}
+
+// _kernels.pyx:448-478
+__device__ __forceinline__ bool bvh_occluded(const SceneView& b, double ox, double oy, double oz,
+                                             double dx, double dy, double dz, double tmin,
+                                             double tmax) {
+  int32_t stack[64];
+  double ix = 1.0 / dx, iy = 1.0 / dy, iz = 1.0 / dz;
+  stack[0] = 0;
+  int sp = 1;
+  while (sp > 0) {
+    --sp;
+    int32_t node = stack[sp];
+    double n, f;
+    slab(b.blo + 3 * node, b.bhi + 3 * node, ox, oy, oz, ix, iy, iz, &n, &f);
+    if (!(f >= n && n <= tmax && f >= tmin)) continue;
+    int32_t cnt = b.bcount[node];
+    if (cnt > 0) {
+      int32_t first = b.bleft[node];
+      for (int32_t k = first; k < first + cnt; ++k) {
+        int32_t tri = b.border[k];
+        if (tri_hit(b.v0 + 3 * tri, b.e1 + 3 * tri, b.e2 + 3 * tri, ox, oy, oz, dx, dy, dz, tmin,
+                    tmax) > 0.0)
+          return true;
+      }
+    } else if (sp + 2 <= 64) {
+      stack[sp] = b.bleft[node];
+      stack[sp + 1] = b.bright[node];
+      sp += 2;
+    }
+  }
+  return false;
+}
+
+// Brute-force any-hit (wfpg_brute_occluded, _kernels.pyx:99-138).
+__device__ __forceinline__ bool brute_occluded(const TriRec* __restrict__ tris, int n, double ox,
+                                               double oy, double oz, double dx, double dy,
+                                               double dz, double tmin, double tmax) {
+  for (int t = 0; t < n; ++t) {
+    const TriRec& T = tris[t];
+    double px = dy * T.e2z - dz * T.e2y;
+    double py = dz * T.e2x - dx * T.e2z;
+    double pz = dx * T.e2y - dy * T.e2x;
+    double det = T.e1x * px + T.e1y * py + T.e1z * pz;
+    double s = det > 0.0 ? 1.0 : -1.0;
+    double ad = det * s;
+    double tx = ox - T.v0x, ty = oy - T.v0y, tz = oz - T.v0z;
+    double us = (tx * px + ty * py + tz * pz) * s;
+    double qx = ty * T.e1z - tz * T.e1y;
+    double qy = tz * T.e1x - tx * T.e1z;
+    double qz = tx * T.e1y - ty * T.e1x;
+    double vs = (dx * qx + dy * qy + dz * qz) * s;
+    double ts = (T.e2x * qx + T.e2y * qy + T.e2z * qz) * s;
+    if ((ad > 1e-300) & (us >= 0.0) & (vs >= 0.0) & (us + vs <= ad) & (ts > tmin * ad) &
+        (ts < tmax * ad))
+      return true;
+  }
+  return false;
+}
+
+// ray_nearest (_kernels.pyx:481-489): brute force for small scenes (tris in
+// shared memory), BVH otherwise.
+__device__ __forceinline__ void ray_nearest(const SceneView& s, const TriRec* smt, double ox,
+                                            double oy, double oz, double dx, double dy, double dz,
+                                            double tmin, double* bt, int32_t* bid) {
+  if (s.brute)
+    brute_nearest(smt, s.n_tris, ox, oy, oz, dx, dy, dz, tmin, bt, bid);
+  else
+    bvh_nearest(s, ox, oy, oz, dx, dy, dz, tmin, bt, bid);
+}
+
+}  // namespace wfpg

@@ -1,0 +1,75 @@
+// Cone query device function + internal SVO entry points.
+#pragma once
+#include "geometry.cuh"
+
+namespace wfpg {
+
+// Footprint-matched level (trace_one, _kernels.pyx:685-702): the level lv in
+// [0, depth] minimising |side_lv^2 - area| with deeper levels winning ties.
+// Because side_lv^2 is an exact power-of-4 scaling of side_0^2, the error is
+// unimodal in lv, so the level chosen over the materialised chain [0, L] of
+// the reference equals min(L, best) with best taken over [0, depth]; the
+// descent can therefore stop at `best` instead of walking to the leaf.
+__device__ __forceinline__ int best_cone_level(double size, int depth, double area) {
+  double s = size / (double)(1u << depth);
+  double bd = fabs(s * s - area);
+  int best = depth;
+  for (int lv = depth - 1; lv >= 0; --lv) {
+    s = size / (double)(1u << lv);
+    double diff = fabs(s * s - area);
+    if (diff < bd) {
+      bd = diff;
+      best = lv;
+    }
+  }
+  return best;
+}
+
+// Shade a hit point for a cone of solid angle omega: nudge toward the apex,
+// clamp into the cube, descend to the footprint level, return the exitance of
+// the side facing the cone scaled by |d.n| (_kernels.pyx:673-713).
+__device__ __forceinline__ void cone_shade_hit(const SvoView& v, double ox, double oy, double oz,
+                                               double dx, double dy, double dz, double r,
+                                               double omega, double* rgb) {
+  double nudge = (v.size / v.resolution) * 1e-3;
+  double tiny = v.size * 1e-12;
+  double qx = ox + r * dx - dx * nudge;
+  double qy = oy + r * dy - dy * nudge;
+  double qz = oz + r * dz - dz * nudge;
+  qx = fmin(fmax(qx, v.lox + tiny), v.lox + v.size - tiny);
+  qy = fmin(fmax(qy, v.loy + tiny), v.loy + v.size - tiny);
+  qz = fmin(fmax(qz, v.loz + tiny), v.loz + v.size - tiny);
+  int32_t ix = quantise(qx, v.lox, v.scale, v.resolution);
+  int32_t iy = quantise(qy, v.loy, v.scale, v.resolution);
+  int32_t iz = quantise(qz, v.loz, v.scale, v.resolution);
+  int target = best_cone_level(v.size, v.depth, r * r * omega);
+  bool pres;
+  int32_t lvl;
+  int32_t node = descend_coords(v.desc, v.depth, ix, iy, iz, target, &pres, &lvl);
+  const double* nn = v.normal + 3 * (int64_t)node;
+  double da = dx * __ldg(nn) + dy * __ldg(nn + 1) + dz * __ldg(nn + 2);
+  double w = fabs(da);
+  const double* m = (da <= 0.0 ? v.mean_a : v.mean_b) + 3 * (int64_t)node;
+  rgb[0] = __ldg(m) * w;
+  rgb[1] = __ldg(m + 1) * w;
+  rgb[2] = __ldg(m + 2) * w;
+}
+
+__device__ __forceinline__ void cone_query(const SceneView& s, const TriRec* smt, const SvoView& v,
+                                           double ox, double oy, double oz, double dx, double dy,
+                                           double dz, double omega, double* rgb) {
+  rgb[0] = rgb[1] = rgb[2] = 0.0;
+  double bt;
+  int32_t btri;
+  ray_nearest(s, smt, ox, oy, oz, dx, dy, dz, s.ray_eps, &bt, &btri);
+  if (btri < 0) return;
+  cone_shade_hit(v, ox, oy, oz, dx, dy, dz, bt, omega, rgb);
+}
+
+size_t accumulate_ws_bytes(int64_t n);
+int svo_accumulate(wfpg_svo* svo, const int32_t* leaf, const double* dirs, const double* rad,
+                   int64_t n, const int32_t* n_dev, int deterministic, Arena& ws,
+                   cudaStream_t st);
+int svo_propagate(wfpg_svo* svo, cudaStream_t st);
+
+}  // namespace wfpg

@@ -1,0 +1,424 @@
+"""Sparse voxel octree caching radiant exitance — device resident.
+
+Drop-in for the reference module svo.py: same functions, classes, array
+names and dtypes.  The node arrays live in HBM (torch tensors as raw CUDA
+allocations); every build / query / update is a CUDA kernel behind the C ABI
+(include/wfpg_b200.h).  Host numpy copies of the arrays are produced on
+attribute access, so reference-style inspection (``svo.codes``,
+``svo.normal[...]``) keeps working; assigning a whole array uploads it.
+
+Reference map: voxelize svo.py:94-136, build_octree :416-500,
+cluster_normals :139-173, SvoCache :176-397.
+"""
+
+import struct
+
+import numpy as np
+
+from . import _dev, _lib
+
+DUMP_MAGIC = b"WFPGSVO1"
+DUMP_VERSION = 1
+
+# bytes per node for the memory accounting log (svo.py:20-22): morton code,
+# child base, child mask, normal, two RGB sums, two weights, ray counter
+NODE_RECORD_BYTES = 8 + 8 + 1 + 24 + 48 + 16 + 8
+
+
+class VoxelFragments:
+    """Conservative (voxel, triangle) overlap pairs (host arrays)."""
+
+    __slots__ = ("coords", "normals", "tris")
+
+    def __init__(self, coords, normals, tris):
+        self.coords = coords
+        self.normals = normals
+        self.tris = tris
+
+    def __len__(self):
+        return len(self.coords)
+
+
+def scene_cube(scene, pad=1e-4):
+    """Padded cubic bound around the scene (svo.py:39-46)."""
+    lo, hi = scene.bbox_lo, scene.bbox_hi
+    center = 0.5 * (lo + hi)
+    side = float((hi - lo).max()) * (1.0 + pad)
+    return center - 0.5 * side, side
+
+
+def _check_resolution(resolution):
+    r = int(resolution)
+    if r <= 0 or (r & (r - 1)) != 0:
+        raise ValueError("resolution must be a positive power of two")
+    return r
+
+
+def _voxelize_device(scene, resolution):
+    """Device voxelisation; returns (coords int32 (F,3), tris int32 (F,)) tensors."""
+    r = _check_resolution(resolution)
+    cube_lo, side = scene_cube(scene)
+    lo = np.ascontiguousarray(cube_lo, dtype=np.float64)
+    lo_p = lo.ctypes.data_as(_lib.c_vp)
+    st = _dev.stream()
+    sc = scene.abi()
+    ws = _dev.workspace(_lib.load().wfpg_voxelize_workspace_bytes(scene.triangle_count, 0))
+    n_cand = _lib.c_i64(0)
+    _lib.call("wfpg_voxelize_count", _lib.C.byref(sc), lo_p, side, r, _lib.C.byref(n_cand),
+              _lib.ptr(ws), ws.numel(), st)
+    c = n_cand.value
+    ws = _dev.workspace(_lib.load().wfpg_voxelize_workspace_bytes(scene.triangle_count, c))
+    coords = _dev.empty((max(c, 1), 3), np.int32)
+    tris = _dev.empty((max(c, 1),), np.int32)
+    n_frag = _lib.c_i64(0)
+    _lib.call("wfpg_voxelize_emit", _lib.C.byref(sc), lo_p, side, r, c, _lib.ptr(coords),
+              _lib.ptr(tris), c, _lib.C.byref(n_frag), _lib.ptr(ws), ws.numel(), st)
+    f = n_frag.value
+    return coords[:f], tris[:f]
+
+
+def voxelize(scene, resolution):
+    """Conservative voxelisation (svo.py:94-136) computed on the device.
+
+    Fragments come out in (triangle, x, y, z) order with the triangle's
+    geometric normal, exactly as the reference emits them."""
+    coords, tris = _voxelize_device(scene, resolution)
+    if coords.shape[0] == 0:
+        return VoxelFragments(np.zeros((0, 3), dtype=np.int64), np.zeros((0, 3)),
+                              np.zeros(0, dtype=np.int64))
+    t = _dev.download(tris).astype(np.int64)
+    return VoxelFragments(_dev.download(coords).astype(np.int64),
+                          scene.normals[t].copy(), t)
+
+
+def cluster_normals(normals, rng):
+    """Antipodal dual-normal fit (svo.py:139-173) for one small normal set.
+
+    Host helper for API parity; the builder runs the same k-means on the
+    device for every node that needs it."""
+    normals = np.asarray(normals, dtype=np.float64)
+    if len(normals) == 0:
+        raise ValueError("cluster_normals needs at least one normal")
+    k = len(normals)
+    pick = min(int(rng.next() * k), k - 1)
+    ma = normals[pick].copy()
+    mb = -ma
+    prev = None
+    for _ in range(32):
+        side = normals @ ma >= normals @ mb
+        if prev is not None and np.array_equal(side, prev):
+            break
+        prev = side
+        sa = normals[side].sum(axis=0)
+        sb = normals[~side].sum(axis=0)
+        na, nb = np.linalg.norm(sa), np.linalg.norm(sb)
+        if na > 1e-12:
+            ma = sa / na
+        mb = sb / nb if nb > 1e-12 else -ma
+    return ma, -ma
+
+
+_ARRAYS = {
+    # name: (numpy dtype on the host API, device dtype, components)
+    "codes": (np.uint64, np.uint64, 1),
+    "child_base": (np.int64, np.int32, 1),
+    "child_mask": (np.uint8, np.uint8, 1),
+    "parent": (np.int64, np.int32, 1),
+    "normal": (np.float64, np.float64, 3),
+    "sum_a": (np.float64, np.float64, 3),
+    "sum_b": (np.float64, np.float64, 3),
+    "weight_a": (np.float64, np.float64, 1),
+    "weight_b": (np.float64, np.float64, 1),
+    "mean_a": (np.float64, np.float64, 3),
+    "mean_b": (np.float64, np.float64, 3),
+    "counter": (np.int64, np.int32, 1),
+}
+
+
+class SvoCache:
+    """Level-grouped node arrays in HBM; level 0 is the root, level ``depth``
+    the leaves; node ids index the flat arrays (svo.py:176-224)."""
+
+    def __init__(self, resolution, cube_lo, cube_size):
+        self.resolution = int(resolution)
+        self.depth = int(np.log2(self.resolution))
+        self.cube_lo = np.asarray(cube_lo, dtype=np.float64)
+        self.cube_size = float(cube_size)
+        self.level_off = None
+        self._d = {}
+        self._abi = None
+
+    # -- device storage -----------------------------------------------------
+
+    def _alloc(self, n):
+        d = {}
+        for name, (_, ddt, comp) in _ARRAYS.items():
+            shape = (n, comp) if comp > 1 else (n,)
+            d[name] = _dev.zeros(shape, ddt)
+        d["node_desc"] = _dev.zeros((n, 2), np.uint32)
+        self._d = d
+        self._abi = None
+
+    def dev(self, name):
+        return self._d[name]
+
+    def abi(self):
+        s = _lib.Svo()
+        s.depth = self.depth
+        s.resolution = self.resolution
+        s.n_nodes = 0 if self.level_off is None else int(self.level_off[-1])
+        s.lo[:] = self.cube_lo.tolist()
+        s.size = self.cube_size
+        if self.level_off is not None:
+            for i, v in enumerate(self.level_off):
+                s.level_off[i] = int(v)
+        for name in list(_ARRAYS) + ["node_desc"]:
+            if name in self._d:
+                setattr(s, name, self._d[name].data_ptr())
+        self._abi = s
+        return s
+
+    def __getattr__(self, name):
+        if name in _ARRAYS:
+            d = self.__dict__.get("_d", {})
+            if name not in d:
+                return None
+            host_dt = _ARRAYS[name][0]
+            return _dev.download(d[name]).astype(host_dt, copy=False)
+        raise AttributeError(name)
+
+    def __setattr__(self, name, value):
+        if name in _ARRAYS and value is not None and "_d" in self.__dict__ and self._d:
+            dev_dt = _ARRAYS[name][1]
+            arr = np.asarray(value)
+            self._d[name].copy_(_dev.upload(arr.reshape(self._d[name].shape).astype(dev_dt)))
+            return
+        object.__setattr__(self, name, value)
+
+    # -- structure ---------------------------------------------------------
+
+    @property
+    def node_count(self):
+        return int(self.level_off[-1])
+
+    @property
+    def leaf_count(self):
+        return int(self.level_off[self.depth + 1] - self.level_off[self.depth])
+
+    def level_of(self, node_id):
+        return int(np.searchsorted(self.level_off, node_id, side="right") - 1)
+
+    def level_slice(self, level):
+        return slice(int(self.level_off[level]), int(self.level_off[level + 1]))
+
+    def voxel_side(self, level):
+        return self.cube_size / (1 << level)
+
+    def memory_bytes(self):
+        return self.node_count * NODE_RECORD_BYTES
+
+    def point_to_leaf_coords(self, positions):
+        positions = np.atleast_2d(np.asarray(positions, dtype=np.float64))
+        q = np.floor((positions - self.cube_lo) / self.cube_size * self.resolution)
+        return np.clip(q, 0, self.resolution - 1).astype(np.int64)
+
+    # -- queries -----------------------------------------------------------
+
+    def descend_device(self, points):
+        """points: (n,3) float64 device tensor -> (node, present, deepest) tensors."""
+        n = points.shape[0]
+        node = _dev.empty((max(n, 1),), np.int32)
+        pres = _dev.empty((max(n, 1),), np.uint8)
+        deep = _dev.empty((max(n, 1),), np.int32)
+        _lib.call("wfpg_descend", _lib.C.byref(self.abi()), _lib.ptr(points), n, _lib.ptr(node),
+                  _lib.ptr(pres), _lib.ptr(deep), _dev.stream())
+        return node[:n], pres[:n], deep[:n]
+
+    def descend_tracked(self, positions):
+        p = _dev.upload(np.atleast_2d(np.asarray(positions, dtype=np.float64)))
+        node, pres, deep = self.descend_device(p)
+        return (_dev.download(node).astype(np.int64), _dev.download(pres).astype(bool),
+                _dev.download(deep).astype(np.int64))
+
+    def descend_leaf(self, position):
+        """Leaf id containing ``position`` or -1; outside the cube is an error."""
+        p = np.asarray(position, dtype=np.float64)
+        if np.any(p < self.cube_lo) or np.any(p > self.cube_lo + self.cube_size):
+            raise ValueError("position outside the scene bounding cube")
+        return int(self.descend_batch(p[None, :])[0])
+
+    def descend_batch(self, positions):
+        node, present, _ = self.descend_tracked(positions)
+        return np.where(present, node, -1)
+
+    def accumulate_exitance(self, node_id, direction, radiance):
+        """Deposit one outgoing-radiance estimate on the facing side."""
+        self.accumulate_batch(np.array([node_id], dtype=np.int64),
+                              np.asarray(direction, dtype=np.float64)[None, :],
+                              np.asarray(radiance, dtype=np.float64)[None, :])
+
+    def accumulate_device(self, leaf, dirs, rad, n=None, n_dev=None, deterministic=True):
+        n = leaf.shape[0] if n is None else n
+        ws = _dev.workspace(_lib.load().wfpg_accumulate_workspace_bytes(n))
+        _lib.call("wfpg_svo_accumulate", _lib.C.byref(self.abi()), _lib.ptr(leaf),
+                  _lib.ptr(dirs), _lib.ptr(rad), n, _lib.ptr(n_dev), 1 if deterministic else 0,
+                  _lib.ptr(ws), ws.numel(), _dev.stream())
+
+    def accumulate_batch(self, node_ids, directions, radiances, deterministic=True):
+        """Deposits applied in input (path) order, like np.add.at (svo.py:254-263)."""
+        node_ids = np.asarray(node_ids, dtype=np.int64)
+        if len(node_ids):
+            self.accumulate_device(_dev.upload(node_ids, np.int32),
+                                   _dev.upload(directions, np.float64),
+                                   _dev.upload(radiances, np.float64),
+                                   deterministic=deterministic)
+        return np.unique(node_ids)
+
+    def propagate_up(self, dirty_leaves=None):
+        """Refresh mean_a/mean_b bottom-up (svo.py:265-313).
+
+        The device recomputes every node; internal means are pure functions
+        of the leaf means, so this equals the reference's dirty-only update
+        bit for bit.  ``dirty_leaves`` is accepted for API
+        parity; an empty list is a no-op as in the reference."""
+        if dirty_leaves is not None and len(dirty_leaves) == 0:
+            return
+        _lib.call("wfpg_svo_propagate", _lib.C.byref(self.abi()), _dev.stream())
+
+    def cone_trace(self, scene, origin, direction, aperture):
+        """Radiance arriving at ``origin`` from a cone of solid angle ``aperture``."""
+        from . import backend_cuda
+
+        rgb = backend_cuda.trace_cones(self, scene, np.asarray(origin, dtype=np.float64),
+                                       np.asarray(direction, dtype=np.float64)[None, :],
+                                       float(aperture))
+        return rgb[0]
+
+    def ancestor_chain(self, leaf_coords):
+        """Node ids from the root to the deepest materialised node containing
+        the given leaf-grid coordinate (svo.py:326-340)."""
+        x, y, z = (int(c) for c in leaf_coords)
+        if min(x, y, z) < 0 or max(x, y, z) >= (1 << 21):
+            raise ValueError("morton coordinates must be within 21 bits")
+        mask = self.child_mask
+        base = self.child_base
+        node = int(self.level_off[0])
+        chain = [node]
+        for level in range(1, self.depth + 1):
+            sh = self.depth - level
+            octant = ((x >> sh) & 1) | (((y >> sh) & 1) << 1) | (((z >> sh) & 1) << 2)
+            m = int(mask[node])
+            if not (m >> octant) & 1:
+                break
+            node = int(base[node]) + bin(m & ((1 << octant) - 1)).count("1")
+            chain.append(node)
+        return chain
+
+    # -- dump / load (WFPGSVO1) -----------------------------------------------
+
+    def dump(self, path):
+        """Versioned little-endian binary dump (svo.py:344-362)."""
+        with open(path, "wb") as fh:
+            fh.write(DUMP_MAGIC)
+            fh.write(struct.pack("<IIQ", DUMP_VERSION, self.resolution, self.node_count))
+            fh.write(struct.pack("<3dd", *self.cube_lo, self.cube_size))
+            fh.write(np.asarray(self.level_off).astype("<i8").tobytes())
+            for name, dt in (("codes", "<u8"), ("child_base", "<i8"), ("child_mask", "u1"),
+                             ("parent", "<i8"), ("normal", "<f8"), ("sum_a", "<f8"),
+                             ("sum_b", "<f8"), ("weight_a", "<f8"), ("weight_b", "<f8")):
+                fh.write(np.ascontiguousarray(getattr(self, name), dtype=dt).tobytes())
+
+    @classmethod
+    def load_dump(cls, path):
+        with open(path, "rb") as fh:
+            if fh.read(8) != DUMP_MAGIC:
+                raise ValueError("not an SVO dump")
+            version, resolution, n = struct.unpack("<IIQ", fh.read(16))
+            if version != DUMP_VERSION:
+                raise ValueError(f"unsupported dump version {version}")
+            lo = struct.unpack("<3d", fh.read(24))
+            (size,) = struct.unpack("<d", fh.read(8))
+            svo = cls(resolution, np.array(lo), size)
+            svo.level_off = np.frombuffer(fh.read(8 * (svo.depth + 2)), dtype="<i8").copy()
+
+            def take(dt, shape):
+                cnt = int(np.prod(shape))
+                return np.frombuffer(fh.read(cnt * np.dtype(dt).itemsize), dtype=dt).reshape(shape)
+
+            host = {
+                "codes": take("<u8", (n,)), "child_base": take("<i8", (n,)),
+                "child_mask": take("u1", (n,)), "parent": take("<i8", (n,)),
+                "normal": take("<f8", (n, 3)), "sum_a": take("<f8", (n, 3)),
+                "sum_b": take("<f8", (n, 3)), "weight_a": take("<f8", (n,)),
+                "weight_b": take("<f8", (n,)),
+            }
+        svo._alloc(n)
+        for k, v in host.items():
+            setattr(svo, k, v)
+        desc = np.stack([host["child_base"].astype(np.int64) & 0xFFFFFFFF,
+                         host["child_mask"].astype(np.int64)], axis=1).astype(np.uint32)
+        svo._d["node_desc"].copy_(_dev.upload(desc))
+        svo.propagate_up()
+        return svo
+
+
+def _build(frag_coords, frag_tris, tri_normals, cube_lo, cube_size, resolution, seed):
+    """Device build from device fragment arrays (int32 coords (F,3), int32
+    tri index (F,), fp64 normals indexed by tri)."""
+    resolution = _check_resolution(resolution)
+    f = int(frag_coords.shape[0])
+    if f == 0:
+        raise ValueError("cannot build an octree from an empty fragment list")
+    svo = SvoCache(resolution, cube_lo, cube_size)
+    lib = _lib.load()
+    ws = _dev.workspace(lib.wfpg_svo_build_workspace_bytes(f, svo.depth))
+    st = _dev.stream()
+    s = svo.abi()
+    _lib.call("wfpg_svo_build_structure", _lib.C.byref(s), _lib.ptr(frag_coords), f,
+              _lib.ptr(ws), ws.numel(), st)
+    svo.level_off = np.array([s.level_off[i] for i in range(svo.depth + 2)], dtype=np.int64)
+    svo._alloc(svo.node_count)
+    s = svo.abi()
+    _lib.call("wfpg_svo_build_fill", _lib.C.byref(s), _lib.ptr(frag_tris), _lib.ptr(tri_normals),
+              f, int(seed) & 0xFFFFFFFFFFFFFFFF, _lib.ptr(ws), ws.numel(), st)
+    svo._build_ws = ws  # keeps sorted codes / permutation inspectable until the next build
+    svo._n_frag = f
+    return svo
+
+
+def sorted_fragments(svo):
+    """(sorted Morton codes, stable sort permutation) of the last build, as numpy."""
+    codes_p = _lib.c_vp()
+    perm_p = _lib.c_vp()
+    _lib.call("wfpg_svo_build_sorted", _lib.ptr(svo._build_ws), svo._n_frag,
+              _lib.C.byref(codes_p), _lib.C.byref(perm_p))
+    t = _dev.torch()
+    base = svo._build_ws.data_ptr()
+    f = svo._n_frag
+    ws = svo._build_ws
+    co = (codes_p.value - base)
+    po = (perm_p.value - base)
+    codes = ws[co:co + 8 * f].view(t.int64).cpu().numpy().view(np.uint64)
+    perm = ws[po:po + 4 * f].view(t.int32).cpu().numpy().astype(np.int64)
+    return codes, perm
+
+
+def build_octree(fragments, cube_lo, cube_size, resolution, seed=0):
+    """Morton-sort the fragments, materialise the levels bottom-up and fit the
+    dual normals (svo.py:416-500) — on the device."""
+    if len(fragments) == 0:
+        raise ValueError("cannot build an octree from an empty fragment list")
+    coords = np.asarray(fragments.coords)
+    if coords.min() < 0 or coords.max() >= (1 << 21):
+        raise ValueError("morton coordinate exceeds 21 bits")
+    f = len(fragments)
+    return _build(_dev.upload(coords, np.int32), _dev.upload(np.arange(f), np.int32),
+                  _dev.upload(fragments.normals, np.float64), cube_lo, cube_size, resolution,
+                  seed)
+
+
+def build_from_scene(scene, resolution, seed=0):
+    """Voxelise + build entirely on the device (no host round trip)."""
+    coords, tris = _voxelize_device(scene, resolution)
+    cube_lo, side = scene_cube(scene)
+    return _build(coords, tris, scene.device()["normals"], cube_lo, side, resolution, seed)
