@@ -145,6 +145,7 @@ typedef struct wfpg_guide {
   double* total;             /* (B,)    */
   double* block_sums;        /* (B,8,8) product mode (else may be NULL) */
   const int32_t* n_bins;     /* device count of valid slots */
+  const double* upper_dirs;  /* (8,8,3) product-layer cell centres (guiding.UPPER_DIRS) */
 } wfpg_guide;
 
 /* Knobs of one render pass: wavefront.py:21-50 (GuidingConfig). */
@@ -166,6 +167,7 @@ typedef struct wfpg_pass_config {
   int32_t deterministic;     /* 1: exitance splat in path order (np.add.at) */
   int32_t blur_radius;       /* core._blur_kernel radius (0: no blur) */
   double blur_w[33];         /* normalised blur taps, computed by numpy on the host */
+  const double* upper_dirs;  /* device (8,8,3) guiding.UPPER_DIRS, product mode only */
 } wfpg_pass_config;
 
 /* Per-pass statistics returned to the host: wavefront.py:81-85 (PassStats). */
@@ -286,6 +288,11 @@ int wfpg_generate_fields(const wfpg_scene* scene, const wfpg_svo* svo, const dou
                          const double* jitters, int64_t n_bins, const int32_t* n_bins_dev,
                          int32_t n, int32_t blur_radius, const double* blur_w /* host */,
                          wfpg_guide* guide, void* stream);
+
+/* guiding.py:293-309 (GuideTables.fill_batch) for caller-provided floored
+ * values already stored in guide->vals: row sums, marginal CDF, totals and
+ * (product) block sums. */
+int wfpg_guide_fill(wfpg_guide* guide, int64_t n_bins, void* stream);
 
 /* Materialise the reference's full GuideTables arrays (cond, pdftab and the
  * product block CDFs) from a B200 guide, for parity checks. */

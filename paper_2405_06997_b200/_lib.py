@@ -67,7 +67,7 @@ class Guide(C.Structure):
     _fields_ = [
         ("mode", c_i32), ("n", c_i32), ("capacity", c_i32), ("eps", c_dbl),
         ("vals", c_vp), ("row_sum", c_vp), ("marg", c_vp), ("total", c_vp),
-        ("block_sums", c_vp), ("n_bins", c_vp),
+        ("block_sums", c_vp), ("n_bins", c_vp), ("upper_dirs", c_vp),
     ]
 
 
@@ -79,7 +79,7 @@ class PassConfig(C.Structure):
         ("russian_roulette", c_i32), ("rr_depth", c_i32),
         ("seed", c_u64), ("sample_index", c_i64), ("n_samples", c_i32),
         ("deterministic", c_i32),
-        ("blur_radius", c_i32), ("blur_w", c_dbl * 33),
+        ("blur_radius", c_i32), ("blur_w", c_dbl * 33), ("upper_dirs", c_vp),
     ]
 
 
@@ -121,6 +121,7 @@ _SIGS = {
     "wfpg_trace_cones": (c_i32, [P(Scene), P(Svo), c_vp, c_i32, c_vp, c_i64, c_dbl, c_vp, c_vp]),
     "wfpg_generate_fields": (c_i32, [P(Scene), P(Svo), c_vp, c_vp, c_i64, c_vp, c_i32,
                                      c_i32, P(c_dbl), P(Guide), c_vp]),
+    "wfpg_guide_fill": (c_i32, [P(Guide), c_i64, c_vp]),
     "wfpg_guide_expand": (c_i32, [P(Guide), c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "wfpg_camera_rays": (c_i32, [P(Camera), c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "wfpg_intersect": (c_i32, [P(Scene), c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp, c_vp]),

@@ -1,0 +1,382 @@
+// Item 4 — per-bin radiance fields and their sampling tables, one CTA per
+// bin (guiding.py:231-251 generate_fields_batch fused with guiding.py:293-309
+// GuideTables.fill_batch).  The CTA cone-traces the n x n equal-area
+// octahedral grid straight into shared memory, takes the luminance, applies
+// the fold-aware separable Gaussian (core.py:156-195) in place, floors at
+// epsilon, and writes the floored values plus row sums, marginal CDF, total
+// and (product mode) 8x8 block sums.  The blur, sums and CDFs use the
+// reference's numpy operation order, so given identical cone values the
+// tables are bit-identical.
+#include "fields.cuh"
+#include "prims.cuh"
+#include "shade.cuh"
+#include "svo_query.cuh"
+
+namespace wfpg {
+
+// fold (core.py:156-167): reflect until inside, toggling the mirror flag
+__device__ __forceinline__ int fold_index(int raw, int n, bool* flip) {
+  bool f = false;
+  while (raw < 0 || raw >= n) {
+    raw = raw < 0 ? -1 - raw : 2 * n - 1 - raw;
+    f = !f;
+  }
+  *flip = f;
+  return raw;
+}
+
+template <int N>
+struct FieldCfg {
+  static constexpr int kStride = N + 1;  // padded rows: conflict-free column walks
+  static constexpr int kThreads = N >= 128 ? 512 : (N >= 64 ? 512 : (N >= 16 ? 256 : 128));
+  static constexpr int kPerLane = (N + 31) / 32;
+};
+
+template <int N>
+__device__ void blur_rows(double* F, const BlurParams& bp) {
+  constexpr int S = FieldCfg<N>::kStride;
+  constexpr int PL = FieldCfg<N>::kPerLane;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int r = bp.radius;
+  for (int j = warp; j < N / 2; j += nw) {
+    const int jp = N - 1 - j;
+    double oa[PL], ob[PL];
+#pragma unroll
+    for (int q = 0; q < PL; ++q) {
+      int i = lane + 32 * q;
+      double a = 0.0, b = 0.0;
+      if (i < N) {
+        for (int k = 0; k <= 2 * r; ++k) {
+          bool f;
+          int c = fold_index(i + k - r, N, &f);
+          double w = bp.w[k];
+          double sa = f ? F[jp * S + c] : F[j * S + c];
+          double sb = f ? F[j * S + c] : F[jp * S + c];
+          a = __dadd_rn(a, __dmul_rn(w, sa));
+          b = __dadd_rn(b, __dmul_rn(w, sb));
+        }
+      }
+      oa[q] = a;
+      ob[q] = b;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < PL; ++q) {
+      int i = lane + 32 * q;
+      if (i < N) {
+        F[j * S + i] = oa[q];
+        F[jp * S + i] = ob[q];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <int N>
+__device__ void blur_cols(double* F, const BlurParams& bp) {
+  constexpr int S = FieldCfg<N>::kStride;
+  constexpr int PL = FieldCfg<N>::kPerLane;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int r = bp.radius;
+  for (int i = warp; i < N / 2; i += nw) {
+    const int ip = N - 1 - i;
+    double oa[PL], ob[PL];
+#pragma unroll
+    for (int q = 0; q < PL; ++q) {
+      int j = lane + 32 * q;
+      double a = 0.0, b = 0.0;
+      if (j < N) {
+        for (int k = 0; k <= 2 * r; ++k) {
+          bool f;
+          int rr = fold_index(j + k - r, N, &f);
+          double w = bp.w[k];
+          double sa = f ? F[rr * S + ip] : F[rr * S + i];
+          double sb = f ? F[rr * S + i] : F[rr * S + ip];
+          a = __dadd_rn(a, __dmul_rn(w, sa));
+          b = __dadd_rn(b, __dmul_rn(w, sb));
+        }
+      }
+      oa[q] = a;
+      ob[q] = b;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < PL; ++q) {
+      int j = lane + 32 * q;
+      if (j < N) {
+        F[j * S + i] = oa[q];
+        F[j * S + ip] = ob[q];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(FieldCfg<N>::kThreads)
+    k_fields(SceneView s, SvoView v, const double* __restrict__ origins,
+             const double* __restrict__ jitters, int64_t nb_max, const int32_t* __restrict__ nb_dev,
+             BlurParams bp, FieldOut out) {
+  constexpr int S = FieldCfg<N>::kStride;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* F = reinterpret_cast<double*>(smem_raw);
+  double* rs = F + N * S;  // row sums (N)
+  TriRec* smt = reinterpret_cast<TriRec*>(rs + N);
+  if (s.brute) load_tris_smem(s, smt);
+  __syncthreads();
+  const int64_t nb = dev_count(nb_max, nb_dev);
+  const double omega = 4.0 * WFPG_PI / (double)(N * N);  // guiding.py:246
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const double ox = origins[3 * b], oy = origins[3 * b + 1], oz = origins[3 * b + 2];
+    const double ju = __ddiv_rn(jitters[2 * b], (double)N);
+    const double jv = __ddiv_rn(jitters[2 * b + 1], (double)N);
+    // 1. cone-trace every cell: u = i/n + ju/n, v = j/n + jv/n (guiding.py:239-244)
+    for (int c = threadIdx.x; c < N * N; c += blockDim.x) {
+      const int j = c / N, i = c % N;
+      double u = __dadd_rn(__ddiv_rn((double)i, (double)N), ju);
+      double w = __dadd_rn(__ddiv_rn((double)j, (double)N), jv);
+      double dx, dy, dz;
+      octa_uv_to_dir_np(u, w, &dx, &dy, &dz);
+      double rgb[3];
+      cone_query(s, smt, v, ox, oy, oz, dx, dy, dz, omega, rgb);
+      F[j * S + i] = luminance_rows(rgb[0], rgb[1], rgb[2]);
+    }
+    __syncthreads();
+    // 2. fold-aware separable blur, horizontal then vertical (core.py:185-195)
+    if (bp.radius > 0) {
+      blur_rows<N>(F, bp);
+      __syncthreads();
+      blur_cols<N>(F, bp);
+      __syncthreads();
+    }
+    // 3. epsilon floor + store values (coalesced)
+    double* gv = out.vals + b * (int64_t)N * N;
+    for (int c = threadIdx.x; c < N * N; c += blockDim.x) {
+      const int j = c / N, i = c % N;
+      double x = F[j * S + i];
+      x = x < out.eps ? out.eps : x;
+      F[j * S + i] = x;
+      gv[c] = x;
+    }
+    __syncthreads();
+    // 4. row sums (0 + pairwise), then total / marginal CDF (guiding.py:296-298)
+    for (int j = threadIdx.x; j < N; j += blockDim.x) {
+      double r = __dadd_rn(0.0, pairwise_row(F + j * S, N));
+      rs[j] = r;
+      out.row_sum[b * N + j] = r;
+    }
+    if (out.block_sums) {
+      constexpr int M = N / 8;
+      for (int q = threadIdx.x; q < 64; q += blockDim.x) {
+        const int bj = q / 8, bi = q % 8;
+        double acc = 0.0;
+        for (int r = 0; r < M; ++r)
+          acc = __dadd_rn(acc, __dadd_rn(0.0, pairwise_row(F + (bj * M + r) * S + bi * M, M)));
+        out.block_sums[b * 64 + q] = acc;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = __dadd_rn(0.0, pairwise_row(rs, N));
+      out.total[b] = tot;
+      double run = 0.0;
+      for (int j = 0; j < N; ++j) {
+        run = j == 0 ? rs[0] : __dadd_rn(run, rs[j]);
+        out.marg[b * N + j] = __ddiv_rn(run, tot);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int N>
+static int launch_fields_n(const SceneView& s, const SvoView& v, const double* origins,
+                           const double* jitters, int64_t nb_max, const int32_t* nb_dev,
+                           const BlurParams& bp, const FieldOut& out, cudaStream_t st) {
+  constexpr int T = FieldCfg<N>::kThreads;
+  size_t smem = sizeof(double) * (N * FieldCfg<N>::kStride + N) +
+                (s.brute ? sizeof(TriRec) * s.n_tris : 0);
+  static bool configured = false;
+  if (!configured) {
+    WFPG_CUDA(cudaFuncSetAttribute(k_fields<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   227 * 1024));
+    configured = true;
+  }
+  int per_sm = 0;
+  WFPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fields<N>, T, smem));
+  if (per_sm < 1) {
+    set_error("fields: kernel does not fit (smem %zu)", smem);
+    return WFPG_ERR_ARG;
+  }
+  int64_t grid = std::min<int64_t>(nb_max, (int64_t)kNumSMs * per_sm);
+  if (grid < 1) return WFPG_OK;
+  k_fields<N><<<(unsigned)grid, T, smem, st>>>(s, v, origins, jitters, nb_max, nb_dev, bp, out);
+  WFPG_CHECK_LAUNCH("k_fields");
+  return WFPG_OK;
+}
+
+int launch_fields(const SceneView& s, const SvoView& v, const double* origins,
+                  const double* jitters, int64_t nb_max, const int32_t* nb_dev, int n,
+                  const BlurParams& bp, const FieldOut& out, cudaStream_t st) {
+  if (nb_max <= 0) return WFPG_OK;
+  switch (n) {
+    case 8: return launch_fields_n<8>(s, v, origins, jitters, nb_max, nb_dev, bp, out, st);
+    case 16: return launch_fields_n<16>(s, v, origins, jitters, nb_max, nb_dev, bp, out, st);
+    case 32: return launch_fields_n<32>(s, v, origins, jitters, nb_max, nb_dev, bp, out, st);
+    case 64: return launch_fields_n<64>(s, v, origins, jitters, nb_max, nb_dev, bp, out, st);
+    case 128: return launch_fields_n<128>(s, v, origins, jitters, nb_max, nb_dev, bp, out, st);
+    default:
+      set_error("field resolution must be one of 8, 16, 32, 64, 128 (got %d)", n);
+      return WFPG_ERR_ARG;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// reference-layout tables (GuideTables.fill_batch) for parity checks
+// ---------------------------------------------------------------------------
+__global__ void k_guide_expand(GuideView g, int64_t nb, double* cond, double* pdftab,
+                               double* blk_marg, double* blk_cond) {
+  const int n = g.n, m = g.m;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nb * n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t b = r / n;
+    const double* row = g.vals + r * n;
+    double rsum = g.row_sum[r];
+    double run = 0.0;
+    for (int i = 0; i < n; ++i) {
+      run = i == 0 ? row[0] : __dadd_rn(run, row[i]);
+      if (cond) cond[r * n + i] = __ddiv_rn(run, rsum);
+      if (pdftab) pdftab[r * n + i] = __ddiv_rn(__dmul_rn(row[i], g.pdf_scale), g.total[b]);
+    }
+    if (g.mode == 2 && m > 0) {
+      // r indexes (b, j); block row jin = j % m of block (bj = j / m, bi)
+      int j = (int)(r % n);
+      int bj = j / m, jin = j % m;
+      for (int bi = 0; bi < 8; ++bi) {
+        const double* brow = row + bi * m;
+        double rw = __dadd_rn(0.0, pairwise_row(brow, m));
+        double run2 = 0.0;
+        int64_t cbase = ((((b * 8 + bj) * 8 + bi) * m) + jin) * m;
+        for (int i = 0; i < m; ++i) {
+          run2 = i == 0 ? brow[0] : __dadd_rn(run2, brow[i]);
+          if (blk_cond) blk_cond[cbase + i] = __ddiv_rn(run2, rw);
+        }
+        if (blk_marg && jin == m - 1) {
+          // the whole block is known here: cumsum of its row sums / block sum
+          const double* blk0 = g.vals + (b * n + bj * m) * n + bi * m;
+          double bsum = g.block_sums[(b * 8 + bj) * 8 + bi];
+          double run3 = 0.0;
+          for (int q = 0; q < m; ++q) {
+            double rq = __dadd_rn(0.0, pairwise_row(blk0 + (int64_t)q * n, m));
+            run3 = q == 0 ? rq : __dadd_rn(run3, rq);
+            blk_marg[(((b * 8 + bj) * 8 + bi) * m) + q] = __ddiv_rn(run3, bsum);
+          }
+        }
+      }
+    }
+  }
+}
+
+// GuideTables.fill_batch on caller-provided floored values (guiding.py:293-309)
+__global__ void k_guide_fill(const double* __restrict__ vals, int n, int64_t nb,
+                             double* __restrict__ row_sum, double* __restrict__ marg,
+                             double* __restrict__ total, double* __restrict__ block_sums) {
+  extern __shared__ double rs[];
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const double* v = vals + b * (int64_t)n * n;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      double r = __dadd_rn(0.0, pairwise_row(v + (int64_t)j * n, n));
+      rs[j] = r;
+      row_sum[b * n + j] = r;
+    }
+    if (block_sums) {
+      const int M = n / 8;
+      for (int q = threadIdx.x; q < 64; q += blockDim.x) {
+        const int bj = q / 8, bi = q % 8;
+        double acc = 0.0;
+        for (int r = 0; r < M; ++r)
+          acc = __dadd_rn(acc, __dadd_rn(0.0, pairwise_row(v + (int64_t)(bj * M + r) * n + bi * M, M)));
+        block_sums[b * 64 + q] = acc;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = __dadd_rn(0.0, pairwise_row(rs, n));
+      total[b] = tot;
+      double run = 0.0;
+      for (int j = 0; j < n; ++j) {
+        run = j == 0 ? rs[0] : __dadd_rn(run, rs[j]);
+        marg[b * n + j] = __ddiv_rn(run, tot);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace wfpg
+
+using namespace wfpg;
+
+extern "C" int wfpg_guide_fill(wfpg_guide* guide, int64_t n_bins, void* stream) {
+  if (!guide || n_bins < 0 || guide->n < 1 || guide->n > 128 || !guide->vals || !guide->row_sum ||
+      !guide->marg || !guide->total || (guide->mode == 2 && (!guide->block_sums || guide->n % 8))) {
+    set_error("wfpg_guide_fill: bad arguments");
+    return WFPG_ERR_ARG;
+  }
+  if (n_bins == 0) return WFPG_OK;
+  int grid = (int)std::min<int64_t>(n_bins, kNumSMs * 8);
+  k_guide_fill<<<grid, 128, sizeof(double) * guide->n, as_stream(stream)>>>(
+      guide->vals, guide->n, n_bins, guide->row_sum, guide->marg, guide->total,
+      guide->mode == 2 ? guide->block_sums : nullptr);
+  WFPG_CHECK_LAUNCH("k_guide_fill");
+  return WFPG_OK;
+}
+
+extern "C" int wfpg_generate_fields(const wfpg_scene* scene, const wfpg_svo* svo,
+                                    const double* origins, const double* jitters, int64_t n_bins,
+                                    const int32_t* n_bins_dev, int32_t n, int32_t blur_radius,
+                                    const double* blur_w, wfpg_guide* guide, void* stream) {
+  if (!scene || !svo || !guide || n_bins < 0 || blur_radius < 0 || blur_radius > 16 ||
+      (blur_radius > 0 && !blur_w) || (n_bins > 0 && (!origins || !jitters)) ||
+      !guide->vals || !guide->row_sum || !guide->marg || !guide->total) {
+    set_error("wfpg_generate_fields: bad arguments");
+    return WFPG_ERR_ARG;
+  }
+  if (guide->capacity < n_bins) {
+    set_error("wfpg_generate_fields: guide capacity %d < %lld bins", guide->capacity,
+              (long long)n_bins);
+    return WFPG_ERR_CAPACITY;
+  }
+  BlurParams bp{};
+  bp.radius = blur_radius;
+  for (int k = 0; k <= 2 * blur_radius && blur_radius > 0; ++k) bp.w[k] = blur_w[k];
+  FieldOut out{guide->vals, guide->row_sum, guide->marg, guide->total,
+               guide->mode == 2 ? guide->block_sums : nullptr, guide->eps};
+  guide->n = n;
+  return launch_fields(make_scene_view(scene), make_view(svo), origins, jitters, n_bins,
+                       n_bins_dev, n, bp, out, as_stream(stream));
+}
+
+extern "C" int wfpg_guide_expand(const wfpg_guide* guide, int64_t n_bins, double* cond,
+                                 double* pdftab, double* blk_marg, double* blk_cond,
+                                 void* stream) {
+  if (!guide || n_bins < 0 || (guide->mode == 2 && !guide->block_sums)) {
+    set_error("wfpg_guide_expand: bad arguments");
+    return WFPG_ERR_ARG;
+  }
+  if (n_bins == 0) return WFPG_OK;
+  GuideView g{};
+  g.mode = guide->mode;
+  g.n = guide->n;
+  g.m = guide->n / 8;
+  g.pdf_scale = (double)(guide->n * guide->n) / (4.0 * WFPG_PI);
+  g.vals = guide->vals;
+  g.row_sum = guide->row_sum;
+  g.total = guide->total;
+  g.block_sums = guide->block_sums;
+  int64_t rows = n_bins * guide->n;
+  int grid = (int)std::min<int64_t>(ceil_div(rows, 128), kNumSMs * 8);
+  k_guide_expand<<<grid, 128, 0, as_stream(stream)>>>(g, n_bins, cond, pdftab, blk_marg, blk_cond);
+  WFPG_CHECK_LAUNCH("k_guide_expand");
+  return WFPG_OK;
+}

@@ -1,0 +1,24 @@
+#pragma once
+#include "geometry.cuh"
+
+namespace wfpg {
+
+struct BlurParams {
+  int radius;
+  double w[33];
+};
+
+struct FieldOut {
+  double* vals;
+  double* row_sum;
+  double* marg;
+  double* total;
+  double* block_sums;  // NULL unless product mode
+  double eps;
+};
+
+int launch_fields(const SceneView& s, const SvoView& v, const double* origins,
+                  const double* jitters, int64_t nb_max, const int32_t* nb_dev, int n,
+                  const BlurParams& bp, const FieldOut& out, cudaStream_t st);
+
+}  // namespace wfpg

@@ -1,0 +1,227 @@
+// Alg. 2 positional binning over the SVO (wavefront.py:98-157) and the
+// per-bin origin / jitter / slot setup (wavefront.py:160-195).
+//
+// The reference pushes ray counters bottom-up level by level; a node's total
+// is the number of paths whose start node lies in its subtree.  Here every
+// path adds 1 to each node of its own ancestor chain above l_min (only those
+// levels are ever tested: a node at level l_min is marked regardless), which
+// yields the same totals on every node the ascent reads.  Paths then ascend
+// to the first marked node, (bin node, path order) pairs are stably
+// radix-sorted, and runs become bins ordered by node id with members in
+// ascending path order — exactly np.argsort(kind="stable") + np.unique.
+#include "partition.cuh"
+#include "prims.cuh"
+
+namespace wfpg {
+
+__global__ void k_part_count(SvoView v, int32_t* __restrict__ counter,
+                             const double* __restrict__ pos, int64_t n_max,
+                             const int32_t* __restrict__ n_dev, int l_min,
+                             int32_t* __restrict__ start, int8_t* __restrict__ start_lev) {
+  const int64_t n = dev_count(n_max, n_dev);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t qx = quantise(pos[3 * i], v.lox, v.scale, v.resolution);
+    int32_t qy = quantise(pos[3 * i + 1], v.loy, v.scale, v.resolution);
+    int32_t qz = quantise(pos[3 * i + 2], v.loz, v.scale, v.resolution);
+    int32_t node = 0, lvl = 0;
+    int32_t chain[22];
+    chain[0] = 0;
+    for (int level = 1; level <= v.depth; ++level) {
+      int sh = v.depth - level;
+      int oct = ((qx >> sh) & 1) | (((qy >> sh) & 1) << 1) | (((qz >> sh) & 1) << 2);
+      uint2 d = __ldg(&v.desc[node]);
+      if (!((d.y >> oct) & 1u)) break;
+      node = (int32_t)d.x + __popc(d.y & ((1u << oct) - 1u));
+      lvl = level;
+      chain[level] = node;
+    }
+    start[i] = node;
+    start_lev[i] = (int8_t)lvl;
+    for (int l = lvl; l > l_min; --l) atomicAdd(&counter[chain[l]], 1);
+  }
+}
+
+__global__ void k_part_ascend(const int32_t* __restrict__ counter,
+                              const int32_t* __restrict__ parent, const int32_t* __restrict__ start,
+                              const int8_t* __restrict__ start_lev, int64_t n_max,
+                              const int32_t* __restrict__ n_dev, int l_min, int c_ray,
+                              uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const int64_t n = dev_count(n_max, n_dev);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t a = start[i];
+    int lev = start_lev[i];
+    // marked = counter >= c_ray or level == l_min; step while unmarked and above l_min
+    while (lev > l_min && counter[a] < c_ray) {
+      a = parent[a];
+      --lev;
+    }
+    keys[i] = (uint64_t)a;
+    vals[i] = (uint32_t)i;
+  }
+}
+
+__global__ void k_part_clear(int32_t* __restrict__ counter, const int32_t* __restrict__ parent,
+                             const int32_t* __restrict__ start, const int8_t* __restrict__ start_lev,
+                             int64_t n_max, const int32_t* __restrict__ n_dev, int l_min) {
+  const int64_t n = dev_count(n_max, n_dev);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t a = start[i];
+    for (int l = start_lev[i]; l > l_min; --l) {
+      counter[a] = 0;
+      a = parent[a];
+    }
+  }
+}
+
+__global__ void k_part_flags(const uint64_t* __restrict__ keys, int64_t n_max,
+                             const int32_t* __restrict__ n_dev, uint32_t* __restrict__ flags) {
+  const int64_t n = dev_count(n_max, n_dev);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    flags[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1u : 0u;
+}
+
+__global__ void k_part_bins(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                            const uint32_t* __restrict__ flags, const uint32_t* __restrict__ scan,
+                            const int32_t* __restrict__ path_idx, int64_t n_max,
+                            const int32_t* __restrict__ n_dev, int64_t cap,
+                            int32_t* __restrict__ bin_node, int32_t* __restrict__ bin_start,
+                            int32_t* __restrict__ members) {
+  const int64_t n = dev_count(n_max, n_dev);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (members) members[i] = path_idx ? path_idx[vals[i]] : (int32_t)vals[i];
+    if (flags[i]) {
+      uint32_t b = scan[i];
+      if (b < cap) {
+        bin_node[b] = (int32_t)keys[i];
+        bin_start[b] = (int32_t)i;
+      }
+    }
+  }
+}
+
+__global__ void k_part_counts(const int32_t* __restrict__ bin_start, const uint32_t* __restrict__ nb,
+                              int64_t n_max, const int32_t* __restrict__ n_dev, int64_t cap,
+                              int32_t* __restrict__ bin_count, int32_t* __restrict__ n_bins_out,
+                              int32_t* __restrict__ overflow) {
+  const int64_t n = dev_count(n_max, n_dev);
+  const int64_t bins = *nb;
+  const int64_t m = bins < cap ? bins : cap;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < m;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    int64_t end = (b + 1 < bins && b + 1 < cap) ? bin_start[b + 1] : n;
+    if (b + 1 < bins && b + 1 >= cap) end = bin_start[b] + 1;  // truncated; flagged below
+    bin_count[b] = (int32_t)(end - bin_start[b]);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *n_bins_out = (int32_t)m;
+    if (bins > cap && overflow) atomicOr(overflow, 1);
+  }
+}
+
+size_t partition_ws_bytes(int64_t n) {
+  int64_t m = n > 0 ? n : 1;
+  return align_up(4 * m) + align_up(1 * m) + align_up(8 * m) + align_up(4 * m) +
+         align_up(4 * (m + 1)) + align_up(4 * (m + 1)) + align_up(8) +
+         std::max(sort_ws_bytes(m), scan_ws_bytes(m + 1)) + 4096;
+}
+
+int partition_spatial(const SvoView& v, int32_t* counter, const int32_t* parent,
+                      const double* pos, const int32_t* path_idx, int64_t n_max,
+                      const int32_t* n_dev, int l_min, int c_ray, int n_nodes,
+                      PartitionOut& out, Arena& ws, cudaStream_t st) {
+  if (n_max <= 0) {
+    WFPG_CUDA(cudaMemsetAsync(out.n_bins, 0, sizeof(int32_t), st));
+    return WFPG_OK;
+  }
+  int32_t* start = ws.take<int32_t>(n_max);
+  int8_t* lev = ws.take<int8_t>(n_max);
+  uint64_t* keys = ws.take<uint64_t>(n_max);
+  uint32_t* vals = ws.take<uint32_t>(n_max);
+  uint32_t* flags = ws.take<uint32_t>(n_max + 1);
+  uint32_t* scan = ws.take<uint32_t>(n_max + 1);
+  uint32_t* nb = ws.take<uint32_t>(2);
+  if (!ws.ok()) {
+    set_error("partition: workspace too small");
+    return WFPG_ERR_WORKSPACE;
+  }
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_max, 256), kNumSMs * 8));
+  k_part_count<<<grid, 256, 0, st>>>(v, counter, pos, n_max, n_dev, l_min, start, lev);
+  WFPG_CHECK_LAUNCH("k_part_count");
+  k_part_ascend<<<grid, 256, 0, st>>>(counter, parent, start, lev, n_max, n_dev, l_min, c_ray,
+                                      keys, vals);
+  WFPG_CHECK_LAUNCH("k_part_ascend");
+  k_part_clear<<<grid, 256, 0, st>>>(counter, parent, start, lev, n_max, n_dev, l_min);
+  WFPG_CHECK_LAUNCH("k_part_clear");
+  {
+    size_t mark = ws.off;
+    WFPG_TRY(sort_pairs(keys, vals, n_max, n_dev, bits_for((uint64_t)n_nodes), ws, st));
+    ws.off = mark;
+  }
+  k_part_flags<<<grid, 256, 0, st>>>(keys, n_max, n_dev, flags);
+  WFPG_CHECK_LAUNCH("k_part_flags");
+  {
+    size_t mark = ws.off;
+    WFPG_TRY(scan_u32(flags, scan, n_max, n_dev, nb, ws, st));
+    ws.off = mark;
+  }
+  k_part_bins<<<grid, 256, 0, st>>>(keys, vals, flags, scan, path_idx, n_max, n_dev, out.capacity,
+                                    out.bin_node, out.bin_start, out.members);
+  WFPG_CHECK_LAUNCH("k_part_bins");
+  int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(out.capacity, 256), kNumSMs * 4));
+  k_part_counts<<<bgrid, 256, 0, st>>>(out.bin_start, nb, n_max, n_dev, out.capacity,
+                                       out.bin_count, out.n_bins, out.overflow);
+  WFPG_CHECK_LAUNCH("k_part_counts");
+  out.sorted_items = vals;  // valid until the workspace is reused
+  return WFPG_OK;
+}
+
+}  // namespace wfpg
+
+using namespace wfpg;
+
+extern "C" size_t wfpg_partition_workspace_bytes(int64_t n, int64_t n_nodes) {
+  (void)n_nodes;
+  return partition_ws_bytes(n) + 256;
+}
+
+extern "C" int wfpg_partition_spatial(wfpg_svo* svo, const double* positions,
+                                      const int32_t* path_idx, int64_t n, const int32_t* n_dev,
+                                      int32_t l_min, int32_t c_ray, int32_t* bin_node,
+                                      int32_t* bin_start, int32_t* bin_count, int32_t* members,
+                                      int32_t* n_bins_dev, int64_t bin_capacity, void* workspace,
+                                      size_t ws_bytes, void* stream) {
+  if (!svo || !svo->counter || !svo->parent || n < 0 || (n > 0 && !positions) || !n_bins_dev ||
+      !bin_node || !bin_start || !bin_count) {
+    set_error("wfpg_partition_spatial: bad arguments");
+    return WFPG_ERR_ARG;
+  }
+  if (l_min >= svo->depth) {
+    set_error("l_min must be below the SVO depth");
+    return WFPG_ERR_ARG;
+  }
+  Arena ws(workspace, ws_bytes);
+  int32_t* overflow = ws.take<int32_t>(1);
+  if (!ws.ok()) {
+    set_error("partition: workspace too small");
+    return WFPG_ERR_WORKSPACE;
+  }
+  cudaStream_t st = as_stream(stream);
+  WFPG_CUDA(cudaMemsetAsync(overflow, 0, sizeof(int32_t), st));
+  PartitionOut out{bin_node, bin_start, bin_count, members, n_bins_dev, overflow, bin_capacity,
+                   nullptr};
+  WFPG_TRY(partition_spatial(make_view(svo), svo->counter, svo->parent, positions, path_idx, n,
+                             n_dev, l_min, c_ray, (int)svo->n_nodes, out, ws, st));
+  int32_t ov = 0;
+  WFPG_CUDA(cudaMemcpyAsync(&ov, overflow, 4, cudaMemcpyDeviceToHost, st));
+  WFPG_CUDA(cudaStreamSynchronize(st));
+  if (ov) {
+    set_error("partition: more bins than bin_capacity=%lld", (long long)bin_capacity);
+    return WFPG_ERR_CAPACITY;
+  }
+  return WFPG_OK;
+}

@@ -1,0 +1,23 @@
+#pragma once
+#include "common.cuh"
+
+namespace wfpg {
+
+struct PartitionOut {
+  int32_t* bin_node;
+  int32_t* bin_start;
+  int32_t* bin_count;
+  int32_t* members;     // path ids grouped by bin (optional)
+  int32_t* n_bins;      // device count (clamped to capacity)
+  int32_t* overflow;    // device flag, set when bins > capacity (optional)
+  int64_t capacity;
+  const uint32_t* sorted_items;  // out: item index per sorted position
+};
+
+size_t partition_ws_bytes(int64_t n);
+int partition_spatial(const SvoView& v, int32_t* counter, const int32_t* parent,
+                      const double* pos, const int32_t* path_idx, int64_t n_max,
+                      const int32_t* n_dev, int l_min, int c_ray, int n_nodes,
+                      PartitionOut& out, Arena& ws, cudaStream_t st);
+
+}  // namespace wfpg

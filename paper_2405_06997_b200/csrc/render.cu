@@ -1,0 +1,396 @@
+// One guided wavefront pass on the device (wavefront.py:198-277).
+//
+// All per-depth control stays on the GPU: queue lengths, lambert counts and
+// bin counts are device integers consumed by grid-stride kernels sized for
+// the worst case, so the whole pass is a single stream of launches with one
+// host synchronisation at the end (to return PassStats).
+#include <cstring>
+
+#include "exitance.cuh"
+#include "fields.cuh"
+#include "partition.cuh"
+#include "prims.cuh"
+#include "wavefront.cuh"
+
+namespace wfpg {
+
+constexpr int kMaxDepth = 31;
+constexpr int kMatStats = 16;
+
+struct StatsDev {
+  int32_t live[kMaxDepth + 1];
+  int32_t lam[kMaxDepth + 1];
+  int32_t bins[kMaxDepth + 1];
+  int32_t mats[kMaxDepth + 1][kMatStats];
+  int32_t deposits;
+  int32_t overflow;
+};
+
+__global__ void k_flags_alive(const uint8_t* __restrict__ alive, int64_t n,
+                              uint32_t* __restrict__ flags) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    flags[i] = alive[i] ? 1u : 0u;
+}
+
+__global__ void k_scatter_alive(const uint32_t* __restrict__ flags,
+                                const uint32_t* __restrict__ scan, int64_t n,
+                                int32_t* __restrict__ active, const uint32_t* __restrict__ total,
+                                int32_t* __restrict__ n_out, int32_t* __restrict__ stat) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (flags[i]) active[scan[i]] = (int32_t)i;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *n_out = (int32_t)*total;
+    *stat = (int32_t)*total;
+  }
+}
+
+// flags over the active queue: hit a lambert surface; material histogram
+__global__ void k_flags_lambert(SceneView s, const int32_t* __restrict__ active,
+                                const int32_t* __restrict__ n_act, const int32_t* __restrict__ hit_tri,
+                                int64_t n_max, uint32_t* __restrict__ flags,
+                                int32_t* __restrict__ mat_stats) {
+  __shared__ int32_t hist[kMatStats];
+  if (threadIdx.x < kMatStats) hist[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t n = dev_count(n_max, n_act);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t tri = hit_tri[active[i]];
+    uint32_t f = 0;
+    if (tri >= 0) {
+      int mid = s.tri_mat[tri];
+      if (mid < kMatStats) atomicAdd(&hist[mid], 1);
+      f = s.mat_kind[mid] == 0 ? 1u : 0u;
+    }
+    flags[i] = f;
+  }
+  __syncthreads();
+  if (threadIdx.x < kMatStats && hist[threadIdx.x]) atomicAdd(&mat_stats[threadIdx.x], hist[threadIdx.x]);
+}
+
+// lambert list in path order + hit positions, numpy order o + t*d (wavefront.py:553)
+__global__ void k_scatter_lambert(const int32_t* __restrict__ active,
+                                  const int32_t* __restrict__ n_act,
+                                  const uint32_t* __restrict__ flags,
+                                  const uint32_t* __restrict__ scan, int64_t n_max,
+                                  const double* __restrict__ ray_o, const double* __restrict__ ray_d,
+                                  const double* __restrict__ hit_t, int32_t* __restrict__ lam,
+                                  double* __restrict__ lam_pos, const uint32_t* __restrict__ total,
+                                  int32_t* __restrict__ n_lam, int32_t* __restrict__ stat) {
+  const int64_t n = dev_count(n_max, n_act);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (!flags[i]) continue;
+    int32_t p = active[i];
+    uint32_t o = scan[i];
+    lam[o] = p;
+    double t = hit_t[p];
+    for (int c = 0; c < 3; ++c)
+      lam_pos[3 * (int64_t)o + c] = __dadd_rn(ray_o[3 * (int64_t)p + c],
+                                              __dmul_rn(t, ray_d[3 * (int64_t)p + c]));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *n_lam = (int32_t)*total;
+    *stat = (int32_t)*total;
+  }
+}
+
+// per-bin stream, origin pick, jitter and member slots (wavefront.py:170-189)
+__global__ void k_bin_setup(const int32_t* __restrict__ n_bins, const int32_t* __restrict__ bin_node,
+                            const int32_t* __restrict__ bin_start,
+                            const int32_t* __restrict__ bin_count,
+                            const uint32_t* __restrict__ sorted_items,
+                            const int32_t* __restrict__ lam, const double* __restrict__ lam_pos,
+                            uint64_t seed, int64_t sample0, int depth, int jitter,
+                            double* __restrict__ origins, double* __restrict__ jitters,
+                            int32_t* __restrict__ bin_slot, int32_t* __restrict__ stat) {
+  const int64_t nb = *n_bins;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *stat = (int32_t)nb;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t node = bin_node[b];
+    const int64_t len = bin_count[b], s0 = bin_start[b];
+    // bin_stream_id (wavefront.py:160-162): ((sample*64 + depth) << 32 + node) * 4 + 1
+    uint64_t sid = ((((uint64_t)sample0 * 64u + (uint64_t)depth) << 32) + (uint64_t)node) * 4u + 1u;
+    uint64_t key = stream_key(seed, sid);
+    long long k = (long long)(u01(key, 0) * (double)len);
+    if (k > len - 1) k = len - 1;
+    uint32_t item = sorted_items[s0 + k];
+    origins[3 * b] = lam_pos[3 * (int64_t)item];
+    origins[3 * b + 1] = lam_pos[3 * (int64_t)item + 1];
+    origins[3 * b + 2] = lam_pos[3 * (int64_t)item + 2];
+    jitters[2 * b] = jitter ? u01(key, 1) : 0.5;
+    jitters[2 * b + 1] = jitter ? u01(key, 2) : 0.5;
+    if (bin_slot)
+      for (int64_t j = s0; j < s0 + len; ++j) bin_slot[lam[sorted_items[j]]] = (int32_t)b;
+  }
+}
+
+__global__ void k_frame(const double* __restrict__ radiance, int64_t n_pix, int n_samples,
+                        double* __restrict__ frame) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n_pix;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    for (int c = 0; c < 3; ++c) {
+      double acc = 0.0;  // np.add.at over paths in sample-major order
+      for (int s = 0; s < n_samples; ++s)
+        acc = __dadd_rn(acc, radiance[3 * ((int64_t)s * n_pix + q) + c]);
+      frame[3 * q + c] = __ddiv_rn(acc, (double)n_samples);
+    }
+  }
+}
+
+struct PassLayout {
+  int64_t P, n_pix, cap;
+  int n0;
+  // buffers
+  int32_t* active;
+  uint32_t* flags;
+  uint32_t* scan;
+  uint32_t* total;
+  int32_t* n_active;
+  double* hit_t;
+  int32_t* hit_tri;
+  int32_t* lam;
+  double* lam_pos;
+  int32_t* n_lam;
+  int32_t* bin_slot;
+  int32_t* bin_node;
+  int32_t* bin_start;
+  int32_t* bin_count;
+  int32_t* n_bins;
+  double* origins;
+  double* jitters;
+  double* vals;
+  double* row_sum;
+  double* marg;
+  double* tot;
+  double* block_sums;
+  double* upper_dirs;
+  StatsDev* stats;
+  size_t scratch_off;
+};
+
+static int64_t bin_capacity(const wfpg_svo* svo, const wfpg_pass_config* cfg, int64_t P) {
+  if (!svo) return 0;
+  int lm = cfg->l_min < 0 ? 0 : cfg->l_min;
+  if (lm + 1 > svo->depth + 1) lm = svo->depth;
+  int64_t cap = svo->level_off[lm + 1] + (int64_t)(svo->depth - lm) * (P / std::max(1, cfg->c_ray)) + 1;
+  return std::max<int64_t>(1, std::min<int64_t>(cap, P));
+}
+
+static void carve_pass(Arena& a, const wfpg_svo* svo, const wfpg_camera* cam,
+                       const wfpg_pass_config* cfg, PassLayout& L) {
+  L.n_pix = (int64_t)cam->width * cam->height;
+  L.P = L.n_pix * std::max(1, cfg->n_samples);
+  L.cap = bin_capacity(svo, cfg, L.P);
+  L.n0 = std::max(8, cfg->field_res);
+  const int64_t P = L.P;
+  L.active = a.take<int32_t>(P);
+  L.flags = a.take<uint32_t>(P + 1);
+  L.scan = a.take<uint32_t>(P + 1);
+  L.total = a.take<uint32_t>(4);
+  L.n_active = a.take<int32_t>(4);
+  L.hit_t = a.take<double>(P);
+  L.hit_tri = a.take<int32_t>(P);
+  L.stats = a.take<StatsDev>(1);
+  L.upper_dirs = a.take<double>(192);
+  if (svo) {
+    L.lam = a.take<int32_t>(P);
+    L.lam_pos = a.take<double>(3 * P);
+    L.n_lam = a.take<int32_t>(4);
+    L.bin_slot = a.take<int32_t>(P);
+    L.bin_node = a.take<int32_t>(L.cap);
+    L.bin_start = a.take<int32_t>(L.cap);
+    L.bin_count = a.take<int32_t>(L.cap);
+    L.n_bins = a.take<int32_t>(4);
+    L.origins = a.take<double>(3 * L.cap);
+    L.jitters = a.take<double>(2 * L.cap);
+    if (cfg->guided_depths > 0) {
+      L.vals = a.take<double>(L.cap * (int64_t)L.n0 * L.n0);
+      L.row_sum = a.take<double>(L.cap * (int64_t)L.n0);
+      L.marg = a.take<double>(L.cap * (int64_t)L.n0);
+      L.tot = a.take<double>(L.cap);
+      L.block_sums = cfg->product ? a.take<double>(L.cap * 64) : nullptr;
+    }
+  }
+  L.scratch_off = a.off;
+  size_t scratch = std::max(scan_ws_bytes(P + 1), partition_ws_bytes(P));
+  if (svo) scratch = std::max(scratch, update_exitance_ws_bytes(P, cfg->max_depth));
+  a.take<char>((int64_t)scratch);
+}
+
+static bool cfg_ok(const wfpg_pass_config* cfg) {
+  return cfg->max_depth >= 1 && cfg->max_depth <= kMaxDepth && cfg->guided_depths >= 0 &&
+         cfg->guided_depths <= cfg->max_depth && cfg->c_ray >= 1 && cfg->n_samples >= 1 &&
+         cfg->blur_radius >= 0 && cfg->blur_radius <= 16;
+}
+
+}  // namespace wfpg
+
+using namespace wfpg;
+
+extern "C" size_t wfpg_render_workspace_bytes(const wfpg_scene* scene, const wfpg_svo* svo,
+                                              const wfpg_camera* cam,
+                                              const wfpg_pass_config* cfg) {
+  if (!scene || !cam || !cfg) return 0;
+  Arena a(nullptr, 0);
+  PassLayout L;
+  carve_pass(a, svo, cam, cfg, L);
+  return a.off + 4096;
+}
+
+extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camera* cam,
+                                const wfpg_pass_config* cfg, wfpg_paths* paths, double* frame,
+                                wfpg_pass_stats* stats, void* workspace, size_t ws_bytes,
+                                void* stream) {
+  if (!scene || !cam || !cfg || !paths || !frame || !cfg_ok(cfg)) {
+    set_error("wfpg_render_pass: bad arguments");
+    return WFPG_ERR_ARG;
+  }
+  if (svo && cfg->l_min >= svo->depth) {
+    set_error("l_min must be below the SVO depth");
+    return WFPG_ERR_ARG;
+  }
+  if (svo && cfg->product && cfg->guided_depths > 0 && !cfg->upper_dirs) {
+    set_error("wfpg_render_pass: product mode needs upper_dirs");
+    return WFPG_ERR_ARG;
+  }
+  if (paths->max_depth != cfg->max_depth) {
+    set_error("wfpg_render_pass: path state depth %d != config depth %d", paths->max_depth,
+              cfg->max_depth);
+    return WFPG_ERR_ARG;
+  }
+  cudaStream_t st = as_stream(stream);
+  Arena a(workspace, ws_bytes);
+  PassLayout L;
+  carve_pass(a, svo, cam, cfg, L);
+  if (!a.ok()) {
+    set_error("wfpg_render_pass: workspace too small (%zu < %zu)", ws_bytes, a.off);
+    return WFPG_ERR_WORKSPACE;
+  }
+  if (paths->n != L.P) {
+    set_error("wfpg_render_pass: path state holds %lld paths, pass needs %lld",
+              (long long)paths->n, (long long)L.P);
+    return WFPG_ERR_ARG;
+  }
+  Arena scratch(static_cast<char*>(workspace) + L.scratch_off, ws_bytes - L.scratch_off);
+  const int64_t P = L.P;
+  const SceneView sv = make_scene_view(scene);
+  const CameraView cv = make_camera_view(cam);
+  const PathsView pv = make_paths_view(paths);
+  SvoView vv{};
+  if (svo) vv = make_view(svo);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(P, 256), kNumSMs * 8));
+
+  WFPG_CUDA(cudaMemsetAsync(L.stats, 0, sizeof(StatsDev), st));
+  WFPG_TRY(launch_camera_init(cv, pv, P, L.n_pix, cfg->sample_index, cfg->seed, st));
+
+  BlurParams bp{};
+  bp.radius = cfg->blur_radius;
+  for (int k = 0; k <= 2 * bp.radius && bp.radius > 0; ++k) bp.w[k] = cfg->blur_w[k];
+
+  for (int depth = 1; depth <= cfg->max_depth; ++depth) {
+    // live queue (np.nonzero(state.alive), wavefront.py:227)
+    k_flags_alive<<<grid, 256, 0, st>>>(paths->alive, P, L.flags);
+    WFPG_CHECK_LAUNCH("k_flags_alive");
+    {
+      size_t mark = scratch.off;
+      WFPG_TRY(scan_u32(L.flags, L.scan, P, nullptr, L.total, scratch, st));
+      scratch.off = mark;
+    }
+    k_scatter_alive<<<grid, 256, 0, st>>>(L.flags, L.scan, P, L.active, L.total, L.n_active,
+                                          &L.stats->live[depth]);
+    WFPG_CHECK_LAUNCH("k_scatter_alive");
+    WFPG_TRY(launch_intersect(sv, paths->ray_o, paths->ray_d, L.active, P, L.n_active,
+                              scene->ray_eps, L.hit_t, L.hit_tri, false, st));
+
+    GuideView gv{};
+    gv.mode = 0;
+    const int32_t* slots = nullptr;
+    if (svo) {
+      k_flags_lambert<<<grid, 256, 0, st>>>(sv, L.active, L.n_active, L.hit_tri, P, L.flags,
+                                            L.stats->mats[depth]);
+      WFPG_CHECK_LAUNCH("k_flags_lambert");
+      {
+        size_t mark = scratch.off;
+        WFPG_TRY(scan_u32(L.flags, L.scan, P, L.n_active, L.total, scratch, st));
+        scratch.off = mark;
+      }
+      k_scatter_lambert<<<grid, 256, 0, st>>>(L.active, L.n_active, L.flags, L.scan, P,
+                                              paths->ray_o, paths->ray_d, L.hit_t, L.lam,
+                                              L.lam_pos, L.total, L.n_lam, &L.stats->lam[depth]);
+      WFPG_CHECK_LAUNCH("k_scatter_lambert");
+      PartitionOut po{L.bin_node, L.bin_start, L.bin_count, nullptr, L.n_bins,
+                      &L.stats->overflow, L.cap, nullptr};
+      size_t mark = scratch.off;
+      WFPG_TRY(partition_spatial(vv, svo->counter, svo->parent, L.lam_pos, nullptr, P, L.n_lam,
+                                 cfg->l_min, cfg->c_ray, (int)svo->n_nodes, po, scratch, st));
+      const bool guided_depth = depth <= cfg->guided_depths;
+      if (guided_depth) {
+        WFPG_CUDA(cudaMemsetAsync(L.bin_slot, 0xFF, sizeof(int32_t) * P, st));
+      }
+      int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(L.cap, 128), kNumSMs * 8));
+      k_bin_setup<<<bgrid, 128, 0, st>>>(L.n_bins, L.bin_node, L.bin_start, L.bin_count,
+                                         po.sorted_items, L.lam, L.lam_pos, cfg->seed,
+                                         cfg->sample_index, depth, cfg->jitter, L.origins,
+                                         L.jitters, guided_depth ? L.bin_slot : nullptr,
+                                         &L.stats->bins[depth]);
+      WFPG_CHECK_LAUNCH("k_bin_setup");
+      scratch.off = mark;
+      if (guided_depth) {
+        const int n = std::max(8, cfg->field_res >> (depth - 1));
+        FieldOut fo{L.vals, L.row_sum, L.marg, L.tot, cfg->product ? L.block_sums : nullptr,
+                    cfg->epsilon};
+        WFPG_TRY(launch_fields(sv, vv, L.origins, L.jitters, L.cap, L.n_bins, n, bp, fo, st));
+        gv.mode = cfg->product ? 2 : 1;
+        gv.n = n;
+        gv.m = n / 8;
+        gv.eps = cfg->epsilon;
+        gv.pdf_scale = (double)(n * n) / (4.0 * WFPG_PI);
+        gv.vals = L.vals;
+        gv.row_sum = L.row_sum;
+        gv.marg = L.marg;
+        gv.total = L.tot;
+        gv.block_sums = L.block_sums;
+        gv.upper_dirs = cfg->upper_dirs;
+        slots = L.bin_slot;
+      }
+    }
+    WFPG_TRY(launch_shade(sv, gv, pv, depth, L.active, P, L.n_active, L.hit_t, L.hit_tri, slots,
+                          cfg->russian_roulette != 0, cfg->rr_depth, st));
+  }
+
+  if (svo) {
+    WFPG_TRY(update_exitance(svo, paths->emit_depth, paths->emit_le, paths->rec_T,
+                             paths->rec_pos, cfg->max_depth + 1, P, cfg->deterministic,
+                             &L.stats->deposits, scratch, st));
+  }
+  k_frame<<<(int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(L.n_pix, 256), kNumSMs * 8)), 256,
+            0, st>>>(paths->radiance, L.n_pix, cfg->n_samples, frame);
+  WFPG_CHECK_LAUNCH("k_frame");
+
+  if (stats) {
+    StatsDev h;
+    WFPG_CUDA(cudaMemcpyAsync(&h, L.stats, sizeof(StatsDev), cudaMemcpyDeviceToHost, st));
+    WFPG_CUDA(cudaStreamSynchronize(st));
+    if (h.overflow) {
+      set_error("wfpg_render_pass: bin capacity %lld exceeded", (long long)L.cap);
+      return WFPG_ERR_CAPACITY;
+    }
+    std::memset(stats, 0, sizeof(*stats));
+    int run = 0;
+    for (int d = 1; d <= cfg->max_depth; ++d) {
+      if (h.live[d] == 0) break;  // the reference stops at the first empty depth
+      stats->live_per_depth[run] = h.live[d];
+      stats->rays_per_depth[run] = h.lam[d];
+      stats->bins_per_depth[run] = h.bins[d];
+      for (int m = 0; m < kMatStats; ++m) stats->mat_groups[run][m] = h.mats[d][m];
+      ++run;
+    }
+    stats->depths_run = run;
+    stats->deposits = h.deposits;
+  }
+  return WFPG_OK;
+}

@@ -1,0 +1,199 @@
+// Guided sampling helpers + the per-path shading step (_kernels.pyx:800-1161).
+#pragma once
+#include "geometry.cuh"
+
+namespace wfpg {
+
+struct GuideView {
+  int mode;  // 0 off, 1 plain, 2 product
+  int n;
+  int m;     // n / 8
+  double eps;
+  double pdf_scale;  // n*n / (4 pi) as computed by the reference (guiding.py:300)
+  const double* vals;
+  const double* row_sum;
+  const double* marg;
+  const double* total;
+  const double* block_sums;
+  const double* upper_dirs;  // (8,8,3) host-numpy octahedral cell centres
+};
+
+// upper_bound (_kernels.pyx:802-812)
+__device__ __forceinline__ int upper_bound_d(const double* cdf, int n, double u) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (cdf[mid] <= u)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo > n - 1 ? n - 1 : lo;
+}
+
+__device__ __forceinline__ double residual(double u, double lo, double hi) {
+  double span = hi - lo;
+  double f = span > 0.0 ? (u - lo) / span : 0.0;
+  if (f > 1.0 - 1e-12) f = 1.0 - 1e-12;
+  if (f < 0.0) f = 0.0;
+  return f;
+}
+
+// invert_cdf over a stored CDF (_kernels.pyx:815-827)
+__device__ __forceinline__ int invert_cdf(const double* cdf, int n, double u, double* frac) {
+  int i = upper_bound_d(cdf, n, u);
+  double lo = i > 0 ? cdf[i - 1] : 0.0;
+  *frac = residual(u, lo, cdf[i]);
+  return i;
+}
+
+// invert_cdf over cumsum(v[0..n)) / denom evaluated on the fly, with the
+// reference's sequential cumsum (guiding.py:299,309).  A linear scan returns
+// the same index as the binary search because the CDF is non-decreasing.
+__device__ __forceinline__ int invert_cumsum(const double* v, int stride, int n, double denom,
+                                             double u, double* frac) {
+  double run = 0.0, prev = 0.0, cur = 0.0;
+  int i = 0;
+  for (; i < n; ++i) {
+    run = i == 0 ? v[0] : __dadd_rn(run, v[(int64_t)i * stride]);
+    cur = __ddiv_rn(run, denom);
+    if (cur > u) break;
+    if (i < n - 1) prev = cur;
+  }
+  if (i >= n) i = n - 1;  // clamp: cur is cdf[n-1], prev cdf[n-2]
+  double lo = i > 0 ? prev : 0.0;
+  *frac = residual(u, lo, cur);
+  return i;
+}
+
+// numpy pairwise sum of a contiguous row of length n (8 <= n <= 128 or n < 8)
+__device__ __forceinline__ double pairwise_row(const double* a, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
+    return r;
+  }
+  double r0 = a[0], r1 = a[1], r2 = a[2], r3 = a[3], r4 = a[4], r5 = a[5], r6 = a[6], r7 = a[7];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8) {
+    r0 = __dadd_rn(r0, a[i]);
+    r1 = __dadd_rn(r1, a[i + 1]);
+    r2 = __dadd_rn(r2, a[i + 2]);
+    r3 = __dadd_rn(r3, a[i + 3]);
+    r4 = __dadd_rn(r4, a[i + 4]);
+    r5 = __dadd_rn(r5, a[i + 5]);
+    r6 = __dadd_rn(r6, a[i + 6]);
+    r7 = __dadd_rn(r7, a[i + 7]);
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
+                         __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
+  for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+  return res;
+}
+
+__device__ __forceinline__ void cell_of(int n, double dx, double dy, double dz, int* ci, int* cj) {
+  double u, v;
+  octa_dir_to_uv_k(dx, dy, dz, &u, &v);
+  int i = (int)(u * n), j = (int)(v * n);
+  *ci = i > n - 1 ? n - 1 : i;
+  *cj = j > n - 1 ? n - 1 : j;
+}
+
+// pdf_plain_dir (_kernels.pyx:876-885): pdftab = vals * (n^2/4pi) / total
+__device__ __forceinline__ double pdf_plain(const GuideView& g, int slot, double dx, double dy,
+                                            double dz) {
+  int i, j;
+  cell_of(g.n, dx, dy, dz, &i, &j);
+  double v = g.vals[((int64_t)slot * g.n + j) * g.n + i];
+  return __ddiv_rn(__dmul_rn(v, g.pdf_scale), g.total[slot]);
+}
+
+// pdf_product_dir (_kernels.pyx:888-902)
+__device__ __forceinline__ double pdf_product(const GuideView& g, int slot, const double* upper,
+                                              double upsum, double dx, double dy, double dz) {
+  int i, j;
+  cell_of(g.n, dx, dy, dz, &i, &j);
+  int bi = i / g.m, bj = j / g.m;
+  double v = g.vals[((int64_t)slot * g.n + j) * g.n + i];
+  double bs = g.block_sums[((int64_t)slot * 8 + bj) * 8 + bi];
+  return (upper[bj * 8 + bi] / upsum) * (v / bs) * (double)(g.n * g.n) / (4.0 * WFPG_PI);
+}
+
+// plain guided sample (_kernels.pyx:1093-1100): marginal then on-the-fly conditional
+__device__ __forceinline__ void sample_plain(const GuideView& g, int slot, double s1, double s2,
+                                             double* wx, double* wy, double* wz) {
+  const int n = g.n;
+  double fv, fu;
+  int gj = invert_cdf(g.marg + (int64_t)slot * n, n, s1, &fv);
+  const double* row = g.vals + ((int64_t)slot * n + gj) * n;
+  int gi = invert_cumsum(row, 1, n, g.row_sum[(int64_t)slot * n + gj], s2, &fu);
+  octa_uv_to_dir_k((gi + fu) / n, (gj + fv) / n, wx, wy, wz);
+}
+
+// product guided sample (_kernels.pyx:1101-1127)
+__device__ __forceinline__ void sample_product(const GuideView& g, int slot, const double* upper,
+                                               double upsum, double s1, double s2, double s3,
+                                               double s4, double* wx, double* wy, double* wz) {
+  const int n = g.n, m = g.m;
+  double urow[8], ucdf[8], fv, fu;
+  for (int bj = 0; bj < 8; ++bj) {
+    urow[bj] = 0.0;
+    for (int bi = 0; bi < 8; ++bi) urow[bj] += upper[bj * 8 + bi];
+  }
+  ucdf[0] = urow[0] / upsum;
+  for (int bj = 1; bj < 8; ++bj) ucdf[bj] = ucdf[bj - 1] + urow[bj] / upsum;
+  int bj = invert_cdf(ucdf, 8, s1, &fv);
+  ucdf[0] = upper[bj * 8] / urow[bj];
+  for (int bi = 1; bi < 8; ++bi) ucdf[bi] = ucdf[bi - 1] + upper[bj * 8 + bi] / urow[bj];
+  int bi = invert_cdf(ucdf, 8, s2, &fu);
+  // block rows of the selected block: rows[r] = 0 + pairwise(row r), the block
+  // marginal is cumsum(rows) / block_sum (guiding.py:304-309)
+  const double* blk = g.vals + ((int64_t)slot * n + bj * m) * n + bi * m;
+  double bsum = g.block_sums[((int64_t)slot * 8 + bj) * 8 + bi];
+  double rows[16];
+  for (int r = 0; r < m; ++r) rows[r] = __dadd_rn(0.0, pairwise_row(blk + (int64_t)r * n, m));
+  int jin = invert_cumsum(rows, 1, m, bsum, s3, &fv);
+  int iin = invert_cumsum(blk + (int64_t)jin * n, 1, m, rows[jin], s4, &fu);
+  int gj = bj * m + jin, gi = bi * m + iin;
+  octa_uv_to_dir_k((gi + fu) / n, (gj + fv) / n, wx, wy, wz);
+}
+
+// cosine_dir (_kernels.pyx:830-843)
+__device__ __forceinline__ void cosine_dir(double nx, double ny, double nz, double u1, double u2,
+                                           double* ox, double* oy, double* oz) {
+  double r = sqrt(u1);
+  double phi = 2.0 * WFPG_PI * u2;
+  double sp, cp;
+  sincos(phi, &sp, &cp);
+  double x = r * cp, y = r * sp;
+  double z = sqrt(fmax(1.0 - u1, 0.0));
+  double s = copysign(1.0, nz);
+  double a = -1.0 / (s + nz);
+  double b = nx * ny * a;
+  *ox = x * (1.0 + s * nx * nx * a) + y * b + z * nx;
+  *oy = x * (s * b) + y * (s + ny * ny * a) + z * ny;
+  *oz = x * (-s * nx) + y * (-ny) + z * nz;
+}
+
+struct PathsView {
+  double* ray_o;
+  double* ray_d;
+  double* beta;
+  double* radiance;
+  const uint64_t* key;
+  uint64_t* ctr;
+  uint8_t* alive;
+  double* prev_pdf;
+  double* rec_pos;
+  double* rec_T;
+  double* emit_le;
+  int32_t* emit_depth;
+  int32_t rec_depths;
+};
+
+// shade_one (_kernels.pyx:905-1161) for path p.
+__device__ void shade_path(int64_t p, int depth, const SceneView& sa, const GuideView& g,
+                           const PathsView& P, const double* hit_t, const int32_t* hit_tri,
+                           const int32_t* bin_slot, bool rr_enabled, int rr_depth);
+
+}  // namespace wfpg

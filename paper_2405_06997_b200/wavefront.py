@@ -1,0 +1,268 @@
+"""Wavefront render loop — the whole pass runs on the device.
+
+Drop-in for wavefront.py of the reference (wavefront.py:1-332): same
+GuidingConfig, PassStats, SpatialBin, partition_spatial, bin_stream_id,
+render_pass, render_sample and update_exitance.  ``render_pass`` enqueues one
+device pass (csrc/render.cu): camera rays, then per depth compaction,
+intersection, Alg. 2 binning, per-bin field + table generation and shading,
+then the Eq. 5 exitance update and the bottom-up SVO refresh.  Path state
+lives in HBM (``PathState`` holds torch tensors; numpy views on access).
+"""
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _dev, _lib, core, guiding
+
+PATH_STREAM_SPACE = 4
+BIN_STREAM_TAG = 1
+
+
+@dataclass
+class GuidingConfig:
+    """Guiding knobs (wavefront.py:21-50); defaults mirror the reference."""
+
+    l_min: int = 5
+    c_ray: int = 512
+    field_res: int = 128
+    guided_depths: int = 4
+    max_depth: int = 5
+    product: bool = False
+    jitter: bool = True
+    blur_sigma: float = 1.0
+    epsilon: float = guiding.EPSILON_FLOOR
+    russian_roulette: bool = False
+    rr_depth: int = 3
+    seed: int = 0
+
+    def validate(self, svo_depth=None):
+        if self.field_res not in (16, 32, 64, 128):
+            raise ValueError("field_res must be one of 16, 32, 64, 128")
+        if self.c_ray < 1:
+            raise ValueError("c_ray must be >= 1")
+        if self.guided_depths > self.max_depth:
+            raise ValueError("guided_depths cannot exceed max_depth")
+        if svo_depth is not None and self.l_min >= svo_depth:
+            raise ValueError("l_min must be below the SVO depth")
+
+    def field_res_at(self, depth):
+        return max(8, self.field_res >> (depth - 1))
+
+
+_STATE = {
+    # name: (dtype, trailing shape builder)
+    "ray_o": (np.float64, lambda d: (3,)), "ray_d": (np.float64, lambda d: (3,)),
+    "beta": (np.float64, lambda d: (3,)), "radiance": (np.float64, lambda d: (3,)),
+    "key": (np.uint64, lambda d: ()), "ctr": (np.uint64, lambda d: ()),
+    "alive": (np.uint8, lambda d: ()), "prev_pdf": (np.float64, lambda d: ()),
+    "rec_pos": (np.float64, lambda d: (d + 1, 3)), "rec_T": (np.float64, lambda d: (d + 1, 3)),
+    "emit_le": (np.float64, lambda d: (3,)), "emit_depth": (np.int32, lambda d: ()),
+}
+
+
+class PathState:
+    """SoA wavefront state in HBM (wavefront.py:53-71).  Attribute access
+    returns numpy copies; ``dev[name]`` is the device tensor."""
+
+    def __init__(self, n_paths, max_depth, camera_pos):
+        self.n = int(n_paths)
+        self.max_depth = int(max_depth)
+        self.dev = {}
+        for name, (dt, shp) in _STATE.items():
+            self.dev[name] = _dev.zeros((self.n,) + shp(self.max_depth), dt)
+        self.dev["beta"].fill_(1.0)
+        self.dev["alive"].fill_(1)
+        self.dev["prev_pdf"].fill_(-1.0)
+        cp = np.asarray(camera_pos, dtype=np.float64)
+        self.dev["rec_pos"][:, 0] = _dev.upload(cp)
+        self.pixel = np.arange(self.n, dtype=np.int64)
+
+    def abi(self):
+        p = _lib.Paths()
+        p.n = self.n
+        p.max_depth = self.max_depth
+        for name in _STATE:
+            setattr(p, name, self.dev[name].data_ptr())
+        return p
+
+    def __getattr__(self, name):
+        if name in _STATE and "dev" in self.__dict__:
+            a = _dev.download(self.dev[name])
+            return a.astype(bool) if name == "alive" else a
+        raise AttributeError(name)
+
+
+@dataclass
+class SpatialBin:
+    node: int
+    level: int
+    members: np.ndarray
+
+
+@dataclass
+class PassStats:
+    bins_per_depth: list = field(default_factory=list)
+    rays_per_depth: list = field(default_factory=list)
+    material_groups: list = field(default_factory=list)
+    live_per_depth: list = field(default_factory=list)
+    deposits: int = 0
+
+
+def partition_material(mat_ids, path_idx):
+    """Stable grouping of live paths by material id (stats only)."""
+    order = np.argsort(mat_ids, kind="stable")
+    srt = mat_ids[order]
+    return {int(m): path_idx[order[np.searchsorted(srt, m, "left"):np.searchsorted(srt, m, "right")]]
+            for m in np.unique(mat_ids)}
+
+
+def partition_spatial(svo, positions, path_idx, l_min, c_ray):
+    """Alg. 2 positional binning (wavefront.py:98-157) on the device; returns
+    SpatialBin records ordered by node id with members in path order."""
+    if l_min >= svo.depth:
+        raise ValueError("l_min must be below the SVO depth")
+    path_idx = np.asarray(path_idx)
+    n = len(path_idx)
+    if n == 0:
+        return []
+    pos = _dev.upload(np.asarray(positions, dtype=np.float64).reshape(n, 3))
+    pidx = _dev.upload(path_idx, np.int32)
+    cap = n
+    node = _dev.empty((cap,), np.int32)
+    start = _dev.empty((cap,), np.int32)
+    count = _dev.empty((cap,), np.int32)
+    members = _dev.empty((n,), np.int32)
+    nb = _dev.zeros((1,), np.int32)
+    ws = _dev.workspace(_lib.load().wfpg_partition_workspace_bytes(n, svo.node_count))
+    _lib.call("wfpg_partition_spatial", C.byref(svo.abi()), _lib.ptr(pos), _lib.ptr(pidx), n,
+              None, int(l_min), int(c_ray), _lib.ptr(node), _lib.ptr(start), _lib.ptr(count),
+              _lib.ptr(members), _lib.ptr(nb), cap, _lib.ptr(ws), ws.numel(), _dev.stream())
+    k = int(_dev.download(nb)[0])
+    node_h = _dev.download(node[:k]).astype(np.int64)
+    start_h = _dev.download(start[:k])
+    count_h = _dev.download(count[:k])
+    mem_h = _dev.download(members).astype(np.int64)
+    levels = np.searchsorted(svo.level_off, node_h, side="right") - 1
+    return [SpatialBin(int(node_h[b]), int(levels[b]), mem_h[start_h[b]:start_h[b] + count_h[b]])
+            for b in range(k)]
+
+
+def bin_stream_id(sample_index, depth, node_id):
+    sid = ((sample_index * 64 + depth) << 32) + node_id
+    return sid * PATH_STREAM_SPACE + BIN_STREAM_TAG
+
+
+def bin_stream(cfg_seed, sample_index, depth, node_id):
+    return core.RngStream(cfg_seed, bin_stream_id(sample_index, depth, node_id))
+
+
+class PassRunner:
+    """Owns the device buffers of repeated passes with one configuration
+    (path state, frame, workspace) so that steady-state rendering allocates
+    nothing.  ``render_pass`` uses a cached runner per (scene, svo, cfg)."""
+
+    def __init__(self, scene, svo, cfg, n_samples=1, deterministic=True):
+        cam = scene.camera
+        self.scene = scene
+        self.svo = svo
+        self.cfg = cfg
+        self.n_samples = int(n_samples)
+        self.n_pix = cam.width * cam.height
+        self.P = self.n_pix * self.n_samples
+        self.cam = cam.as_abi()
+        self.state = PathState(self.P, cfg.max_depth, cam.position)
+        self.frame = _dev.zeros((self.n_pix, 3), np.float64)
+        self.pc = _lib.PassConfig()
+        pc = self.pc
+        pc.l_min, pc.c_ray, pc.field_res = int(cfg.l_min), int(cfg.c_ray), int(cfg.field_res)
+        pc.guided_depths, pc.max_depth = int(cfg.guided_depths), int(cfg.max_depth)
+        pc.product, pc.jitter = int(bool(cfg.product)), int(bool(cfg.jitter))
+        pc.blur_sigma, pc.epsilon = float(cfg.blur_sigma), float(cfg.epsilon)
+        pc.russian_roulette, pc.rr_depth = int(bool(cfg.russian_roulette)), int(cfg.rr_depth)
+        pc.seed = int(cfg.seed) & 0xFFFFFFFFFFFFFFFF
+        pc.n_samples = self.n_samples
+        pc.deterministic = 1 if deterministic else 0
+        radius, taps = guiding.blur_params(cfg.blur_sigma)
+        pc.blur_radius = radius
+        for i, w in enumerate(taps[:2 * radius + 1] if radius else []):
+            pc.blur_w[i] = float(w)
+        pc.upper_dirs = guiding.upper_dirs_device().data_ptr() if cfg.product else None
+        self.svo_abi = svo.abi() if svo is not None else None
+        nbytes = _lib.load().wfpg_render_workspace_bytes(
+            C.byref(scene.abi()), C.byref(self.svo_abi) if svo is not None else None,
+            C.byref(self.cam), C.byref(pc))
+        self.ws = _dev.workspace(nbytes)
+        self.stats = _lib.PassStats()
+
+    def launch(self, sample_index, want_stats=True):
+        """Enqueue one pass; with want_stats the call synchronises and fills self.stats."""
+        self.pc.sample_index = int(sample_index)
+        _lib.call("wfpg_render_pass", C.byref(self.scene.abi()),
+                  C.byref(self.svo_abi) if self.svo is not None else None, C.byref(self.cam),
+                  C.byref(self.pc), C.byref(self.state.abi()), _lib.ptr(self.frame),
+                  C.byref(self.stats) if want_stats else None, _lib.ptr(self.ws),
+                  self.ws.numel(), _dev.stream())
+
+    def pass_stats(self):
+        s = self.stats
+        st = PassStats()
+        for d in range(s.depths_run):
+            st.live_per_depth.append(int(s.live_per_depth[d]))
+            if self.svo is not None:
+                st.bins_per_depth.append(int(s.bins_per_depth[d]))
+                st.rays_per_depth.append(int(s.rays_per_depth[d]))
+                groups = {m: int(s.mat_groups[d][m]) for m in range(16) if s.mat_groups[d][m]}
+                st.material_groups.append(groups)
+        st.deposits = int(s.deposits)
+        return st
+
+
+_RUNNERS = {}
+
+
+def _runner(scene, svo, cfg, n_samples):
+    key = (id(scene), id(svo), tuple(sorted(vars(cfg).items())), n_samples)
+    r = _RUNNERS.get(key)
+    if r is None or r.scene is not scene or r.svo is not svo:
+        _RUNNERS.clear()  # one live configuration at a time keeps HBM bounded
+        r = PassRunner(scene, svo, cfg, n_samples)
+        _RUNNERS[key] = r
+    return r
+
+
+def render_pass(scene, svo, cfg, sample_indices, collect_bin_image=False):
+    """One wavefront pass over every pixel for each sample index (consecutive
+    indices); returns (frame (H,W,3), PassStats)."""
+    samples = np.asarray(sample_indices, dtype=np.int64).reshape(-1)
+    if len(samples) == 0:
+        raise ValueError("render_pass needs at least one sample index")
+    if np.any(np.diff(samples) != 1):
+        raise ValueError("render_pass on the device takes consecutive sample indices")
+    if collect_bin_image:
+        raise NotImplementedError("collect_bin_image is not supported by the device pass yet")
+    if svo is not None:
+        cfg.validate(svo.depth)
+    r = _runner(scene, svo, cfg, len(samples))
+    r.launch(int(samples[0]))
+    cam = scene.camera
+    frame = _dev.download(r.frame).reshape(cam.height, cam.width, 3)
+    return frame, r.pass_stats()
+
+
+def render_sample(scene, svo, cfg, sample_index):
+    frame, _ = render_pass(scene, svo, cfg, [sample_index])
+    return frame
+
+
+def update_exitance(state, svo, deterministic=True):
+    """Eq. 5 back-propagation of emitter radiance into the SVO leaves
+    (wavefront.py:286-332), followed by the bottom-up refresh.  Returns the
+    number of deposits."""
+    n_dep = _dev.zeros((1,), np.int32)
+    ws = _dev.workspace(_lib.load().wfpg_update_exitance_workspace_bytes(state.n, state.max_depth))
+    _lib.call("wfpg_update_exitance", C.byref(svo.abi()), C.byref(state.abi()),
+              1 if deterministic else 0, _lib.ptr(n_dep), _lib.ptr(ws), ws.numel(),
+              _dev.stream())
+    return int(_dev.download(n_dep)[0])

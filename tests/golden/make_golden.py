@@ -103,6 +103,162 @@ def gen_svo():
     save("svo_golden.npz", **out)
 
 
+# ---------------------------------------------------------------------------
+RENDER_CFG = dict(W=32, H=32, R=64, svo_seed=0, max_depth=4, field_res=32, l_min=3, c_ray=16,
+                  seed=7)
+
+
+def _capture_pass(scene, tree, cfg, sample):
+    """Run the reference render_pass and capture PathState, guide tables and bins."""
+    cap = {"tables": {}, "bins": {}}
+    orig_update = wavefront.update_exitance
+    orig_build = wavefront._build_guide_tables
+    orig_part = wavefront.partition_spatial
+
+    def upd(state, svo):
+        cap["state"] = {k: getattr(state, k).copy() for k in
+                        ("radiance", "rec_pos", "rec_T", "emit_le", "emit_depth", "ray_o",
+                         "ray_d", "beta", "ctr", "alive", "prev_pdf")}
+        return orig_update(state, svo)
+
+    depth_box = [0]
+
+    def part(svo, positions, path_idx, l_min, c_ray):
+        depth_box[0] += 1
+        bins = orig_part(svo, positions, path_idx, l_min, c_ray)
+        cap["bins"][depth_box[0]] = (np.array([b.node for b in bins], dtype=np.int64),
+                                     [b.members.copy() for b in bins],
+                                     positions.copy(), path_idx.copy())
+        return bins
+
+    def build(svo, scene_, cfg_, bins, pos, sample_index, depth, n_paths):
+        tables, slot = orig_build(svo, scene_, cfg_, bins, pos, sample_index, depth, n_paths)
+        keys = core.stream_key(np.uint64(cfg_.seed), np.array(
+            [wavefront.bin_stream_id(sample_index, depth, b.node) for b in bins], dtype=np.uint64))
+        origins = np.array([pos[b.members[min(int(core.u01_at(k, np.uint64(0)) * len(b.members)),
+                                              len(b.members) - 1)]] for k, b in zip(keys, bins)])
+        jit = np.stack([core.u01_at(keys, np.uint64(1)), core.u01_at(keys, np.uint64(2))], axis=1)
+        cap["tables"][depth] = (tables, slot.copy(), origins, jit)
+        return tables, slot
+
+    wavefront.update_exitance = upd
+    wavefront._build_guide_tables = build
+    wavefront.partition_spatial = part
+    try:
+        frame, stats = wavefront.render_pass(scene, tree, cfg, [sample])
+    finally:
+        wavefront.update_exitance = orig_update
+        wavefront._build_guide_tables = orig_build
+        wavefront.partition_spatial = orig_part
+    return frame, stats, cap
+
+
+def _svo_state(tree):
+    return {k: getattr(tree, k).copy() for k in ("sum_a", "sum_b", "weight_a", "weight_b",
+                                                  "mean_a", "mean_b")}
+
+
+def gen_render():
+    c = RENDER_CFG
+    sc = load_scene("cornell.scene", c["W"], c["H"])
+    tree = rsvo.build_from_scene(sc, c["R"], seed=c["svo_seed"])
+    out = {"cfg_keys": np.array(list(c)), "cfg_vals": np.array(list(c.values()))}
+    pt_cfg = wavefront.GuidingConfig(max_depth=c["max_depth"], guided_depths=0,
+                                     field_res=c["field_res"], l_min=c["l_min"],
+                                     c_ray=c["c_ray"], seed=c["seed"])
+    f0, st0, cap0 = _capture_pass(sc, tree, pt_cfg, 0)
+    out["p0_frame"] = f0
+    for k, v in cap0["state"].items():
+        out["p0_" + k] = v
+    for k, v in _svo_state(tree).items():
+        out["p0_svo_" + k] = v
+    out["p0_bins_per_depth"] = np.array(st0.bins_per_depth)
+    out["p0_rays_per_depth"] = np.array(st0.rays_per_depth)
+    for d, (nodes, members, pos, pidx) in cap0["bins"].items():
+        out[f"p0_d{d}_bin_nodes"] = nodes
+        out[f"p0_d{d}_bin_sizes"] = np.array([len(m) for m in members])
+        out[f"p0_d{d}_bin_members"] = (np.concatenate(members) if members
+                                       else np.zeros(0, dtype=np.int64))
+        out[f"p0_d{d}_positions"] = pos
+        out[f"p0_d{d}_path_idx"] = pidx
+    base_state = _svo_state(tree)
+    for tag, product in (("p1", False), ("p1x", True)):
+        for k, v in base_state.items():
+            setattr(tree, k, v.copy())
+        g_cfg = wavefront.GuidingConfig(max_depth=c["max_depth"], guided_depths=c["max_depth"],
+                                        field_res=c["field_res"], l_min=c["l_min"],
+                                        c_ray=c["c_ray"], seed=c["seed"], product=product)
+        f1, st1, cap1 = _capture_pass(sc, tree, g_cfg, 1)
+        out[tag + "_frame"] = f1
+        for k, v in cap1["state"].items():
+            out[f"{tag}_{k}"] = v
+        for k, v in _svo_state(tree).items():
+            out[f"{tag}_svo_" + k] = v
+        out[tag + "_bins_per_depth"] = np.array(st1.bins_per_depth)
+        out[tag + "_rays_per_depth"] = np.array(st1.rays_per_depth)
+        for d, (tables, slot, origins, jit) in cap1["tables"].items():
+            out[f"{tag}_d{d}_origins"] = origins
+            out[f"{tag}_d{d}_jitters"] = jit
+            out[f"{tag}_d{d}_bin_slot"] = slot
+            for k in ("marg", "cond", "pdftab", "vals", "block_sums", "blk_marg", "blk_cond"):
+                out[f"{tag}_d{d}_{k}"] = getattr(tables, k)
+        print(tag, "bins", st1.bins_per_depth, "rays", st1.rays_per_depth)
+    # cone queries against the PT-first exitance state
+    for k, v in base_state.items():
+        setattr(tree, k, v.copy())
+    rng = np.random.default_rng(11)
+    m = 4096
+    lo, hi = sc.bbox_lo, sc.bbox_hi
+    org = lo + (hi - lo) * (0.05 + 0.9 * rng.random((m, 3)))
+    dirs = rng.standard_normal((m, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    for omega in (4 * np.pi / 32 ** 2, 4 * np.pi / 128 ** 2):
+        tag = f"cone_{int(round(np.sqrt(4 * np.pi / omega)))}"
+        out[tag + "_rgb"] = wfpg.backend.get().trace_cones_multi(tree, sc, org, dirs, omega)
+        out[tag + "_omega"] = np.array(omega)
+    out["cone_origins"] = org
+    out["cone_dirs"] = dirs
+    # intersection queries
+    t, tri = sc.intersect_batch(org, dirs)
+    out["isect_t"] = t
+    out["isect_tri"] = tri
+    occ = sc.occluded_batch(org, dirs, 0.5 * np.where(np.isfinite(t), t, 1e3))
+    out["occ_half"] = occ
+    save("render_golden.npz", **out)
+
+
+def gen_fields():
+    """Field generation at every resolution from fixed origins (PT-first SVO state)."""
+    c = RENDER_CFG
+    sc = load_scene("cornell.scene", c["W"], c["H"])
+    tree = rsvo.build_from_scene(sc, c["R"], seed=c["svo_seed"])
+    cfg = wavefront.GuidingConfig(max_depth=c["max_depth"], guided_depths=0, seed=c["seed"])
+    wavefront.render_pass(sc, tree, cfg, [0])
+    wavefront.render_pass(sc, tree, cfg, [1])
+    out = {}
+    for k, v in _svo_state(tree).items():
+        out["svo_" + k] = v
+    rng = np.random.default_rng(5)
+    lo, hi = sc.bbox_lo, sc.bbox_hi
+    b = 6
+    org = lo + (hi - lo) * (0.1 + 0.8 * rng.random((b, 3)))
+    jit = rng.random((b, 2))
+    out["origins"] = org
+    out["jitters"] = jit
+    for n in (8, 16, 32, 64, 128):
+        vals = guiding.generate_fields_batch(tree, sc, org, n, jit, blur_sigma=1.0)
+        out[f"vals_{n}"] = vals
+        t = guiding.GuideTables(2, n, b)
+        t.fill_batch(vals)
+        for k in ("marg", "cond", "pdftab", "block_sums", "blk_marg", "blk_cond"):
+            out[f"tab_{n}_{k}"] = getattr(t, k)
+    vals = guiding.generate_fields_batch(tree, sc, org, 16, jit, blur_sigma=2.5)
+    out["vals_16_s25"] = vals
+    vals = guiding.generate_fields_batch(tree, sc, org, 16, jit, blur_sigma=0.0)
+    out["vals_16_s0"] = vals
+    save("fields_golden.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["svo"]
     for w in which:
