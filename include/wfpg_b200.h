@@ -168,6 +168,17 @@ typedef struct wfpg_pass_config {
   int32_t blur_radius;       /* core._blur_kernel radius (0: no blur) */
   double blur_w[33];         /* normalised blur taps, computed by numpy on the host */
   const double* upper_dirs;  /* device (8,8,3) guiding.UPPER_DIRS, product mode only */
+  /* Image tiling (multi-GPU): this pass renders pixels [pixel_offset,
+   * pixel_offset + n_pixels) of the camera image; RNG streams use the global
+   * pixel index, so every path draws what it would draw on one GPU.
+   * n_pixels = 0 renders the whole image. */
+  int64_t pixel_offset;
+  int64_t n_pixels;
+  /* When non-NULL the Eq. 5 deposits of this pass go to this zeroed leaf
+   * buffer (8 doubles per leaf: sum_a[3], sum_b[3], weight_a, weight_b as
+   * four planes) instead of the SVO, and the bottom-up refresh is skipped;
+   * the caller all-reduces it and applies it with wfpg_svo_apply_leaf_acc. */
+  double* leaf_acc;
 } wfpg_pass_config;
 
 /* Per-pass statistics returned to the host: wavefront.py:81-85 (PassStats). */
@@ -259,6 +270,10 @@ int wfpg_svo_accumulate(wfpg_svo* svo, const int32_t* leaf, const double* dirs,
  * bitwise equal to the reference's dirty-only update. */
 int wfpg_svo_propagate(wfpg_svo* svo, void* stream);
 
+/* Adds an (all-reduced) leaf accumulator buffer into the SVO leaf sums and
+ * refreshes every mean bottom-up (multi-GPU exitance exchange). */
+int wfpg_svo_apply_leaf_acc(wfpg_svo* svo, const double* leaf_acc, void* stream);
+
 /* wavefront.py:286-332 (update_exitance) over a finished pass. */
 size_t wfpg_update_exitance_workspace_bytes(int64_t n_paths, int32_t max_depth);
 int wfpg_update_exitance(wfpg_svo* svo, const wfpg_paths* paths, int32_t deterministic,
@@ -341,6 +356,12 @@ size_t wfpg_render_workspace_bytes(const wfpg_scene* scene, const wfpg_svo* svo,
 int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camera* cam,
                      const wfpg_pass_config* cfg, wfpg_paths* paths, double* frame,
                      wfpg_pass_stats* stats, void* workspace, size_t ws_bytes, void* stream);
+
+/* Live timing of the per-depth field kernels inside wfpg_render_pass (CUDA
+ * events on the pass stream; collected when a pass returns stats).
+ * field_ms / cones / launches have max_depth+1 entries indexed by depth. */
+int wfpg_profile_enable(int32_t on);
+int wfpg_profile_read(double* field_ms, double* cones, int64_t* launches, int32_t max_depth);
 
 #ifdef __cplusplus
 }

@@ -80,6 +80,7 @@ class PassConfig(C.Structure):
         ("seed", c_u64), ("sample_index", c_i64), ("n_samples", c_i32),
         ("deterministic", c_i32),
         ("blur_radius", c_i32), ("blur_w", c_dbl * 33), ("upper_dirs", c_vp),
+        ("pixel_offset", c_i64), ("n_pixels", c_i64), ("leaf_acc", c_vp),
     ]
 
 
@@ -116,6 +117,7 @@ _SIGS = {
     "wfpg_svo_accumulate": (c_i32, [P(Svo), c_vp, c_vp, c_vp, c_i64, c_vp, c_i32, c_vp, c_size,
                                     c_vp]),
     "wfpg_svo_propagate": (c_i32, [P(Svo), c_vp]),
+    "wfpg_svo_apply_leaf_acc": (c_i32, [P(Svo), c_vp, c_vp]),
     "wfpg_update_exitance_workspace_bytes": (c_size, [c_i64, c_i32]),
     "wfpg_update_exitance": (c_i32, [P(Svo), P(Paths), c_i32, c_vp, c_vp, c_size, c_vp]),
     "wfpg_trace_cones": (c_i32, [P(Scene), P(Svo), c_vp, c_i32, c_vp, c_i64, c_dbl, c_vp, c_vp]),
@@ -134,6 +136,8 @@ _SIGS = {
     "wfpg_render_workspace_bytes": (c_size, [P(Scene), P(Svo), P(Camera), P(PassConfig)]),
     "wfpg_render_pass": (c_i32, [P(Scene), P(Svo), P(Camera), P(PassConfig), P(Paths), c_vp,
                                  P(PassStats), c_vp, c_size, c_vp]),
+    "wfpg_profile_enable": (c_i32, [c_i32]),
+    "wfpg_profile_read": (c_i32, [P(c_dbl), P(c_dbl), P(c_i64), c_i32]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -28,7 +28,8 @@ __device__ __forceinline__ int fold_index(int raw, int n, bool* flip) {
 template <int N>
 struct FieldCfg {
   static constexpr int kStride = N + 1;  // padded rows: conflict-free column walks
-  static constexpr int kThreads = N >= 128 ? 512 : (N >= 64 ? 512 : (N >= 16 ? 256 : 128));
+  // one warp per 8x4-cell tile at most: N=8 has 2 tiles, N=16 8, N=32 32
+  static constexpr int kThreads = N >= 64 ? 512 : (N == 32 ? 256 : (N == 16 ? 128 : 64));
   static constexpr int kPerLane = (N + 31) / 32;
 };
 
@@ -118,27 +119,40 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads)
              const double* __restrict__ jitters, int64_t nb_max, const int32_t* __restrict__ nb_dev,
              BlurParams bp, FieldOut out) {
   constexpr int S = FieldCfg<N>::kStride;
+  // warp tiles of 8 (u) x 4 (v) cells: the 32 cones of a warp are angularly
+  // coherent, so whole-warp triangle culling is effective
+  constexpr int TU = 8, TV = 4, TILES_U = N / TU, TILES = (N / TU) * (N / TV);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* F = reinterpret_cast<double*>(smem_raw);
   double* rs = F + N * S;  // row sums (N)
-  TriRec* smt = reinterpret_cast<TriRec*>(rs + N);
-  if (s.brute) load_tris_smem(s, smt);
-  __syncthreads();
+  TriBin* tb = reinterpret_cast<TriBin*>(rs + N);
   const int64_t nb = dev_count(nb_max, nb_dev);
   const double omega = 4.0 * WFPG_PI / (double)(N * N);  // guiding.py:246
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
     const double ox = origins[3 * b], oy = origins[3 * b + 1], oz = origins[3 * b + 2];
     const double ju = __ddiv_rn(jitters[2 * b], (double)N);
     const double jv = __ddiv_rn(jitters[2 * b + 1], (double)N);
+    if (s.brute) {
+      for (int t = threadIdx.x; t < s.n_tris; t += blockDim.x) make_tri_bin(s, t, ox, oy, oz, tb[t]);
+      __syncthreads();
+    }
     // 1. cone-trace every cell: u = i/n + ju/n, v = j/n + jv/n (guiding.py:239-244)
-    for (int c = threadIdx.x; c < N * N; c += blockDim.x) {
-      const int j = c / N, i = c % N;
+    for (int tile = warp; tile < TILES; tile += nwarps) {
+      const int i = (tile % TILES_U) * TU + (lane % TU);
+      const int j = (tile / TILES_U) * TV + (lane / TU);
       double u = __dadd_rn(__ddiv_rn((double)i, (double)N), ju);
       double w = __dadd_rn(__ddiv_rn((double)j, (double)N), jv);
       double dx, dy, dz;
       octa_uv_to_dir_np(u, w, &dx, &dy, &dz);
-      double rgb[3];
-      cone_query(s, smt, v, ox, oy, oz, dx, dy, dz, omega, rgb);
+      double rgb[3] = {0.0, 0.0, 0.0};
+      double bt;
+      int32_t bid;
+      if (s.brute)
+        warp_nearest_bin(tb, s.n_tris, dx, dy, dz, s.ray_eps, &bt, &bid);
+      else
+        bvh_nearest(s, ox, oy, oz, dx, dy, dz, s.ray_eps, &bt, &bid);
+      if (bid >= 0) cone_shade_hit(v, ox, oy, oz, dx, dy, dz, bt, omega, rgb);
       F[j * S + i] = luminance_rows(rgb[0], rgb[1], rgb[2]);
     }
     __syncthreads();
@@ -195,7 +209,7 @@ static int launch_fields_n(const SceneView& s, const SvoView& v, const double* o
                            const BlurParams& bp, const FieldOut& out, cudaStream_t st) {
   constexpr int T = FieldCfg<N>::kThreads;
   size_t smem = sizeof(double) * (N * FieldCfg<N>::kStride + N) +
-                (s.brute ? sizeof(TriRec) * s.n_tris : 0);
+                (s.brute ? sizeof(TriBin) * s.n_tris : 0);
   static bool configured = false;
   if (!configured) {
     WFPG_CUDA(cudaFuncSetAttribute(k_fields<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,

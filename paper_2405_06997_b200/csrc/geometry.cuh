@@ -249,6 +249,109 @@ __device__ __forceinline__ bool bvh_occluded(const SceneView& b, double ox, doub
   return false;
 }
 
+// Per-(origin, triangle) record for rays that share one origin (all cones of a
+// field bin).  tvec = o - v0, q = tvec x e1 and ts0 = e2 . q depend only on the
+// origin, so the per-ray Moeller-Trumbore test reduces to p = d x e2 and three
+// dot products with the same operands as _kernels.pyx:63-81.  `axis` /
+// `cos_lim` bound the triangle's directions from o (a cone containing the
+// three vertex directions, widened by 1e-6 rad); a ray outside that cone
+// cannot hit the triangle, which lets a warp skip triangles none of its 32
+// rays can reach.  cos_lim = -2 disables the cull (origin too close).
+struct TriBin {
+  double e1x, e1y, e1z, e2x, e2y, e2z;
+  double tx, ty, tz, qx, qy, qz, ts0;
+  double ax, ay, az, cos_lim;
+};
+
+__device__ __forceinline__ void make_tri_bin(const SceneView& s, int t, double ox, double oy,
+                                             double oz, TriBin& B) {
+  const double* v0 = s.v0 + 3 * t;
+  const double* e1 = s.e1 + 3 * t;
+  const double* e2 = s.e2 + 3 * t;
+  B.e1x = e1[0];
+  B.e1y = e1[1];
+  B.e1z = e1[2];
+  B.e2x = e2[0];
+  B.e2y = e2[1];
+  B.e2z = e2[2];
+  B.tx = ox - v0[0];
+  B.ty = oy - v0[1];
+  B.tz = oz - v0[2];
+  B.qx = B.ty * B.e1z - B.tz * B.e1y;
+  B.qy = B.tz * B.e1x - B.tx * B.e1z;
+  B.qz = B.tx * B.e1y - B.ty * B.e1x;
+  B.ts0 = B.e2x * B.qx + B.e2y * B.qy + B.e2z * B.qz;
+  // bounding cone of the vertex directions
+  double w[3][3];
+  double cx = 0.0, cy = 0.0, cz = 0.0;
+  bool degenerate = false;
+  for (int k = 0; k < 3; ++k) {
+    double px = v0[0] + (k == 1 ? e1[0] : (k == 2 ? e2[0] : 0.0)) - ox;
+    double py = v0[1] + (k == 1 ? e1[1] : (k == 2 ? e2[1] : 0.0)) - oy;
+    double pz = v0[2] + (k == 1 ? e1[2] : (k == 2 ? e2[2] : 0.0)) - oz;
+    double len = sqrt(px * px + py * py + pz * pz);
+    if (!(len > 1e-9 * s.ray_eps)) degenerate = true;
+    double inv = 1.0 / len;
+    w[k][0] = px * inv;
+    w[k][1] = py * inv;
+    w[k][2] = pz * inv;
+    cx += w[k][0];
+    cy += w[k][1];
+    cz += w[k][2];
+  }
+  double cl = sqrt(cx * cx + cy * cy + cz * cz);
+  B.cos_lim = -2.0;
+  B.ax = 0.0;
+  B.ay = 0.0;
+  B.az = 1.0;
+  if (!degenerate && cl > 1e-6) {
+    B.ax = cx / cl;
+    B.ay = cy / cl;
+    B.az = cz / cl;
+    double cmin = 1.0;
+    for (int k = 0; k < 3; ++k)
+      cmin = fmin(cmin, B.ax * w[k][0] + B.ay * w[k][1] + B.az * w[k][2]);
+    if (cmin > 1e-3) B.cos_lim = cos(fmin(acos(fmin(cmin, 1.0)) + 1e-6, 0.5 * WFPG_PI));
+  }
+}
+
+// _kernels.pyx:63-81 with the origin-dependent terms precomputed.
+__device__ __forceinline__ double mt_bin(const TriBin& B, double dx, double dy, double dz,
+                                         double tmin) {
+  double px = dy * B.e2z - dz * B.e2y;
+  double py = dz * B.e2x - dx * B.e2z;
+  double pz = dx * B.e2y - dy * B.e2x;
+  double det = B.e1x * px + B.e1y * py + B.e1z * pz;
+  double s = det > 0.0 ? 1.0 : -1.0;
+  double ad = det * s;
+  double us = (B.tx * px + B.ty * py + B.tz * pz) * s;
+  double vs = (dx * B.qx + dy * B.qy + dz * B.qz) * s;
+  double ts = B.ts0 * s;
+  bool ok = (ad > 1e-300) & (us >= 0.0) & (vs >= 0.0) & (us + vs <= ad) & (ts > tmin * ad);
+  return ok ? ts / ad : -1.0;
+}
+
+// Nearest hit for one lane of a warp whose rays share the origin; triangles
+// no lane can reach are skipped warp-uniformly.  Same result as brute force.
+__device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, int n, double dx,
+                                                 double dy, double dz, double tmin, double* bt,
+                                                 int32_t* bid) {
+  double best = 1e300;
+  int32_t id = -1;
+  for (int t = 0; t < n; ++t) {
+    const TriBin& B = tb[t];
+    bool maybe = dx * B.ax + dy * B.ay + dz * B.az >= B.cos_lim;
+    if (!__any_sync(0xffffffffu, maybe)) continue;
+    double h = mt_bin(B, dx, dy, dz, tmin);
+    if (h > 0.0 && h < best) {
+      best = h;
+      id = t;
+    }
+  }
+  *bt = best;
+  *bid = id;
+}
+
 // Brute-force any-hit (wfpg_brute_occluded, _kernels.pyx:99-138).
 __device__ __forceinline__ bool brute_occluded(const TriRec* __restrict__ tris, int n, double ox,
                                                double oy, double oz, double dx, double dy,

@@ -89,11 +89,16 @@ __global__ void k_part_bins(const uint64_t* __restrict__ keys, const uint32_t* _
                             const int32_t* __restrict__ path_idx, int64_t n_max,
                             const int32_t* __restrict__ n_dev, int64_t cap,
                             int32_t* __restrict__ bin_node, int32_t* __restrict__ bin_start,
-                            int32_t* __restrict__ members) {
+                            int32_t* __restrict__ members, int32_t* __restrict__ bin_slot,
+                            const int32_t* __restrict__ item_path) {
   const int64_t n = dev_count(n_max, n_dev);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     if (members) members[i] = path_idx ? path_idx[vals[i]] : (int32_t)vals[i];
+    if (bin_slot) {
+      uint32_t b = scan[i] + flags[i] - 1u;  // bin of this sorted position
+      if (b < cap) bin_slot[item_path[vals[i]]] = (int32_t)b;
+    }
     if (flags[i]) {
       uint32_t b = scan[i];
       if (b < cap) {
@@ -170,7 +175,8 @@ int partition_spatial(const SvoView& v, int32_t* counter, const int32_t* parent,
     ws.off = mark;
   }
   k_part_bins<<<grid, 256, 0, st>>>(keys, vals, flags, scan, path_idx, n_max, n_dev, out.capacity,
-                                    out.bin_node, out.bin_start, out.members);
+                                    out.bin_node, out.bin_start, out.members, out.bin_slot,
+                                    out.item_path);
   WFPG_CHECK_LAUNCH("k_part_bins");
   int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(out.capacity, 256), kNumSMs * 4));
   k_part_counts<<<bgrid, 256, 0, st>>>(out.bin_start, nb, n_max, n_dev, out.capacity,
@@ -213,7 +219,7 @@ extern "C" int wfpg_partition_spatial(wfpg_svo* svo, const double* positions,
   cudaStream_t st = as_stream(stream);
   WFPG_CUDA(cudaMemsetAsync(overflow, 0, sizeof(int32_t), st));
   PartitionOut out{bin_node, bin_start, bin_count, members, n_bins_dev, overflow, bin_capacity,
-                   nullptr};
+                   nullptr, nullptr, nullptr};
   WFPG_TRY(partition_spatial(make_view(svo), svo->counter, svo->parent, positions, path_idx, n,
                              n_dev, l_min, c_ray, (int)svo->n_nodes, out, ws, st));
   int32_t ov = 0;

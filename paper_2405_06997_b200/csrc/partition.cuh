@@ -12,6 +12,8 @@ struct PartitionOut {
   int32_t* overflow;    // device flag, set when bins > capacity (optional)
   int64_t capacity;
   const uint32_t* sorted_items;  // out: item index per sorted position
+  int32_t* bin_slot;    // optional (P,): slot of every member path, indexed by path id
+  const int32_t* item_path;  // path id per item (required with bin_slot)
 };
 
 size_t partition_ws_bytes(int64_t n);

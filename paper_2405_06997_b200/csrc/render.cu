@@ -10,6 +10,7 @@
 #include "fields.cuh"
 #include "partition.cuh"
 #include "prims.cuh"
+#include "svo_query.cuh"
 #include "wavefront.cuh"
 
 namespace wfpg {
@@ -123,8 +124,6 @@ __global__ void k_bin_setup(const int32_t* __restrict__ n_bins, const int32_t* _
     origins[3 * b + 2] = lam_pos[3 * (int64_t)item + 2];
     jitters[2 * b] = jitter ? u01(key, 1) : 0.5;
     jitters[2 * b + 1] = jitter ? u01(key, 2) : 0.5;
-    if (bin_slot)
-      for (int64_t j = s0; j < s0 + len; ++j) bin_slot[lam[sorted_items[j]]] = (int32_t)b;
   }
 }
 
@@ -182,7 +181,7 @@ static int64_t bin_capacity(const wfpg_svo* svo, const wfpg_pass_config* cfg, in
 
 static void carve_pass(Arena& a, const wfpg_svo* svo, const wfpg_camera* cam,
                        const wfpg_pass_config* cfg, PassLayout& L) {
-  L.n_pix = (int64_t)cam->width * cam->height;
+  L.n_pix = cfg->n_pixels > 0 ? cfg->n_pixels : (int64_t)cam->width * cam->height;
   L.P = L.n_pix * std::max(1, cfg->n_samples);
   L.cap = bin_capacity(svo, cfg, L.P);
   L.n0 = std::max(8, cfg->field_res);
@@ -219,6 +218,51 @@ static void carve_pass(Arena& a, const wfpg_svo* svo, const wfpg_camera* cam,
   size_t scratch = std::max(scan_ws_bytes(P + 1), partition_ws_bytes(P));
   if (svo) scratch = std::max(scratch, update_exitance_ws_bytes(P, cfg->max_depth));
   a.take<char>((int64_t)scratch);
+}
+
+// Optional live timing of the field kernels: CUDA events on the pass stream
+// plus an async copy of the device bin count into pinned memory, kept in a
+// ring and folded into totals by wfpg_profile_read (no per-pass host sync).
+struct ProfRec {
+  cudaEvent_t a, b;
+  int32_t* nb_host;
+  int n, depth;
+};
+struct Profile {
+  bool on = false;
+  ProfRec* ring = nullptr;
+  int cap = 0, used = 0;
+  double field_ms[kMaxDepth + 1];
+  double cones[kMaxDepth + 1];
+  int64_t launches[kMaxDepth + 1];
+};
+static Profile g_prof;
+
+static void prof_alloc() {
+  if (!g_prof.ring) {
+    g_prof.cap = 4096;
+    g_prof.ring = new ProfRec[g_prof.cap];
+    for (int i = 0; i < g_prof.cap; ++i) {
+      cudaEventCreate(&g_prof.ring[i].a);
+      cudaEventCreate(&g_prof.ring[i].b);
+      cudaMallocHost(&g_prof.ring[i].nb_host, sizeof(int32_t));
+    }
+  }
+}
+
+static ProfRec* prof_begin(cudaStream_t st, int depth) {
+  if (!g_prof.on || !g_prof.ring) return nullptr;
+  if (g_prof.used >= g_prof.cap) return nullptr;
+  ProfRec* r = &g_prof.ring[g_prof.used++];
+  r->depth = depth;
+  cudaEventRecord(r->a, st);
+  return r;
+}
+static void prof_end(ProfRec* r, cudaStream_t st, int n, const int32_t* nb_dev) {
+  if (!r) return;
+  cudaEventRecord(r->b, st);
+  cudaMemcpyAsync(r->nb_host, nb_dev, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+  r->n = n;
 }
 
 static bool cfg_ok(const wfpg_pass_config* cfg) {
@@ -285,7 +329,13 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(P, 256), kNumSMs * 8));
 
   WFPG_CUDA(cudaMemsetAsync(L.stats, 0, sizeof(StatsDev), st));
-  WFPG_TRY(launch_camera_init(cv, pv, P, L.n_pix, cfg->sample_index, cfg->seed, st));
+  const int64_t n_img = (int64_t)cam->width * cam->height;
+  if (cfg->pixel_offset < 0 || cfg->pixel_offset + L.n_pix > n_img) {
+    set_error("wfpg_render_pass: pixel range outside the image");
+    return WFPG_ERR_ARG;
+  }
+  WFPG_TRY(launch_camera_init(cv, pv, P, L.n_pix, n_img, cfg->pixel_offset, cfg->sample_index,
+                              cfg->seed, st));
 
   BlurParams bp{};
   bp.radius = cfg->blur_radius;
@@ -322,15 +372,17 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
                                               paths->ray_o, paths->ray_d, L.hit_t, L.lam,
                                               L.lam_pos, L.total, L.n_lam, &L.stats->lam[depth]);
       WFPG_CHECK_LAUNCH("k_scatter_lambert");
-      PartitionOut po{L.bin_node, L.bin_start, L.bin_count, nullptr, L.n_bins,
-                      &L.stats->overflow, L.cap, nullptr};
-      size_t mark = scratch.off;
-      WFPG_TRY(partition_spatial(vv, svo->counter, svo->parent, L.lam_pos, nullptr, P, L.n_lam,
-                                 cfg->l_min, cfg->c_ray, (int)svo->n_nodes, po, scratch, st));
       const bool guided_depth = depth <= cfg->guided_depths;
       if (guided_depth) {
         WFPG_CUDA(cudaMemsetAsync(L.bin_slot, 0xFF, sizeof(int32_t) * P, st));
       }
+      // bin slots of guided depths are written by the partition itself
+      PartitionOut po{L.bin_node, L.bin_start, L.bin_count, nullptr, L.n_bins,
+                      &L.stats->overflow, L.cap, nullptr,
+                      guided_depth ? L.bin_slot : nullptr, L.lam};
+      size_t mark = scratch.off;
+      WFPG_TRY(partition_spatial(vv, svo->counter, svo->parent, L.lam_pos, nullptr, P, L.n_lam,
+                                 cfg->l_min, cfg->c_ray, (int)svo->n_nodes, po, scratch, st));
       int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(L.cap, 128), kNumSMs * 8));
       k_bin_setup<<<bgrid, 128, 0, st>>>(L.n_bins, L.bin_node, L.bin_start, L.bin_count,
                                          po.sorted_items, L.lam, L.lam_pos, cfg->seed,
@@ -343,7 +395,9 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
         const int n = std::max(8, cfg->field_res >> (depth - 1));
         FieldOut fo{L.vals, L.row_sum, L.marg, L.tot, cfg->product ? L.block_sums : nullptr,
                     cfg->epsilon};
+        ProfRec* pr = prof_begin(st, depth);
         WFPG_TRY(launch_fields(sv, vv, L.origins, L.jitters, L.cap, L.n_bins, n, bp, fo, st));
+        prof_end(pr, st, n, L.n_bins);
         gv.mode = cfg->product ? 2 : 1;
         gv.n = n;
         gv.m = n / 8;
@@ -362,7 +416,14 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
                           cfg->russian_roulette != 0, cfg->rr_depth, st));
   }
 
-  if (svo) {
+  if (svo && cfg->leaf_acc) {
+    int64_t nleaf = svo->level_off[svo->depth + 1] - svo->level_off[svo->depth];
+    WFPG_CUDA(cudaMemsetAsync(cfg->leaf_acc, 0, sizeof(double) * 8 * nleaf, st));
+    wfpg_svo acc_view = leaf_acc_view(svo, cfg->leaf_acc);
+    WFPG_TRY(update_exitance(&acc_view, paths->emit_depth, paths->emit_le, paths->rec_T,
+                             paths->rec_pos, cfg->max_depth + 1, P, cfg->deterministic,
+                             &L.stats->deposits, scratch, st, false));
+  } else if (svo) {
     WFPG_TRY(update_exitance(svo, paths->emit_depth, paths->emit_le, paths->rec_T,
                              paths->rec_pos, cfg->max_depth + 1, P, cfg->deterministic,
                              &L.stats->deposits, scratch, st));
@@ -391,6 +452,41 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
     }
     stats->depths_run = run;
     stats->deposits = h.deposits;
+  }
+  return WFPG_OK;
+}
+
+extern "C" int wfpg_profile_enable(int32_t on) {
+  using namespace wfpg;
+  g_prof.on = on != 0;
+  g_prof.used = 0;
+  if (g_prof.on) prof_alloc();
+  for (int d = 0; d <= kMaxDepth; ++d) {
+    g_prof.field_ms[d] = 0.0;
+    g_prof.cones[d] = 0.0;
+    g_prof.launches[d] = 0;
+  }
+  return WFPG_OK;
+}
+
+// Synchronises the recorded events and returns per-depth totals since enable.
+extern "C" int wfpg_profile_read(double* field_ms, double* cones, int64_t* launches,
+                                 int32_t max_depth) {
+  using namespace wfpg;
+  for (int i = 0; i < g_prof.used; ++i) {
+    ProfRec& r = g_prof.ring[i];
+    WFPG_CUDA(cudaEventSynchronize(r.b));
+    float ms = 0.f;
+    WFPG_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    g_prof.field_ms[r.depth] += ms;
+    g_prof.cones[r.depth] += (double)(*r.nb_host) * r.n * r.n;
+    g_prof.launches[r.depth] += 1;
+  }
+  g_prof.used = 0;
+  for (int d = 0; d <= max_depth && d <= kMaxDepth; ++d) {
+    field_ms[d] = g_prof.field_ms[d];
+    cones[d] = g_prof.cones[d];
+    launches[d] = g_prof.launches[d];
   }
   return WFPG_OK;
 }

@@ -208,6 +208,41 @@ int svo_propagate(wfpg_svo* svo, cudaStream_t st) {
   return WFPG_OK;
 }
 
+__global__ void k_apply_leaf_acc(int64_t off, int64_t L, const double* __restrict__ acc,
+                                 double* sum_a, double* sum_b, double* w_a, double* w_b) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < L;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = off + k;
+    for (int c = 0; c < 3; ++c) {
+      sum_a[3 * i + c] = __dadd_rn(sum_a[3 * i + c], acc[3 * k + c]);
+      sum_b[3 * i + c] = __dadd_rn(sum_b[3 * i + c], acc[3 * L + 3 * k + c]);
+    }
+    w_a[i] = __dadd_rn(w_a[i], acc[6 * L + k]);
+    w_b[i] = __dadd_rn(w_b[i], acc[7 * L + k]);
+  }
+}
+
+int svo_apply_leaf_acc(wfpg_svo* svo, const double* acc, cudaStream_t st) {
+  int64_t off = svo->level_off[svo->depth], L = svo->level_off[svo->depth + 1] - off;
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(L, 256), (int64_t)kNumSMs * 8));
+  k_apply_leaf_acc<<<grid, 256, 0, st>>>(off, L, acc, svo->sum_a, svo->sum_b, svo->weight_a,
+                                         svo->weight_b);
+  WFPG_CHECK_LAUNCH("k_apply_leaf_acc");
+  return svo_propagate(svo, st);
+}
+
+// A view of the SVO whose leaf accumulators are redirected into a zeroed
+// per-pass leaf buffer (4 planes: sum_a, sum_b, weight_a, weight_b).
+wfpg_svo leaf_acc_view(const wfpg_svo* svo, double* acc) {
+  wfpg_svo v = *svo;
+  int64_t off = svo->level_off[svo->depth], L = svo->level_off[svo->depth + 1] - off;
+  v.sum_a = acc - 3 * off;
+  v.sum_b = acc + 3 * L - 3 * off;
+  v.weight_a = acc + 6 * L - off;
+  v.weight_b = acc + 7 * L - off;
+  return v;
+}
+
 // ---------------------------------------------------------------------------
 // cone tracer (standalone batch API; the field generator inlines cone_query)
 // ---------------------------------------------------------------------------
@@ -272,6 +307,14 @@ extern "C" int wfpg_svo_propagate(wfpg_svo* svo, void* stream) {
     return WFPG_ERR_ARG;
   }
   return svo_propagate(svo, as_stream(stream));
+}
+
+extern "C" int wfpg_svo_apply_leaf_acc(wfpg_svo* svo, const double* leaf_acc, void* stream) {
+  if (!svo_ok(svo) || !leaf_acc) {
+    set_error("wfpg_svo_apply_leaf_acc: bad arguments");
+    return WFPG_ERR_ARG;
+  }
+  return svo_apply_leaf_acc(svo, leaf_acc, as_stream(stream));
 }
 
 extern "C" int wfpg_trace_cones(const wfpg_scene* scene, const wfpg_svo* svo,

@@ -39,12 +39,12 @@ __global__ void k_camera(CameraView c, const uint64_t* __restrict__ keys,
 // Pass initialisation (wavefront.py:211-219): keys, camera rays, ctr = 2,
 // beta = 1, radiance = 0, alive, prev_pdf = -1, records, emitter slots.
 __global__ void k_init_paths(CameraView c, PathsView P, int64_t n_paths, int64_t n_pix,
-                             int64_t sample0, uint64_t seed) {
+                             int64_t n_img, int64_t pix0, int64_t sample0, uint64_t seed) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_paths;
        p += (int64_t)gridDim.x * blockDim.x) {
-    int64_t pix = p % n_pix;
+    int64_t pix = pix0 + p % n_pix;  // global pixel index
     int64_t sample = sample0 + p / n_pix;
-    uint64_t key = stream_key(seed, (uint64_t)(sample * n_pix + pix) * 4u);
+    uint64_t key = stream_key(seed, (uint64_t)(sample * n_img + pix) * 4u);
     const_cast<uint64_t*>(P.key)[p] = key;
     camera_ray(c, key, pix, P.ray_o + 3 * p, P.ray_d + 3 * p);
     P.ctr[p] = 2;
@@ -56,12 +56,7 @@ __global__ void k_init_paths(CameraView c, PathsView P, int64_t n_paths, int64_t
     P.alive[p] = 1;
     P.prev_pdf[p] = -1.0;
     P.emit_depth[p] = 0;
-    double* rp = P.rec_pos + (int64_t)p * P.rec_depths * 3;
-    double* rt = P.rec_T + (int64_t)p * P.rec_depths * 3;
-    for (int k = 0; k < 3 * P.rec_depths; ++k) {
-      rp[k] = 0.0;
-      rt[k] = 0.0;
-    }
+    double* rp = P.rec_pos + (int64_t)p * P.rec_depths * 3;  // zeroed by the launcher
     rp[0] = c.pos[0];
     rp[1] = c.pos[1];
     rp[2] = c.pos[2];
@@ -356,9 +351,13 @@ __global__ void __launch_bounds__(256) k_shade(SceneView s, GuideView g, PathsVi
 // internal launchers
 // ---------------------------------------------------------------------------
 int launch_camera_init(const CameraView& c, const PathsView& P, int64_t n_paths, int64_t n_pix,
-                       int64_t sample0, uint64_t seed, cudaStream_t st) {
+                       int64_t n_img, int64_t pix0, int64_t sample0, uint64_t seed,
+                       cudaStream_t st) {
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_paths, 256), kNumSMs * 8));
-  k_init_paths<<<grid, 256, 0, st>>>(c, P, n_paths, n_pix, sample0, seed);
+  size_t rec_bytes = sizeof(double) * 3 * (size_t)P.rec_depths * (size_t)n_paths;
+  WFPG_CUDA(cudaMemsetAsync(P.rec_pos, 0, rec_bytes, st));
+  WFPG_CUDA(cudaMemsetAsync(P.rec_T, 0, rec_bytes, st));
+  k_init_paths<<<grid, 256, 0, st>>>(c, P, n_paths, n_pix, n_img, pix0, sample0, seed);
   WFPG_CHECK_LAUNCH("k_init_paths");
   return WFPG_OK;
 }

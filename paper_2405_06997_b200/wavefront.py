@@ -163,13 +163,14 @@ class PassRunner:
     (path state, frame, workspace) so that steady-state rendering allocates
     nothing.  ``render_pass`` uses a cached runner per (scene, svo, cfg)."""
 
-    def __init__(self, scene, svo, cfg, n_samples=1, deterministic=True):
+    def __init__(self, scene, svo, cfg, n_samples=1, deterministic=True, pixel_offset=0,
+                 n_pixels=None, leaf_acc=None):
         cam = scene.camera
         self.scene = scene
         self.svo = svo
         self.cfg = cfg
         self.n_samples = int(n_samples)
-        self.n_pix = cam.width * cam.height
+        self.n_pix = int(n_pixels) if n_pixels else cam.width * cam.height
         self.P = self.n_pix * self.n_samples
         self.cam = cam.as_abi()
         self.state = PathState(self.P, cfg.max_depth, cam.position)
@@ -189,6 +190,10 @@ class PassRunner:
         for i, w in enumerate(taps[:2 * radius + 1] if radius else []):
             pc.blur_w[i] = float(w)
         pc.upper_dirs = guiding.upper_dirs_device().data_ptr() if cfg.product else None
+        pc.pixel_offset = int(pixel_offset)
+        pc.n_pixels = self.n_pix
+        self.leaf_acc = leaf_acc
+        pc.leaf_acc = leaf_acc.data_ptr() if leaf_acc is not None else None
         self.svo_abi = svo.abi() if svo is not None else None
         nbytes = _lib.load().wfpg_render_workspace_bytes(
             C.byref(scene.abi()), C.byref(self.svo_abi) if svo is not None else None,
