@@ -75,6 +75,29 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        try:  # in-process NVML sampling (nvidia_ml_py), 20 ms period
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.stop = threading.Event()
+
+            def loop():
+                mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                while not self.stop.is_set():
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    flags = ["Active" if rs & b else "Not Active" for b in (
+                        0x8, 0x40, 0x20, 0x4)]  # hw_slowdown, hw_thermal, sw_thermal, sw_power
+                    self.rows.append([str(sm), str(mx), hex(rs)] + flags)
+                    self.stop.wait(0.02)
+
+            self.t = threading.Thread(target=loop, daemon=True)
+            self.t.start()
+            self.nvml = True
+            return self
+        except Exception:
+            self.nvml = False
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -91,6 +114,10 @@ class ClockSampler:
             self.rows.append([x.strip() for x in line.split(",")])
 
     def __exit__(self, *a):
+        if getattr(self, "nvml", False):
+            self.stop.set()
+            self.t.join(timeout=2)
+            return
         if self.proc is not None:
             self.proc.terminate()
             try:

@@ -125,26 +125,28 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* F = reinterpret_cast<double*>(smem_raw);
   double* rs = F + N * S;  // row sums (N)
-  TriBin* tb = reinterpret_cast<TriBin*>(rs + N);
+  double* uv = rs + N;     // u of column i, then v of row j (2N)
+  TriBin* tb = reinterpret_cast<TriBin*>(uv + 2 * N);
   const int64_t nb = dev_count(nb_max, nb_dev);
   const double omega = 4.0 * WFPG_PI / (double)(N * N);  // guiding.py:246
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
     const double ox = origins[3 * b], oy = origins[3 * b + 1], oz = origins[3 * b + 2];
-    const double ju = __ddiv_rn(jitters[2 * b], (double)N);
-    const double jv = __ddiv_rn(jitters[2 * b + 1], (double)N);
-    if (s.brute) {
-      for (int t = threadIdx.x; t < s.n_tris; t += blockDim.x) make_tri_bin(s, t, ox, oy, oz, tb[t]);
-      __syncthreads();
+    // u = i/n + ju/n, v = j/n + jv/n (guiding.py:239-244), once per bin
+    for (int k = threadIdx.x; k < 2 * N; k += blockDim.x) {
+      const int i = k < N ? k : k - N;
+      const double jit = __ddiv_rn(jitters[2 * b + (k < N ? 0 : 1)], (double)N);
+      uv[k] = __dadd_rn(__ddiv_rn((double)i, (double)N), jit);
     }
-    // 1. cone-trace every cell: u = i/n + ju/n, v = j/n + jv/n (guiding.py:239-244)
+    if (s.brute)
+      for (int t = threadIdx.x; t < s.n_tris; t += blockDim.x) make_tri_bin(s, t, ox, oy, oz, tb[t]);
+    __syncthreads();
+    // 1. cone-trace every cell
     for (int tile = warp; tile < TILES; tile += nwarps) {
       const int i = (tile % TILES_U) * TU + (lane % TU);
       const int j = (tile / TILES_U) * TV + (lane / TU);
-      double u = __dadd_rn(__ddiv_rn((double)i, (double)N), ju);
-      double w = __dadd_rn(__ddiv_rn((double)j, (double)N), jv);
       double dx, dy, dz;
-      octa_uv_to_dir_np(u, w, &dx, &dy, &dz);
+      octa_uv_to_dir_np(uv[i], uv[N + j], &dx, &dy, &dz);
       double rgb[3] = {0.0, 0.0, 0.0};
       double bt;
       int32_t bid;
@@ -208,7 +210,7 @@ static int launch_fields_n(const SceneView& s, const SvoView& v, const double* o
                            const double* jitters, int64_t nb_max, const int32_t* nb_dev,
                            const BlurParams& bp, const FieldOut& out, cudaStream_t st) {
   constexpr int T = FieldCfg<N>::kThreads;
-  size_t smem = sizeof(double) * (N * FieldCfg<N>::kStride + N) +
+  size_t smem = sizeof(double) * (N * FieldCfg<N>::kStride + 3 * N) +
                 (s.brute ? sizeof(TriBin) * s.n_tris : 0);
   static bool configured = false;
   if (!configured) {

@@ -261,6 +261,12 @@ struct TriBin {
   double e1x, e1y, e1z, e2x, e2y, e2z;
   double tx, ty, tz, qx, qy, qz, ts0;
   double ax, ay, az, cos_lim;
+  // unit normals of the three planes through o and an edge, oriented toward
+  // the opposite vertex: the triangle's solid angle seen from o is the
+  // intersection of their positive half-spaces.  cull = 0 disables (o on or
+  // near the triangle's plane / an edge line).
+  double n0x, n0y, n0z, n1x, n1y, n1z, n2x, n2y, n2z;
+  int cull;
 };
 
 __device__ __forceinline__ void make_tri_bin(const SceneView& s, int t, double ox, double oy,
@@ -300,7 +306,7 @@ __device__ __forceinline__ void make_tri_bin(const SceneView& s, int t, double o
     cz += w[k][2];
   }
   double cl = sqrt(cx * cx + cy * cy + cz * cz);
-  B.cos_lim = -2.0;
+  B.cos_lim = WFPG_PI;  // half-angle of the bounding cone; pi disables culling
   B.ax = 0.0;
   B.ay = 0.0;
   B.az = 1.0;
@@ -311,7 +317,56 @@ __device__ __forceinline__ void make_tri_bin(const SceneView& s, int t, double o
     double cmin = 1.0;
     for (int k = 0; k < 3; ++k)
       cmin = fmin(cmin, B.ax * w[k][0] + B.ay * w[k][1] + B.az * w[k][2]);
-    if (cmin > 1e-3) B.cos_lim = cos(fmin(acos(fmin(cmin, 1.0)) + 1e-6, 0.5 * WFPG_PI));
+    // the cone contains the spherical triangle only while all vertex
+    // directions lie in the axis' open hemisphere
+    if (cmin > 1e-3) B.cos_lim = acos(fmin(cmin, 1.0));
+  }
+  // edge planes
+  B.cull = 0;
+  if (!degenerate) {
+    double nrm[3][3];
+    bool ok = true;
+    for (int e = 0; e < 3 && ok; ++e) {
+      const double* a = w[e];
+      const double* b = w[(e + 1) % 3];
+      const double* c = w[(e + 2) % 3];
+      double nx = a[1] * b[2] - a[2] * b[1];
+      double ny = a[2] * b[0] - a[0] * b[2];
+      double nz = a[0] * b[1] - a[1] * b[0];
+      double len = sqrt(nx * nx + ny * ny + nz * nz);
+      if (!(len > 1e-9)) {
+        ok = false;
+        break;
+      }
+      nx /= len;
+      ny /= len;
+      nz /= len;
+      double side = nx * c[0] + ny * c[1] + nz * c[2];
+      if (fabs(side) < 1e-9) {  // origin (nearly) in the triangle's plane
+        ok = false;
+        break;
+      }
+      if (side < 0.0) {
+        nx = -nx;
+        ny = -ny;
+        nz = -nz;
+      }
+      nrm[e][0] = nx;
+      nrm[e][1] = ny;
+      nrm[e][2] = nz;
+    }
+    if (ok) {
+      B.n0x = nrm[0][0];
+      B.n0y = nrm[0][1];
+      B.n0z = nrm[0][2];
+      B.n1x = nrm[1][0];
+      B.n1y = nrm[1][1];
+      B.n1z = nrm[1][2];
+      B.n2x = nrm[2][0];
+      B.n2y = nrm[2][1];
+      B.n2z = nrm[2][2];
+      B.cull = 1;
+    }
   }
 }
 
@@ -331,21 +386,58 @@ __device__ __forceinline__ double mt_bin(const TriBin& B, double dx, double dy, 
   return ok ? ts / ad : -1.0;
 }
 
-// Nearest hit for one lane of a warp whose rays share the origin; triangles
-// no lane can reach are skipped warp-uniformly.  Same result as brute force.
+__device__ __forceinline__ double warp_sum_d(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+__device__ __forceinline__ double warp_min_d(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmin(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+
+// Nearest hit for the 32 rays of a warp that share one origin.  The warp
+// bounds its own 32 directions by a cone (axis = the tile's centre lane,
+// cos of the half-angle = smallest dot with the axis).  A cone of half-angle
+// th around a reaches the positive side of a plane with unit normal n only
+// if a.n >= -sin(th); a triangle one of whose three edge planes (TriBin) the
+// whole cone misses cannot be hit by any lane.  Lanes vote on 32 triangles at
+// a time and the warp then tests only the surviving candidates, in ascending
+// triangle order with the strict '<' of the brute-force kernel, so the result
+// (minimum t, lowest id on ties) is exactly brute force over all triangles
+// (the 1e-6 slack dwarfs the rounding of both the cull and the hit test).
 __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, int n, double dx,
                                                  double dy, double dz, double tmin, double* bt,
                                                  int32_t* bid) {
+  const int lane = threadIdx.x & 31;
+  const double ax = __shfl_sync(0xffffffffu, dx, 12);
+  const double ay = __shfl_sync(0xffffffffu, dy, 12);
+  const double az = __shfl_sync(0xffffffffu, dz, 12);
+  const double cmin = warp_min_d(dx * ax + dy * ay + dz * az);
+  const bool cull = cmin > 0.0;
+  const double reach = -(sqrt(fmax(1.0 - cmin * cmin, 0.0)) + 1e-6);  // -sin(th) - slack
   double best = 1e300;
   int32_t id = -1;
-  for (int t = 0; t < n; ++t) {
-    const TriBin& B = tb[t];
-    bool maybe = dx * B.ax + dy * B.ay + dz * B.az >= B.cos_lim;
-    if (!__any_sync(0xffffffffu, maybe)) continue;
-    double h = mt_bin(B, dx, dy, dz, tmin);
-    if (h > 0.0 && h < best) {
-      best = h;
-      id = t;
+  for (int g = 0; g < n; g += 32) {
+    const int t = g + lane;
+    bool cand = t < n;
+    if (cand && cull) {
+      const TriBin& B = tb[t];
+      if (B.cull)
+        cand = (ax * B.n0x + ay * B.n0y + az * B.n0z >= reach) &&
+               (ax * B.n1x + ay * B.n1y + az * B.n1z >= reach) &&
+               (ax * B.n2x + ay * B.n2y + az * B.n2z >= reach);
+    }
+    unsigned m = __ballot_sync(0xffffffffu, cand);
+    while (m) {
+      const int k = g + __ffs(m) - 1;
+      m &= m - 1;
+      double h = mt_bin(tb[k], dx, dy, dz, tmin);
+      if (h > 0.0 && h < best) {
+        best = h;
+        id = k;
+      }
     }
   }
   *bt = best;

@@ -10,13 +10,16 @@ namespace wfpg {
 // unimodal in lv, so the level chosen over the materialised chain [0, L] of
 // the reference equals min(L, best) with best taken over [0, depth]; the
 // descent can therefore stop at `best` instead of walking to the leaf.
+// (size / 2^lv)^2 == round(size * size) * 4^-lv exactly (power-of-two scaling
+// commutes with rounding), so the per-level squares come from one product and
+// exact multiplications by 4 — same bits as the reference's divisions.
 __device__ __forceinline__ int best_cone_level(double size, int depth, double area) {
-  double s = size / (double)(1u << depth);
-  double bd = fabs(s * s - area);
+  double s2 = ldexp(size * size, -2 * depth);
+  double bd = fabs(s2 - area);
   int best = depth;
   for (int lv = depth - 1; lv >= 0; --lv) {
-    s = size / (double)(1u << lv);
-    double diff = fabs(s * s - area);
+    s2 *= 4.0;
+    double diff = fabs(s2 - area);
     if (diff < bd) {
       bd = diff;
       best = lv;
