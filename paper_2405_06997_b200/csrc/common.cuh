@@ -221,6 +221,8 @@ struct SvoView {
   const double* mean_b;
   double lox, loy, loz, size;
   double scale;        // resolution / size
+  double nudge;        // (size / resolution) * 1e-3 (_kernels.pyx:676)
+  double clo[3], chi[3];  // lo + size*1e-12, (lo + size) - size*1e-12 (:677-683)
   int32_t resolution, depth;
 };
 
@@ -236,6 +238,12 @@ __host__ inline SvoView make_view(const wfpg_svo* s) {
   v.loz = s->lo[2];
   v.size = s->size;
   v.scale = (double)s->resolution / s->size;
+  v.nudge = (s->size / s->resolution) * 1e-3;
+  const double tiny = s->size * 1e-12;
+  for (int a = 0; a < 3; ++a) {
+    v.clo[a] = s->lo[a] + tiny;
+    v.chi[a] = s->lo[a] + s->size - tiny;
+  }
   v.resolution = s->resolution;
   v.depth = s->depth;
   return v;

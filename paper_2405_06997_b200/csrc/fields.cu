@@ -29,7 +29,7 @@ template <int N>
 struct FieldCfg {
   static constexpr int kStride = N + 1;  // padded rows: conflict-free column walks
   // one warp per 8x4-cell tile at most: N=8 has 2 tiles, N=16 8, N=32 32
-  static constexpr int kThreads = N >= 64 ? 512 : (N == 32 ? 256 : (N == 16 ? 128 : 64));
+  static constexpr int kThreads = N >= 64 ? 1024 : (N == 32 ? 256 : (N == 16 ? 128 : 64));
   static constexpr int kPerLane = (N + 31) / 32;
 };
 
@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads)
   // coherent, so whole-warp triangle culling is effective
   constexpr int TU = 8, TV = 4, TILES_U = N / TU, TILES = (N / TU) * (N / TV);
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int tile_ctr;
   double* F = reinterpret_cast<double*>(smem_raw);
   double* rs = F + N * S;  // row sums (N)
   double* uv = rs + N;     // u of column i, then v of row j (2N)
@@ -140,9 +141,12 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads)
     }
     if (s.brute)
       for (int t = threadIdx.x; t < s.n_tris; t += blockDim.x) make_tri_bin(s, t, ox, oy, oz, tb[t]);
+    if (threadIdx.x == 0) tile_ctr = nwarps;
     __syncthreads();
-    // 1. cone-trace every cell
-    for (int tile = warp; tile < TILES; tile += nwarps) {
+    // 1. cone-trace every cell; tiles are handed out dynamically (cull
+    // candidates and hit depths vary per tile, static striping left warps
+    // idling at the barrier)
+    for (int tile = warp; tile < TILES;) {
       const int i = (tile % TILES_U) * TU + (lane % TU);
       const int j = (tile / TILES_U) * TV + (lane / TU);
       double dx, dy, dz;
@@ -156,6 +160,9 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads)
         bvh_nearest(s, ox, oy, oz, dx, dy, dz, s.ray_eps, &bt, &bid);
       if (bid >= 0) cone_shade_hit(v, ox, oy, oz, dx, dy, dz, bt, omega, rgb);
       F[j * S + i] = luminance_rows(rgb[0], rgb[1], rgb[2]);
+      int next = 0;
+      if (lane == 0) next = atomicAdd(&tile_ctr, 1);
+      tile = __shfl_sync(0xffffffffu, next, 0);
     }
     __syncthreads();
     // 2. fold-aware separable blur, horizontal then vertical (core.py:185-195)
@@ -212,11 +219,11 @@ static int launch_fields_n(const SceneView& s, const SvoView& v, const double* o
   constexpr int T = FieldCfg<N>::kThreads;
   size_t smem = sizeof(double) * (N * FieldCfg<N>::kStride + 3 * N) +
                 (s.brute ? sizeof(TriBin) * s.n_tris : 0);
-  static bool configured = false;
-  if (!configured) {
+  static size_t configured = 0;
+  if (smem > configured) {
     WFPG_CUDA(cudaFuncSetAttribute(k_fields<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   227 * 1024));
-    configured = true;
+                                   (int)smem));
+    configured = smem;
   }
   int per_sm = 0;
   WFPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fields<N>, T, smem));

@@ -34,14 +34,13 @@ __device__ __forceinline__ int best_cone_level(double size, int depth, double ar
 __device__ __forceinline__ void cone_shade_hit(const SvoView& v, double ox, double oy, double oz,
                                                double dx, double dy, double dz, double r,
                                                double omega, double* rgb) {
-  double nudge = (v.size / v.resolution) * 1e-3;
-  double tiny = v.size * 1e-12;
+  const double nudge = v.nudge;  // (size / resolution) * 1e-3, precomputed on the host
   double qx = ox + r * dx - dx * nudge;
   double qy = oy + r * dy - dy * nudge;
   double qz = oz + r * dz - dz * nudge;
-  qx = fmin(fmax(qx, v.lox + tiny), v.lox + v.size - tiny);
-  qy = fmin(fmax(qy, v.loy + tiny), v.loy + v.size - tiny);
-  qz = fmin(fmax(qz, v.loz + tiny), v.loz + v.size - tiny);
+  qx = fmin(fmax(qx, v.clo[0]), v.chi[0]);
+  qy = fmin(fmax(qy, v.clo[1]), v.chi[1]);
+  qz = fmin(fmax(qz, v.clo[2]), v.chi[2]);
   int32_t ix = quantise(qx, v.lox, v.scale, v.resolution);
   int32_t iy = quantise(qy, v.loy, v.scale, v.resolution);
   int32_t iz = quantise(qz, v.loz, v.scale, v.resolution);
