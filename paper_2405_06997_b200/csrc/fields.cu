@@ -113,6 +113,105 @@ __device__ void blur_cols(double* F, const BlurParams& bp) {
   }
 }
 
+// Fixed-radius variants (sigma = 1 gives radius 3): interior outputs use an
+// unrolled tap loop with compile-time offsets; only the r outputs at each
+// edge take the fold path.  Same taps, same order, same rounding.
+template <int N, int R>
+__device__ void blur_rows_r(double* F, const BlurParams& bp) {
+  constexpr int S = FieldCfg<N>::kStride;
+  constexpr int PL = FieldCfg<N>::kPerLane;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double w[2 * R + 1];
+#pragma unroll
+  for (int k = 0; k <= 2 * R; ++k) w[k] = bp.w[k];
+  for (int j = warp; j < N / 2; j += nw) {
+    const int jp = N - 1 - j;
+    const double* A = F + j * S;
+    const double* B = F + jp * S;
+    double oa[PL], ob[PL];
+#pragma unroll
+    for (int q = 0; q < PL; ++q) {
+      const int i = lane + 32 * q;
+      double a = 0.0, b = 0.0;
+      if (i >= R && i < N - R) {
+#pragma unroll
+        for (int k = 0; k <= 2 * R; ++k) {
+          a = __dadd_rn(a, __dmul_rn(w[k], A[i + k - R]));
+          b = __dadd_rn(b, __dmul_rn(w[k], B[i + k - R]));
+        }
+      } else if (i < N) {
+#pragma unroll
+        for (int k = 0; k <= 2 * R; ++k) {
+          bool f;
+          const int c = fold_index(i + k - R, N, &f);
+          a = __dadd_rn(a, __dmul_rn(w[k], f ? B[c] : A[c]));
+          b = __dadd_rn(b, __dmul_rn(w[k], f ? A[c] : B[c]));
+        }
+      }
+      oa[q] = a;
+      ob[q] = b;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < PL; ++q) {
+      const int i = lane + 32 * q;
+      if (i < N) {
+        F[j * S + i] = oa[q];
+        F[jp * S + i] = ob[q];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <int N, int R>
+__device__ void blur_cols_r(double* F, const BlurParams& bp) {
+  constexpr int S = FieldCfg<N>::kStride;
+  constexpr int PL = FieldCfg<N>::kPerLane;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double w[2 * R + 1];
+#pragma unroll
+  for (int k = 0; k <= 2 * R; ++k) w[k] = bp.w[k];
+  for (int i = warp; i < N / 2; i += nw) {
+    const int ip = N - 1 - i;
+    double oa[PL], ob[PL];
+#pragma unroll
+    for (int q = 0; q < PL; ++q) {
+      const int j = lane + 32 * q;
+      double a = 0.0, b = 0.0;
+      if (j >= R && j < N - R) {
+#pragma unroll
+        for (int k = 0; k <= 2 * R; ++k) {
+          const double* row = F + (j + k - R) * S;
+          a = __dadd_rn(a, __dmul_rn(w[k], row[i]));
+          b = __dadd_rn(b, __dmul_rn(w[k], row[ip]));
+        }
+      } else if (j < N) {
+#pragma unroll
+        for (int k = 0; k <= 2 * R; ++k) {
+          bool f;
+          const int rr = fold_index(j + k - R, N, &f);
+          const double* row = F + rr * S;
+          a = __dadd_rn(a, __dmul_rn(w[k], f ? row[ip] : row[i]));
+          b = __dadd_rn(b, __dmul_rn(w[k], f ? row[i] : row[ip]));
+        }
+      }
+      oa[q] = a;
+      ob[q] = b;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < PL; ++q) {
+      const int j = lane + 32 * q;
+      if (j < N) {
+        F[j * S + i] = oa[q];
+        F[j * S + ip] = ob[q];
+      }
+    }
+    __syncwarp();
+  }
+}
+
 template <int N>
 __global__ void __launch_bounds__(FieldCfg<N>::kThreads)
     k_fields(SceneView s, SvoView v, const double* __restrict__ origins,
@@ -166,7 +265,12 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads)
     }
     __syncthreads();
     // 2. fold-aware separable blur, horizontal then vertical (core.py:185-195)
-    if (bp.radius > 0) {
+    if (bp.radius == 3 && N > 8) {
+      blur_rows_r<N, 3>(F, bp);
+      __syncthreads();
+      blur_cols_r<N, 3>(F, bp);
+      __syncthreads();
+    } else if (bp.radius > 0) {
       blur_rows<N>(F, bp);
       __syncthreads();
       blur_cols<N>(F, bp);

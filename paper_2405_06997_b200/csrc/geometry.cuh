@@ -411,12 +411,18 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
                                                  double dy, double dz, double tmin, double* bt,
                                                  int32_t* bid) {
   const int lane = threadIdx.x & 31;
-  const double ax = __shfl_sync(0xffffffffu, dx, 12);
-  const double ay = __shfl_sync(0xffffffffu, dy, 12);
-  const double az = __shfl_sync(0xffffffffu, dz, 12);
-  const double cmin = warp_min_d(dx * ax + dy * ay + dz * az);
+  // axis: the centre lane's direction, broadcast as floats (any common axis is
+  // valid); cmin rounded down to float and min-reduced in fp32 (conservative)
+  const double ax = (double)__shfl_sync(0xffffffffu, (float)dx, 12);
+  const double ay = (double)__shfl_sync(0xffffffffu, (float)dy, 12);
+  const double az = (double)__shfl_sync(0xffffffffu, (float)dz, 12);
+  const double al = sqrt(ax * ax + ay * ay + az * az);
+  float cm = __double2float_rd((dx * ax + dy * ay + dz * az) / al);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cm = fminf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+  const double cmin = (double)cm;
   const bool cull = cmin > 0.0;
-  const double reach = -(sqrt(fmax(1.0 - cmin * cmin, 0.0)) + 1e-6);  // -sin(th) - slack
+  const double reach = -(sqrt(fmax(1.0 - cmin * cmin, 0.0)) + 1e-6) * al;  // -|a| sin(th) - slack
   double best = 1e300;
   int32_t id = -1;
   for (int g = 0; g < n; g += 32) {
@@ -433,10 +439,23 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
     while (m) {
       const int k = g + __ffs(m) - 1;
       m &= m - 1;
-      double h = mt_bin(tb[k], dx, dy, dz, tmin);
-      if (h > 0.0 && h < best) {
-        best = h;
-        id = k;
+      const TriBin& B = tb[k];
+      double px = dy * B.e2z - dz * B.e2y;
+      double py = dz * B.e2x - dx * B.e2z;
+      double pz = dx * B.e2y - dy * B.e2x;
+      double det = B.e1x * px + B.e1y * py + B.e1z * pz;
+      double sg = det > 0.0 ? 1.0 : -1.0;
+      double ad = det * sg;
+      double us = (B.tx * px + B.ty * py + B.tz * pz) * sg;
+      double vs = (dx * B.qx + dy * B.qy + dz * B.qz) * sg;
+      double ts = B.ts0 * sg;
+      bool ok = (ad > 1e-300) & (us >= 0.0) & (vs >= 0.0) & (us + vs <= ad) & (ts > tmin * ad);
+      if (__any_sync(0xffffffffu, ok)) {  // the division only when some lane hits
+        double h = ts / ad;
+        if (ok && h < best) {
+          best = h;
+          id = k;
+        }
       }
     }
   }
