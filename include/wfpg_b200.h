@@ -146,6 +146,9 @@ typedef struct wfpg_guide {
   double* block_sums;        /* (B,8,8) product mode (else may be NULL) */
   const int32_t* n_bins;     /* device count of valid slots */
   const double* upper_dirs;  /* (8,8,3) product-layer cell centres (guiding.UPPER_DIRS) */
+  double* cum;               /* optional (B,n,n) unnormalised row prefix sums
+                                (np.cumsum order); lets the plain sampler invert the
+                                conditional CDF with a binary search */
 } wfpg_guide;
 
 /* Knobs of one render pass: wavefront.py:21-50 (GuidingConfig). */

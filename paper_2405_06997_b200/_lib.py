@@ -67,7 +67,7 @@ class Guide(C.Structure):
     _fields_ = [
         ("mode", c_i32), ("n", c_i32), ("capacity", c_i32), ("eps", c_dbl),
         ("vals", c_vp), ("row_sum", c_vp), ("marg", c_vp), ("total", c_vp),
-        ("block_sums", c_vp), ("n_bins", c_vp), ("upper_dirs", c_vp),
+        ("block_sums", c_vp), ("n_bins", c_vp), ("upper_dirs", c_vp), ("cum", c_vp),
     ]
 
 

@@ -312,6 +312,21 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads)
         out.marg[b * N + j] = __ddiv_rn(run, tot);
       }
     }
+    // 5. unnormalised row prefix sums (np.cumsum order) for the samplers:
+    // cond[j, i] = cum[j, i] / row_sum[j] is then one division at the picked
+    // cell instead of a division per scanned cell
+    if (out.cum) {
+      for (int j = threadIdx.x; j < N; j += blockDim.x) {
+        double run = F[j * S];
+        for (int i = 1; i < N; ++i) {
+          run = __dadd_rn(run, F[j * S + i]);
+          F[j * S + i] = run;
+        }
+      }
+      __syncthreads();
+      double* gc = out.cum + b * (int64_t)N * N;
+      for (int c = threadIdx.x; c < N * N; c += blockDim.x) gc[c] = F[(c / N) * S + c % N];
+    }
     __syncthreads();
   }
 }
@@ -478,7 +493,7 @@ extern "C" int wfpg_generate_fields(const wfpg_scene* scene, const wfpg_svo* svo
   bp.radius = blur_radius;
   for (int k = 0; k <= 2 * blur_radius && blur_radius > 0; ++k) bp.w[k] = blur_w[k];
   FieldOut out{guide->vals, guide->row_sum, guide->marg, guide->total,
-               guide->mode == 2 ? guide->block_sums : nullptr, guide->eps};
+               guide->mode == 2 ? guide->block_sums : nullptr, guide->eps, guide->cum};
   guide->n = n;
   return launch_fields(make_scene_view(scene), make_view(svo), origins, jitters, n_bins,
                        n_bins_dev, n, bp, out, as_stream(stream));

@@ -15,6 +15,7 @@ struct FieldOut {
   double* total;
   double* block_sums;  // NULL unless product mode
   double eps;
+  double* cum = nullptr;  // optional (B,n,n) row prefix sums
 };
 
 int launch_fields(const SceneView& s, const SvoView& v, const double* origins,

@@ -166,6 +166,7 @@ struct PassLayout {
   double* marg;
   double* tot;
   double* block_sums;
+  double* cum;
   double* upper_dirs;
   StatsDev* stats;
   size_t scratch_off;
@@ -212,6 +213,7 @@ static void carve_pass(Arena& a, const wfpg_svo* svo, const wfpg_camera* cam,
       L.marg = a.take<double>(L.cap * (int64_t)L.n0);
       L.tot = a.take<double>(L.cap);
       L.block_sums = cfg->product ? a.take<double>(L.cap * 64) : nullptr;
+      L.cum = a.take<double>(L.cap * (int64_t)L.n0 * L.n0);
     }
   }
   L.scratch_off = a.off;
@@ -394,7 +396,7 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
       if (guided_depth) {
         const int n = std::max(8, cfg->field_res >> (depth - 1));
         FieldOut fo{L.vals, L.row_sum, L.marg, L.tot, cfg->product ? L.block_sums : nullptr,
-                    cfg->epsilon};
+                    cfg->epsilon, L.cum};
         ProfRec* pr = prof_begin(st, depth);
         WFPG_TRY(launch_fields(sv, vv, L.origins, L.jitters, L.cap, L.n_bins, n, bp, fo, st));
         prof_end(pr, st, n, L.n_bins);
@@ -408,6 +410,7 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
         gv.marg = L.marg;
         gv.total = L.tot;
         gv.block_sums = L.block_sums;
+        gv.cum = L.cum;
         gv.upper_dirs = cfg->upper_dirs;
         slots = L.bin_slot;
       }

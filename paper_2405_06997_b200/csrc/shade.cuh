@@ -16,6 +16,7 @@ struct GuideView {
   const double* total;
   const double* block_sums;
   const double* upper_dirs;  // (8,8,3) host-numpy octahedral cell centres
+  const double* cum;         // optional row prefix sums (plain sampler fast path)
 };
 
 // upper_bound (_kernels.pyx:802-812)
@@ -63,6 +64,33 @@ __device__ __forceinline__ int invert_cumsum(const double* v, int stride, int n,
   if (i >= n) i = n - 1;  // clamp: cur is cdf[n-1], prev cdf[n-2]
   double lo = i > 0 ? prev : 0.0;
   *frac = residual(u, lo, cur);
+  return i;
+}
+
+// Same result as invert_cumsum given the stored prefix sums cum[0..n):
+// cdf_i = cum_i / denom is non-decreasing; every cum_i < u*denom*(1-1e-12)
+// gives cdf_i < u (the bound covers the roundings of the product and of the
+// division), so a binary search finds the first index that can exceed u and
+// the exact divisions are only evaluated from there (usually once).
+__device__ __forceinline__ int invert_prefix(const double* cum, int n, double denom, double u,
+                                             double* frac) {
+  const double thr = u * denom * (1.0 - 1e-12);
+  int lo = 0, hi = n;  // first index with cum >= thr
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (cum[mid] < thr)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  int i = lo < n ? lo : n - 1;
+  double cur = __ddiv_rn(cum[i], denom);
+  while (!(cur > u) && i < n - 1) {
+    ++i;
+    cur = __ddiv_rn(cum[i], denom);
+  }
+  double prev = i > 0 ? __ddiv_rn(cum[i - 1], denom) : 0.0;
+  *frac = residual(u, prev, cur);
   return i;
 }
 
@@ -125,8 +153,9 @@ __device__ __forceinline__ void sample_plain(const GuideView& g, int slot, doubl
   const int n = g.n;
   double fv, fu;
   int gj = invert_cdf(g.marg + (int64_t)slot * n, n, s1, &fv);
-  const double* row = g.vals + ((int64_t)slot * n + gj) * n;
-  int gi = invert_cumsum(row, 1, n, g.row_sum[(int64_t)slot * n + gj], s2, &fu);
+  const double denom = g.row_sum[(int64_t)slot * n + gj];
+  int gi = g.cum ? invert_prefix(g.cum + ((int64_t)slot * n + gj) * n, n, denom, s2, &fu)
+                 : invert_cumsum(g.vals + ((int64_t)slot * n + gj) * n, 1, n, denom, s2, &fu);
   octa_uv_to_dir_k((gi + fu) / n, (gj + fv) / n, wx, wy, wz);
 }
 

@@ -432,6 +432,7 @@ GuideView make_guide_view(const wfpg_guide* g) {
   v.total = g->total;
   v.block_sums = g->block_sums;
   v.upper_dirs = g->upper_dirs;
+  v.cum = g->cum;
   return v;
 }
 

@@ -212,7 +212,9 @@ class GuideTables:
         self.d_marg = _dev.zeros((b, n), np.float64)
         self.d_total = _dev.zeros((b,), np.float64)
         self.d_block_sums = _dev.zeros((b, 8, 8), np.float64) if mode == 2 else None
+        self.d_cum = _dev.zeros((b, n, n), np.float64)
         self._expanded = None
+        self._cum_valid = False
 
     def abi(self):
         g = _lib.Guide()
@@ -227,6 +229,7 @@ class GuideTables:
         g.block_sums = self.d_block_sums.data_ptr() if self.d_block_sums is not None else None
         g.n_bins = None
         g.upper_dirs = upper_dirs_device().data_ptr()
+        g.cum = self.d_cum.data_ptr() if self._cum_valid else None
         return g
 
     def fill_batch(self, values):
@@ -310,6 +313,7 @@ def generate_fields_device(svo, scene, origins, jitters, n, blur_sigma=1.0,
     tables = GuideTables(2 if product else 1, n, b)
     tables.epsilon = epsilon
     radius, taps = blur_params(blur_sigma)
+    tables._cum_valid = True
     g = tables.abi()
     _lib.call("wfpg_generate_fields", C.byref(scene.abi()), C.byref(svo.abi()),
               _lib.ptr(origins), _lib.ptr(jitters), b, None, n, radius,
