@@ -256,10 +256,13 @@ def run_b200(args):
     e2e = None
     if world == 1 and not args.no_e2e:
         frame_bytes = n_paths * 3 * 8
+        out_frame = wavefront.pinned_frame(sc)  # page-locked destination, reused
+        wavefront.render_pass(sc, tree, g_cfg, [sample], out=out_frame)  # API warm-up
+        sample += 1
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            f, _ = wavefront.render_pass(sc, tree, g_cfg, [sample])
+            f, _ = wavefront.render_pass(sc, tree, g_cfg, [sample], out=out_frame)
             sample += 1
         e2e_s = time.perf_counter() - t0
         e2e = {"value": n_paths * args.steps / e2e_s, "unit": "path samples/s",

@@ -28,8 +28,12 @@ __device__ __forceinline__ int fold_index(int raw, int n, bool* flip) {
 template <int N>
 struct FieldCfg {
   static constexpr int kStride = N + 1;  // padded rows: conflict-free column walks
-  // one warp per 8x4-cell tile at most: N=8 has 2 tiles, N=16 8, N=32 32
-  static constexpr int kThreads = N >= 64 ? 1024 : (N == 32 ? 256 : (N == 16 ? 128 : 64));
+  // one warp per 8x4-cell tile at most: N=8 has 2 tiles, N=16 8, N=32 32.
+  // kThreads * kMinBlocks = 1024 -> a 64-register budget and 32+ warps per SM;
+  // several CTAs (bins) per SM overlap one bin's barrier phases with
+  // another's cone tracing
+  static constexpr int kThreads = N >= 128 ? 1024 : (N == 64 ? 512 : (N == 32 ? 256 : (N == 16 ? 128 : 64)));
+  static constexpr int kMinBlocks = 1024 / kThreads;
   static constexpr int kPerLane = (N + 31) / 32;
 };
 
@@ -213,7 +217,7 @@ __device__ void blur_cols_r(double* F, const BlurParams& bp) {
 }
 
 template <int N>
-__global__ void __launch_bounds__(FieldCfg<N>::kThreads)
+__global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks)
     k_fields(SceneView s, SvoView v, const double* __restrict__ origins,
              const double* __restrict__ jitters, int64_t nb_max, const int32_t* __restrict__ nb_dev,
              BlurParams bp, FieldOut out) {

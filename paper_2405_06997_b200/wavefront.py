@@ -237,9 +237,18 @@ def _runner(scene, svo, cfg, n_samples):
     return r
 
 
-def render_pass(scene, svo, cfg, sample_indices, collect_bin_image=False):
+def pinned_frame(scene):
+    """A page-locked (H, W, 3) float64 host array for render_pass(out=...):
+    the frame then arrives by one DMA instead of a pageable copy."""
+    t = _dev.torch()
+    cam = scene.camera
+    return t.empty((cam.height, cam.width, 3), dtype=t.float64, pin_memory=True).numpy()
+
+
+def render_pass(scene, svo, cfg, sample_indices, collect_bin_image=False, out=None):
     """One wavefront pass over every pixel for each sample index (consecutive
-    indices); returns (frame (H,W,3), PassStats)."""
+    indices); returns (frame (H,W,3), PassStats).  ``out`` (optional, e.g.
+    from pinned_frame) receives the frame instead of a fresh array."""
     samples = np.asarray(sample_indices, dtype=np.int64).reshape(-1)
     if len(samples) == 0:
         raise ValueError("render_pass needs at least one sample index")
@@ -252,6 +261,12 @@ def render_pass(scene, svo, cfg, sample_indices, collect_bin_image=False):
     r = _runner(scene, svo, cfg, len(samples))
     r.launch(int(samples[0]))
     cam = scene.camera
+    if out is not None:
+        t = _dev.torch()
+        dst = t.from_numpy(out).view(-1, 3)
+        dst.copy_(r.frame, non_blocking=dst.is_pinned())
+        t.cuda.current_stream().synchronize()
+        return out, r.pass_stats()
     frame = _dev.download(r.frame).reshape(cam.height, cam.width, 3)
     return frame, r.pass_stats()
 
