@@ -160,8 +160,13 @@ int partition_spatial(const SvoView& v, int32_t* counter, const int32_t* parent,
   k_part_ascend<<<grid, 256, 0, st>>>(counter, parent, start, lev, n_max, n_dev, l_min, c_ray,
                                       keys, vals);
   WFPG_CHECK_LAUNCH("k_part_ascend");
-  k_part_clear<<<grid, 256, 0, st>>>(counter, parent, start, lev, n_max, n_dev, l_min);
-  WFPG_CHECK_LAUNCH("k_part_clear");
+  if (out.clear_from >= 0 && out.clear_from <= n_nodes) {
+    WFPG_CUDA(cudaMemsetAsync(counter + out.clear_from, 0,
+                              sizeof(int32_t) * (size_t)(n_nodes - out.clear_from), st));
+  } else {
+    k_part_clear<<<grid, 256, 0, st>>>(counter, parent, start, lev, n_max, n_dev, l_min);
+    WFPG_CHECK_LAUNCH("k_part_clear");
+  }
   {
     size_t mark = ws.off;
     WFPG_TRY(sort_pairs(keys, vals, n_max, n_dev, bits_for((uint64_t)n_nodes), ws, st));

@@ -14,6 +14,9 @@ struct PartitionOut {
   const uint32_t* sorted_items;  // out: item index per sorted position
   int32_t* bin_slot;    // optional (P,): slot of every member path, indexed by path id
   const int32_t* item_path;  // path id per item (required with bin_slot)
+  // first node id above level l_min (level_off[l_min + 1]); counters live only
+  // there, so one memset of [clear_from, n_nodes) clears them.  < 0: per-path walk.
+  int64_t clear_from = -1;
 };
 
 size_t partition_ws_bytes(int64_t n);

@@ -119,19 +119,54 @@ __global__ void __launch_bounds__(kSortBlock) k_sort_hist(const uint64_t* __rest
     if (i < n) atomicAdd(&cnt[(keys[i] >> shift) & 255u], 1u);
   }
   __syncthreads();
-  hist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = cnt[threadIdx.x];
+  if (base < n) hist[(int64_t)blockIdx.x * 256 + threadIdx.x] = cnt[threadIdx.x];  // block-major
+}
+
+// Digit offsets for the active tiles only (ceil(n / tile) of them, n from the
+// device): 4 threads per digit split the tiles, exclusive prefix over tiles
+// per digit, then the exclusive prefix of the digit totals.  Replaces a full
+// scan of 256 x (worst-case tiles) entries.
+constexpr int kOffThreads = 1024;
+__global__ void __launch_bounds__(kOffThreads) k_sort_offsets(uint32_t* __restrict__ hist,
+                                                              int64_t n_max,
+                                                              const int32_t* __restrict__ n_dev,
+                                                              uint32_t* __restrict__ dbase) {
+  __shared__ uint32_t seg_tot[4][256];
+  __shared__ uint32_t sw[kOffThreads / 32 + 1];
+  const int64_t n = dev_count(n_max, n_dev);
+  const int64_t nb = (n + kSortTile - 1) / kSortTile;
+  const int d = threadIdx.x & 255, sgi = threadIdx.x >> 8;
+  const int64_t per = (nb + 3) / 4, b0 = sgi * per, b1 = b0 + per < nb ? b0 + per : nb;
+  uint32_t s = 0;
+#pragma unroll 8
+  for (int64_t b = b0; b < b1; ++b) s += hist[b * 256 + d];
+  seg_tot[sgi][d] = s;
+  __syncthreads();
+  uint32_t run = 0;
+  for (int g = 0; g < sgi; ++g) run += seg_tot[g][d];
+  uint32_t total = seg_tot[0][d] + seg_tot[1][d] + seg_tot[2][d] + seg_tot[3][d];
+#pragma unroll 8
+  for (int64_t b = b0; b < b1; ++b) {
+    uint32_t h = hist[b * 256 + d];
+    hist[b * 256 + d] = run;
+    run += h;
+  }
+  // exclusive prefix of the digit totals (threads 0..255 carry them)
+  uint32_t ex = block_exclusive_scan<kOffThreads>(sgi == 0 ? total : 0u, sw, nullptr);
+  if (sgi == 0) dbase[d] = ex;
 }
 
 __global__ void __launch_bounds__(kSortBlock) k_sort_scatter(
     const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint64_t* __restrict__ kout,
     uint32_t* __restrict__ vout, int64_t n_max, const int32_t* __restrict__ n_dev, int shift,
-    int64_t nblocks, const uint32_t* __restrict__ offs) {
+    int64_t nblocks, const uint32_t* __restrict__ offs, const uint32_t* __restrict__ dbase) {
   __shared__ uint32_t whist[kSortWarps][256];
   __shared__ uint32_t goff[256];
   const int64_t n = dev_count(n_max, n_dev);
+  if ((int64_t)blockIdx.x * kSortTile >= n) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < kSortWarps * 256; i += kSortBlock) (&whist[0][0])[i] = 0;
-  goff[threadIdx.x] = offs[(int64_t)threadIdx.x * nblocks + blockIdx.x];
+  goff[threadIdx.x] = dbase[threadIdx.x] + offs[(int64_t)blockIdx.x * 256 + threadIdx.x];
   __syncthreads();
 
   const int64_t wbase = (int64_t)blockIdx.x * kSortTile + (int64_t)warp * 32 * kSortIpt;
@@ -176,11 +211,22 @@ __global__ void __launch_bounds__(kSortBlock) k_sort_scatter(
   }
 }
 
+__global__ void k_copy_pairs(const uint64_t* __restrict__ ks, const uint32_t* __restrict__ vs,
+                             uint64_t* __restrict__ kd, uint32_t* __restrict__ vd, int64_t n_max,
+                             const int32_t* __restrict__ n_dev) {
+  const int64_t n = dev_count(n_max, n_dev);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    kd[i] = ks[i];
+    vd[i] = vs[i];
+  }
+}
+
 size_t sort_ws_bytes(int64_t n_max) {
   int64_t n = n_max > 0 ? n_max : 1;
   int64_t nb = ceil_div(n, kSortTile);
   return align_up(sizeof(uint64_t) * n) + align_up(sizeof(uint32_t) * n) +
-         align_up(sizeof(uint32_t) * 256 * nb) + scan_ws_bytes(256 * nb) + 1024;
+         align_up(sizeof(uint32_t) * 256 * nb) + align_up(sizeof(uint32_t) * 256) + 1024;
 }
 
 int sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n_max, const int32_t* n_dev, int key_bits,
@@ -190,6 +236,7 @@ int sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n_max, const int32_t* n_d
   uint64_t* k2 = ws.take<uint64_t>(n_max);
   uint32_t* v2 = ws.take<uint32_t>(n_max);
   uint32_t* hist = ws.take<uint32_t>(256 * nb);
+  uint32_t* dbase = ws.take<uint32_t>(256);
   if (!ws.ok()) {
     set_error("sort: workspace too small");
     return WFPG_ERR_WORKSPACE;
@@ -203,11 +250,10 @@ int sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n_max, const int32_t* n_d
     int shift = 8 * p;
     k_sort_hist<<<(unsigned)nb, kSortBlock, 0, st>>>(ka, n_max, n_dev, shift, nb, hist);
     WFPG_CHECK_LAUNCH("k_sort_hist");
-    size_t mark = ws.off;
-    WFPG_TRY(scan_u32(hist, hist, 256 * nb, nullptr, nullptr, ws, st));
-    ws.off = mark;
+    k_sort_offsets<<<1, kOffThreads, 0, st>>>(hist, n_max, n_dev, dbase);
+    WFPG_CHECK_LAUNCH("k_sort_offsets");
     k_sort_scatter<<<(unsigned)nb, kSortBlock, 0, st>>>(ka, va, kb, vb, n_max, n_dev, shift, nb,
-                                                         hist);
+                                                         hist, dbase);
     WFPG_CHECK_LAUNCH("k_sort_scatter");
     uint64_t* tk = ka;
     ka = kb;
@@ -217,9 +263,10 @@ int sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n_max, const int32_t* n_d
     vb = tv;
   }
   if (ka != keys) {
-    // odd number of passes: copy back (device count may be smaller; copy n_max)
-    WFPG_CUDA(cudaMemcpyAsync(keys, ka, sizeof(uint64_t) * n_max, cudaMemcpyDeviceToDevice, st));
-    WFPG_CUDA(cudaMemcpyAsync(vals, va, sizeof(uint32_t) * n_max, cudaMemcpyDeviceToDevice, st));
+    // odd number of passes: copy the live prefix back
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_max, 256), kNumSMs * 8));
+    k_copy_pairs<<<grid, 256, 0, st>>>(ka, va, keys, vals, n_max, n_dev);
+    WFPG_CHECK_LAUNCH("k_copy_pairs");
   }
   return WFPG_OK;
 }

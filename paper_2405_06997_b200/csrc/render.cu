@@ -382,6 +382,7 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
       PartitionOut po{L.bin_node, L.bin_start, L.bin_count, nullptr, L.n_bins,
                       &L.stats->overflow, L.cap, nullptr,
                       guided_depth ? L.bin_slot : nullptr, L.lam};
+      po.clear_from = svo->level_off[cfg->l_min + 1];
       size_t mark = scratch.off;
       WFPG_TRY(partition_spatial(vv, svo->counter, svo->parent, L.lam_pos, nullptr, P, L.n_lam,
                                  cfg->l_min, cfg->c_ray, (int)svo->n_nodes, po, scratch, st));

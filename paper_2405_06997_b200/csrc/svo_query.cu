@@ -53,12 +53,12 @@ __global__ void k_splat_atomic(int32_t* __restrict__ leaf, const double* __restr
 
 __global__ void k_splat_keys(const int32_t* __restrict__ leaf, int64_t n_max,
                              const int32_t* __restrict__ n_dev, uint64_t* __restrict__ keys,
-                             uint32_t* __restrict__ idx) {
+                             uint32_t* __restrict__ idx, uint64_t sentinel) {
   int64_t n = dev_count(n_max, n_dev);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int32_t l = leaf[i];
-    keys[i] = l < 0 ? 0xFFFFFFFFull : (uint64_t)l;
+    keys[i] = l < 0 ? sentinel : (uint64_t)l;  // misses sort last
     idx[i] = (uint32_t)i;
   }
 }
@@ -68,12 +68,12 @@ __global__ void k_splat_segments(const uint64_t* __restrict__ keys, const uint32
                                  int64_t n_max, const int32_t* __restrict__ n_dev,
                                  const double* __restrict__ dirs, const double* __restrict__ rad,
                                  const double* __restrict__ normal, double* sum_a, double* sum_b,
-                                 double* w_a, double* w_b) {
+                                 double* w_a, double* w_b, uint64_t sentinel) {
   int64_t n = dev_count(n_max, n_dev);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t k = keys[i];
-    if (k == 0xFFFFFFFFull) continue;
+    if (k == sentinel) continue;
     if (i > 0 && keys[i - 1] == k) continue;
     int32_t l = (int32_t)k;
     double a0 = sum_a[3 * (int64_t)l], a1 = sum_a[3 * (int64_t)l + 1], a2 = sum_a[3 * (int64_t)l + 2];
@@ -127,11 +127,12 @@ int svo_accumulate(wfpg_svo* svo, const int32_t* leaf, const double* dirs, const
     set_error("accumulate: workspace too small");
     return WFPG_ERR_WORKSPACE;
   }
-  k_splat_keys<<<grid, 256, 0, st>>>(leaf, n, n_dev, keys, idx);
+  const uint64_t sentinel = (uint64_t)svo->n_nodes;
+  k_splat_keys<<<grid, 256, 0, st>>>(leaf, n, n_dev, keys, idx, sentinel);
   WFPG_CHECK_LAUNCH("k_splat_keys");
-  WFPG_TRY(sort_pairs(keys, idx, n, n_dev, 32, ws, st));
+  WFPG_TRY(sort_pairs(keys, idx, n, n_dev, bits_for(sentinel), ws, st));
   k_splat_segments<<<grid, 256, 0, st>>>(keys, idx, n, n_dev, dirs, rad, svo->normal, svo->sum_a,
-                                         svo->sum_b, svo->weight_a, svo->weight_b);
+                                         svo->sum_b, svo->weight_a, svo->weight_b, sentinel);
   WFPG_CHECK_LAUNCH("k_splat_segments");
   return WFPG_OK;
 }
