@@ -86,7 +86,7 @@ size_t update_exitance_ws_bytes(int64_t n_paths, int max_depth) {
 int update_exitance(wfpg_svo* svo, const int32_t* emit_depth, const double* emit_le,
                     const double* rec_T, const double* rec_pos, int rec_depths, int64_t n_paths,
                     int deterministic, int32_t* n_dep_out, Arena& ws, cudaStream_t st,
-                    bool propagate) {
+                    int propagate, uint8_t* dirty) {
   if (n_paths <= 0) return WFPG_OK;
   const int64_t m = n_paths * (int64_t)(rec_depths - 1 > 0 ? rec_depths - 1 : 1);
   uint32_t* counts = ws.take<uint32_t>(n_paths + 1);
@@ -119,6 +119,7 @@ int update_exitance(wfpg_svo* svo, const int32_t* emit_depth, const double* emit
     WFPG_TRY(svo_accumulate(svo, leaf, dirs, rad, m, n_dev, deterministic, ws, st));
     ws.off = mark;
   }
+  if (propagate == 2 && dirty) return svo_propagate_dirty(svo, leaf, m, n_dev, dirty, st);
   return propagate ? svo_propagate(svo, st) : WFPG_OK;
 }
 
@@ -140,5 +141,5 @@ extern "C" int wfpg_update_exitance(wfpg_svo* svo, const wfpg_paths* paths, int3
   Arena ws(workspace, ws_bytes);
   return update_exitance(svo, paths->emit_depth, paths->emit_le, paths->rec_T, paths->rec_pos,
                          paths->max_depth + 1, paths->n, deterministic, n_deposits_dev, ws,
-                         as_stream(stream), true);
+                         as_stream(stream), 1, nullptr);
 }

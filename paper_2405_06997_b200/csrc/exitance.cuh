@@ -7,6 +7,6 @@ size_t update_exitance_ws_bytes(int64_t n_paths, int max_depth);
 int update_exitance(wfpg_svo* svo, const int32_t* emit_depth, const double* emit_le,
                     const double* rec_T, const double* rec_pos, int rec_depths, int64_t n_paths,
                     int deterministic, int32_t* n_dep_out, Arena& ws, cudaStream_t st,
-                    bool propagate = true);
+                    int propagate = 1, uint8_t* dirty = nullptr);  // 0 none, 1 full, 2 dirty-only
 
 }  // namespace wfpg

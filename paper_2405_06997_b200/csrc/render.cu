@@ -167,6 +167,7 @@ struct PassLayout {
   double* tot;
   double* block_sums;
   double* cum;
+  uint8_t* dirty;
   double* upper_dirs;
   StatsDev* stats;
   size_t scratch_off;
@@ -207,6 +208,7 @@ static void carve_pass(Arena& a, const wfpg_svo* svo, const wfpg_camera* cam,
     L.n_bins = a.take<int32_t>(4);
     L.origins = a.take<double>(3 * L.cap);
     L.jitters = a.take<double>(2 * L.cap);
+    L.dirty = a.take<uint8_t>(svo->n_nodes);
     if (cfg->guided_depths > 0) {
       L.vals = a.take<double>(L.cap * (int64_t)L.n0 * L.n0);
       L.row_sum = a.take<double>(L.cap * (int64_t)L.n0);
@@ -426,11 +428,14 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
     wfpg_svo acc_view = leaf_acc_view(svo, cfg->leaf_acc);
     WFPG_TRY(update_exitance(&acc_view, paths->emit_depth, paths->emit_le, paths->rec_T,
                              paths->rec_pos, cfg->max_depth + 1, P, cfg->deterministic,
-                             &L.stats->deposits, scratch, st, false));
+                             &L.stats->deposits, scratch, st, 0));
   } else if (svo) {
+    // the SVO means are consistent at pass start, so only the deposited
+    // subtrees need refreshing (bitwise equal to the full recompute)
+    WFPG_CUDA(cudaMemsetAsync(L.dirty, 0, (size_t)svo->n_nodes, st));
     WFPG_TRY(update_exitance(svo, paths->emit_depth, paths->emit_le, paths->rec_T,
                              paths->rec_pos, cfg->max_depth + 1, P, cfg->deterministic,
-                             &L.stats->deposits, scratch, st));
+                             &L.stats->deposits, scratch, st, 2, L.dirty));
   }
   k_frame<<<(int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(L.n_pix, 256), kNumSMs * 8)), 256,
             0, st>>>(paths->radiance, L.n_pix, cfg->n_samples, frame);

@@ -191,6 +191,89 @@ __global__ void k_average_children(int64_t off, int64_t n, const int32_t* __rest
   }
 }
 
+// Dirty-only refresh after a splat (the reference's propagate_up(dirty),
+// svo.py:265-295): recompute the deposited leaves' means, flag their
+// ancestors, then average flagged nodes level by level.  Internal means are
+// pure functions of the leaf means, so this equals the full recompute bit for
+// bit while touching only the deposited subtrees.  `dirty` (n_nodes bytes)
+// must be zero on entry and is zero again on exit.
+__global__ void k_dirty_leaves(const int32_t* __restrict__ leaf, int64_t n_max,
+                               const int32_t* __restrict__ n_dev, const int32_t* __restrict__ parent,
+                               const double* __restrict__ sum_a, const double* __restrict__ sum_b,
+                               const double* __restrict__ w_a, const double* __restrict__ w_b,
+                               double* __restrict__ mean_a, double* __restrict__ mean_b,
+                               uint8_t* __restrict__ dirty) {
+  int64_t n = dev_count(n_max, n_dev);
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = leaf[k];
+    if (i < 0) continue;
+    const double wa = w_a[i], wb = w_b[i];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {  // identical values if several deposits share a leaf
+      mean_a[3 * i + c] = wa > 0.0 ? __ddiv_rn(sum_a[3 * i + c], wa) : 0.0;
+      mean_b[3 * i + c] = wb > 0.0 ? __ddiv_rn(sum_b[3 * i + c], wb) : 0.0;
+    }
+    for (int32_t p = parent[i]; p >= 0; p = parent[p]) dirty[p] = 1;
+  }
+}
+
+__global__ void k_average_dirty(int64_t off, int64_t n, const int32_t* __restrict__ child_base,
+                                const uint8_t* __restrict__ child_mask,
+                                const double* __restrict__ normal, double* mean_a, double* mean_b,
+                                uint8_t* __restrict__ dirty) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t node = off + k;
+    if (!dirty[node]) continue;
+    dirty[node] = 0;
+    const int64_t base = child_base[node];
+    const int cnt = __popc((uint32_t)child_mask[node]);
+    const double* pn = normal + 3 * node;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0;
+    for (int j = 0; j < cnt; ++j) {
+      const int64_t c = base + j;
+      const double* cn = normal + 3 * c;
+      const bool aligned = dot_einsum(cn[0], cn[1], cn[2], pn[0], pn[1], pn[2]) >= 0.0;
+      const double* ca = (aligned ? mean_a : mean_b) + 3 * c;
+      const double* cb = (aligned ? mean_b : mean_a) + 3 * c;
+      a0 = __dadd_rn(a0, ca[0]);
+      a1 = __dadd_rn(a1, ca[1]);
+      a2 = __dadd_rn(a2, ca[2]);
+      b0 = __dadd_rn(b0, cb[0]);
+      b1 = __dadd_rn(b1, cb[1]);
+      b2 = __dadd_rn(b2, cb[2]);
+    }
+    const double dc = (double)cnt;
+    mean_a[3 * node] = __ddiv_rn(a0, dc);
+    mean_a[3 * node + 1] = __ddiv_rn(a1, dc);
+    mean_a[3 * node + 2] = __ddiv_rn(a2, dc);
+    mean_b[3 * node] = __ddiv_rn(b0, dc);
+    mean_b[3 * node + 1] = __ddiv_rn(b1, dc);
+    mean_b[3 * node + 2] = __ddiv_rn(b2, dc);
+  }
+}
+
+int svo_propagate_dirty(wfpg_svo* svo, const int32_t* leaf, int64_t n_max, const int32_t* n_dev,
+                        uint8_t* dirty, cudaStream_t st) {
+  auto grid_for = [](int64_t m) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 256), (int64_t)kNumSMs * 8));
+  };
+  if (n_max > 0) {
+    k_dirty_leaves<<<grid_for(n_max), 256, 0, st>>>(leaf, n_max, n_dev, svo->parent, svo->sum_a,
+                                                    svo->sum_b, svo->weight_a, svo->weight_b,
+                                                    svo->mean_a, svo->mean_b, dirty);
+    WFPG_CHECK_LAUNCH("k_dirty_leaves");
+  }
+  for (int l = svo->depth - 1; l >= 0; --l) {
+    int64_t o = svo->level_off[l], m = svo->level_off[l + 1] - o;
+    k_average_dirty<<<grid_for(m), 256, 0, st>>>(o, m, svo->child_base, svo->child_mask,
+                                                 svo->normal, svo->mean_a, svo->mean_b, dirty);
+    WFPG_CHECK_LAUNCH("k_average_dirty");
+  }
+  return WFPG_OK;
+}
+
 int svo_propagate(wfpg_svo* svo, cudaStream_t st) {
   const int depth = svo->depth;
   auto grid_for = [](int64_t m) {

@@ -73,6 +73,8 @@ int svo_accumulate(wfpg_svo* svo, const int32_t* leaf, const double* dirs, const
                    int64_t n, const int32_t* n_dev, int deterministic, Arena& ws,
                    cudaStream_t st);
 int svo_propagate(wfpg_svo* svo, cudaStream_t st);
+int svo_propagate_dirty(wfpg_svo* svo, const int32_t* leaf, int64_t n_max, const int32_t* n_dev,
+                        uint8_t* dirty, cudaStream_t st);
 int svo_apply_leaf_acc(wfpg_svo* svo, const double* acc, cudaStream_t st);
 wfpg_svo leaf_acc_view(const wfpg_svo* svo, double* acc);
 

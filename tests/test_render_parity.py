@@ -183,6 +183,11 @@ def test_pt_first_pass(R, setup):
     assert np.array_equal(tree.weight_a, R["p0_svo_weight_a"])
     assert np.array_equal(tree.weight_b, R["p0_svo_weight_b"])
     np.testing.assert_allclose(tree.sum_a, R["p0_svo_sum_a"], rtol=1e-9, atol=1e-12)
+    # the pass refreshes only the deposited subtrees; a full recompute agrees bitwise
+    ma, mb = tree.mean_a, tree.mean_b
+    tree.propagate_up()
+    assert np.array_equal(ma.view(np.uint64), tree.mean_a.view(np.uint64))
+    assert np.array_equal(mb.view(np.uint64), tree.mean_b.view(np.uint64))
 
 
 @pytest.mark.parametrize("tag,product", [("p1", False), ("p1x", True)])
