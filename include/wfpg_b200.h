@@ -182,6 +182,10 @@ typedef struct wfpg_pass_config {
    * four planes) instead of the SVO, and the bottom-up refresh is skipped;
    * the caller all-reduces it and applies it with wfpg_svo_apply_leaf_acc. */
   double* leaf_acc;
+  /* 1: replay the pass as a CUDA graph.  The first call with a given
+   * (workspace, configuration, buffers) runs eagerly, the second captures,
+   * later calls replay; only sample_index may change between them. */
+  int32_t use_graph;
 } wfpg_pass_config;
 
 /* Per-pass statistics returned to the host: wavefront.py:81-85 (PassStats). */

@@ -81,6 +81,7 @@ class PassConfig(C.Structure):
         ("deterministic", c_i32),
         ("blur_radius", c_i32), ("blur_w", c_dbl * 33), ("upper_dirs", c_vp),
         ("pixel_offset", c_i64), ("n_pixels", c_i64), ("leaf_acc", c_vp),
+        ("use_graph", c_i32),
     ]
 
 

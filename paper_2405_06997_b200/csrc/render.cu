@@ -5,6 +5,8 @@
 // the worst case, so the whole pass is a single stream of launches with one
 // host synchronisation at the end (to return PassStats).
 #include <cstring>
+#include <utility>
+#include <vector>
 
 #include "exitance.cuh"
 #include "fields.cuh"
@@ -104,10 +106,11 @@ __global__ void k_bin_setup(const int32_t* __restrict__ n_bins, const int32_t* _
                             const int32_t* __restrict__ bin_count,
                             const uint32_t* __restrict__ sorted_items,
                             const int32_t* __restrict__ lam, const double* __restrict__ lam_pos,
-                            uint64_t seed, int64_t sample0, int depth, int jitter,
-                            double* __restrict__ origins, double* __restrict__ jitters,
-                            int32_t* __restrict__ bin_slot, int32_t* __restrict__ stat) {
+                            uint64_t seed, const int64_t* __restrict__ sample_dev, int depth,
+                            int jitter, double* __restrict__ origins,
+                            double* __restrict__ jitters, int32_t* __restrict__ stat) {
   const int64_t nb = *n_bins;
+  const int64_t sample0 = *sample_dev;  // device-resident so a captured graph can replay
   if (blockIdx.x == 0 && threadIdx.x == 0) *stat = (int32_t)nb;
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
        b += (int64_t)gridDim.x * blockDim.x) {
@@ -170,6 +173,7 @@ struct PassLayout {
   uint8_t* dirty;
   double* upper_dirs;
   StatsDev* stats;
+  int64_t* sample;  // device copy of cfg->sample_index (graph replays read it)
   size_t scratch_off;
 };
 
@@ -196,6 +200,7 @@ static void carve_pass(Arena& a, const wfpg_svo* svo, const wfpg_camera* cam,
   L.hit_t = a.take<double>(P);
   L.hit_tri = a.take<int32_t>(P);
   L.stats = a.take<StatsDev>(1);
+  L.sample = a.take<int64_t>(1);
   L.upper_dirs = a.take<double>(192);
   if (svo) {
     L.lam = a.take<int32_t>(P);
@@ -224,50 +229,32 @@ static void carve_pass(Arena& a, const wfpg_svo* svo, const wfpg_camera* cam,
   a.take<char>((int64_t)scratch);
 }
 
-// Optional live timing of the field kernels: CUDA events on the pass stream
-// plus an async copy of the device bin count into pinned memory, kept in a
-// ring and folded into totals by wfpg_profile_read (no per-pass host sync).
-struct ProfRec {
-  cudaEvent_t a, b;
-  int32_t* nb_host;
-  int n, depth;
-};
-struct Profile {
-  bool on = false;
-  ProfRec* ring = nullptr;
-  int cap = 0, used = 0;
-  double field_ms[kMaxDepth + 1];
+// Live timing of the field kernels that also works inside a replayed CUDA
+// graph: tiny stamp kernels on the pass stream read %globaltimer right
+// before and after each field launch and fold the interval, the launch's
+// bin count and its cone count into device accumulators.
+struct ProfDev {
+  unsigned long long t0[kMaxDepth + 1];
+  double ms[kMaxDepth + 1];
   double cones[kMaxDepth + 1];
-  int64_t launches[kMaxDepth + 1];
+  long long launches[kMaxDepth + 1];
 };
-static Profile g_prof;
+static ProfDev* g_prof_dev = nullptr;
+static bool g_prof_on = false;
 
-static void prof_alloc() {
-  if (!g_prof.ring) {
-    g_prof.cap = 4096;
-    g_prof.ring = new ProfRec[g_prof.cap];
-    for (int i = 0; i < g_prof.cap; ++i) {
-      cudaEventCreate(&g_prof.ring[i].a);
-      cudaEventCreate(&g_prof.ring[i].b);
-      cudaMallocHost(&g_prof.ring[i].nb_host, sizeof(int32_t));
-    }
-  }
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
-
-static ProfRec* prof_begin(cudaStream_t st, int depth) {
-  if (!g_prof.on || !g_prof.ring) return nullptr;
-  if (g_prof.used >= g_prof.cap) return nullptr;
-  ProfRec* r = &g_prof.ring[g_prof.used++];
-  r->depth = depth;
-  cudaEventRecord(r->a, st);
-  return r;
+__global__ void k_stamp_begin(ProfDev* p, int depth) { p->t0[depth] = globaltimer_ns(); }
+__global__ void k_stamp_end(ProfDev* p, int depth, int n, const int32_t* __restrict__ nb) {
+  unsigned long long t = globaltimer_ns();
+  p->ms[depth] += (double)(t - p->t0[depth]) * 1e-6;
+  p->cones[depth] += (double)(*nb) * n * n;
+  p->launches[depth] += 1;
 }
-static void prof_end(ProfRec* r, cudaStream_t st, int n, const int32_t* nb_dev) {
-  if (!r) return;
-  cudaEventRecord(r->b, st);
-  cudaMemcpyAsync(r->nb_host, nb_dev, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
-  r->n = n;
-}
+__global__ void k_set_i64(int64_t* dst, int64_t v) { *dst = v; }
 
 static bool cfg_ok(const wfpg_pass_config* cfg) {
   return cfg->max_depth >= 1 && cfg->max_depth <= kMaxDepth && cfg->guided_depths >= 0 &&
@@ -289,40 +276,12 @@ extern "C" size_t wfpg_render_workspace_bytes(const wfpg_scene* scene, const wfp
   return a.off + 4096;
 }
 
-extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camera* cam,
-                                const wfpg_pass_config* cfg, wfpg_paths* paths, double* frame,
-                                wfpg_pass_stats* stats, void* workspace, size_t ws_bytes,
-                                void* stream) {
-  if (!scene || !cam || !cfg || !paths || !frame || !cfg_ok(cfg)) {
-    set_error("wfpg_render_pass: bad arguments");
-    return WFPG_ERR_ARG;
-  }
-  if (svo && cfg->l_min >= svo->depth) {
-    set_error("l_min must be below the SVO depth");
-    return WFPG_ERR_ARG;
-  }
-  if (svo && cfg->product && cfg->guided_depths > 0 && !cfg->upper_dirs) {
-    set_error("wfpg_render_pass: product mode needs upper_dirs");
-    return WFPG_ERR_ARG;
-  }
-  if (paths->max_depth != cfg->max_depth) {
-    set_error("wfpg_render_pass: path state depth %d != config depth %d", paths->max_depth,
-              cfg->max_depth);
-    return WFPG_ERR_ARG;
-  }
-  cudaStream_t st = as_stream(stream);
-  Arena a(workspace, ws_bytes);
-  PassLayout L;
-  carve_pass(a, svo, cam, cfg, L);
-  if (!a.ok()) {
-    set_error("wfpg_render_pass: workspace too small (%zu < %zu)", ws_bytes, a.off);
-    return WFPG_ERR_WORKSPACE;
-  }
-  if (paths->n != L.P) {
-    set_error("wfpg_render_pass: path state holds %lld paths, pass needs %lld",
-              (long long)paths->n, (long long)L.P);
-    return WFPG_ERR_ARG;
-  }
+// Everything a pass enqueues after the sample index is set; capturable into a
+// CUDA graph (no host synchronisation, no host-dependent control flow).
+static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camera* cam,
+                        const wfpg_pass_config* cfg, wfpg_paths* paths, double* frame,
+                        void* workspace, size_t ws_bytes, const PassLayout& L, ProfDev* prof,
+                        cudaStream_t st) {
   Arena scratch(static_cast<char*>(workspace) + L.scratch_off, ws_bytes - L.scratch_off);
   const int64_t P = L.P;
   const SceneView sv = make_scene_view(scene);
@@ -334,11 +293,7 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
 
   WFPG_CUDA(cudaMemsetAsync(L.stats, 0, sizeof(StatsDev), st));
   const int64_t n_img = (int64_t)cam->width * cam->height;
-  if (cfg->pixel_offset < 0 || cfg->pixel_offset + L.n_pix > n_img) {
-    set_error("wfpg_render_pass: pixel range outside the image");
-    return WFPG_ERR_ARG;
-  }
-  WFPG_TRY(launch_camera_init(cv, pv, P, L.n_pix, n_img, cfg->pixel_offset, cfg->sample_index,
+  WFPG_TRY(launch_camera_init(cv, pv, P, L.n_pix, n_img, cfg->pixel_offset, L.sample,
                               cfg->seed, st));
 
   BlurParams bp{};
@@ -391,8 +346,7 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
       int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(L.cap, 128), kNumSMs * 8));
       k_bin_setup<<<bgrid, 128, 0, st>>>(L.n_bins, L.bin_node, L.bin_start, L.bin_count,
                                          po.sorted_items, L.lam, L.lam_pos, cfg->seed,
-                                         cfg->sample_index, depth, cfg->jitter, L.origins,
-                                         L.jitters, guided_depth ? L.bin_slot : nullptr,
+                                         L.sample, depth, cfg->jitter, L.origins, L.jitters,
                                          &L.stats->bins[depth]);
       WFPG_CHECK_LAUNCH("k_bin_setup");
       scratch.off = mark;
@@ -400,9 +354,15 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
         const int n = std::max(8, cfg->field_res >> (depth - 1));
         FieldOut fo{L.vals, L.row_sum, L.marg, L.tot, cfg->product ? L.block_sums : nullptr,
                     cfg->epsilon, L.cum};
-        ProfRec* pr = prof_begin(st, depth);
+        if (prof) {
+          k_stamp_begin<<<1, 1, 0, st>>>(prof, depth);
+          WFPG_CHECK_LAUNCH("k_stamp_begin");
+        }
         WFPG_TRY(launch_fields(sv, vv, L.origins, L.jitters, L.cap, L.n_bins, n, bp, fo, st));
-        prof_end(pr, st, n, L.n_bins);
+        if (prof) {
+          k_stamp_end<<<1, 1, 0, st>>>(prof, depth, n, L.n_bins);
+          WFPG_CHECK_LAUNCH("k_stamp_end");
+        }
         gv.mode = cfg->product ? 2 : 1;
         gv.n = n;
         gv.m = n / 8;
@@ -441,6 +401,151 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
             0, st>>>(paths->radiance, L.n_pix, cfg->n_samples, frame);
   WFPG_CHECK_LAUNCH("k_frame");
 
+  return WFPG_OK;
+}
+
+struct GraphEntry {
+  const void* ws;
+  uint64_t key;
+  cudaGraphExec_t exec;
+  uint64_t kernels;
+};
+static std::vector<GraphEntry> g_graphs;
+static std::vector<std::pair<const void*, uint64_t>> g_seen;
+
+static uint64_t fnv(uint64_t h, const void* p, size_t n) {
+  const unsigned char* b = static_cast<const unsigned char*>(p);
+  for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  return h;
+}
+
+// Everything that shapes the captured launch sequence: the config (minus the
+// sample index, which the graph reads from device memory), all device
+// pointers, sizes and the profiling switch.
+static uint64_t pass_key(const wfpg_scene* sc, const wfpg_svo* svo, const wfpg_camera* cam,
+                         const wfpg_pass_config* cfg, const wfpg_paths* paths, const double* frame,
+                         size_t ws_bytes, const ProfDev* prof) {
+  wfpg_pass_config c = *cfg;
+  c.sample_index = 0;
+  uint64_t h = 1469598103934665603ull;
+  h = fnv(h, &c, sizeof(c));
+  h = fnv(h, sc, sizeof(*sc));
+  if (svo) h = fnv(h, svo, sizeof(*svo));
+  h = fnv(h, cam, sizeof(*cam));
+  h = fnv(h, paths, sizeof(*paths));
+  h = fnv(h, &frame, sizeof(frame));
+  h = fnv(h, &ws_bytes, sizeof(ws_bytes));
+  h = fnv(h, &prof, sizeof(prof));
+  return h;
+}
+
+extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camera* cam,
+                                const wfpg_pass_config* cfg, wfpg_paths* paths, double* frame,
+                                wfpg_pass_stats* stats, void* workspace, size_t ws_bytes,
+                                void* stream) {
+  if (!scene || !cam || !cfg || !paths || !frame || !cfg_ok(cfg)) {
+    set_error("wfpg_render_pass: bad arguments");
+    return WFPG_ERR_ARG;
+  }
+  if (svo && cfg->l_min >= svo->depth) {
+    set_error("l_min must be below the SVO depth");
+    return WFPG_ERR_ARG;
+  }
+  if (svo && cfg->product && cfg->guided_depths > 0 && !cfg->upper_dirs) {
+    set_error("wfpg_render_pass: product mode needs upper_dirs");
+    return WFPG_ERR_ARG;
+  }
+  if (paths->max_depth != cfg->max_depth) {
+    set_error("wfpg_render_pass: path state depth %d != config depth %d", paths->max_depth,
+              cfg->max_depth);
+    return WFPG_ERR_ARG;
+  }
+  cudaStream_t st = as_stream(stream);
+  Arena a(workspace, ws_bytes);
+  PassLayout L;
+  carve_pass(a, svo, cam, cfg, L);
+  if (!a.ok()) {
+    set_error("wfpg_render_pass: workspace too small (%zu < %zu)", ws_bytes, a.off);
+    return WFPG_ERR_WORKSPACE;
+  }
+  if (paths->n != L.P) {
+    set_error("wfpg_render_pass: path state holds %lld paths, pass needs %lld",
+              (long long)paths->n, (long long)L.P);
+    return WFPG_ERR_ARG;
+  }
+  const int64_t n_img = (int64_t)cam->width * cam->height;
+  if (cfg->pixel_offset < 0 || cfg->pixel_offset + L.n_pix > n_img) {
+    set_error("wfpg_render_pass: pixel range outside the image");
+    return WFPG_ERR_ARG;
+  }
+  ProfDev* prof = g_prof_on ? g_prof_dev : nullptr;
+  k_set_i64<<<1, 1, 0, st>>>(L.sample, cfg->sample_index);
+  WFPG_CHECK_LAUNCH("k_set_i64");
+  if (!cfg->use_graph) {
+    WFPG_TRY(enqueue_pass(scene, svo, cam, cfg, paths, frame, workspace, ws_bytes, L, prof, st));
+  } else {
+    const uint64_t key = pass_key(scene, svo, cam, cfg, paths, frame, ws_bytes, prof);
+    GraphEntry* ge = nullptr;
+    for (auto& e : g_graphs)
+      if (e.ws == workspace && e.key == key) ge = &e;
+    bool seen = false;
+    for (auto& e : g_seen)
+      if (e.first == workspace && e.second == key) seen = true;
+    // graphs are captured / replayed on a private non-blocking stream joined to
+    // the caller's stream with events (the legacy default stream cannot be
+    // captured)
+    static cudaStream_t gs = nullptr;
+    static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    if (!gs) {
+      WFPG_CUDA(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking));
+      WFPG_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+      WFPG_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    }
+    if (ge || seen) {
+      WFPG_CUDA(cudaEventRecord(ev_fork, st));
+      WFPG_CUDA(cudaStreamWaitEvent(gs, ev_fork, 0));
+    }
+    if (ge) {
+      WFPG_CUDA(cudaGraphLaunch(ge->exec, gs));
+      count_launch(ge->kernels);
+      WFPG_CUDA(cudaEventRecord(ev_join, gs));
+      WFPG_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
+    } else if (!seen) {
+      // first pass of this configuration runs eagerly (one-time kernel attribute
+      // setup happens outside any capture); the next one is captured
+      g_seen.push_back({workspace, key});
+      WFPG_TRY(enqueue_pass(scene, svo, cam, cfg, paths, frame, workspace, ws_bytes, L, prof, st));
+    } else {
+      for (size_t i = 0; i < g_graphs.size(); ++i)
+        if (g_graphs[i].ws == workspace) {  // replaced configuration for this workspace
+          cudaGraphExecDestroy(g_graphs[i].exec);
+          g_graphs.erase(g_graphs.begin() + i);
+          break;
+        }
+      const uint64_t before = wfpg_launch_count();
+      WFPG_CUDA(cudaStreamBeginCapture(gs, cudaStreamCaptureModeThreadLocal));
+      int rc = enqueue_pass(scene, svo, cam, cfg, paths, frame, workspace, ws_bytes, L, prof, gs);
+      cudaGraph_t graph = nullptr;
+      cudaError_t ce = cudaStreamEndCapture(gs, &graph);
+      if (rc != WFPG_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+      }
+      if (ce != cudaSuccess) return cuda_status(ce, "cudaStreamEndCapture");
+      const uint64_t kernels = wfpg_launch_count() - before;
+      count_launch(0 - kernels);  // captured, not executed
+      cudaGraphExec_t exec;
+      ce = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ce != cudaSuccess) return cuda_status(ce, "cudaGraphInstantiate");
+      g_graphs.push_back({workspace, key, exec, kernels});
+      WFPG_CUDA(cudaGraphLaunch(exec, gs));
+      count_launch(kernels);
+      WFPG_CUDA(cudaEventRecord(ev_join, gs));
+      WFPG_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
+    }
+  }
+
   if (stats) {
     StatsDev h;
     WFPG_CUDA(cudaMemcpyAsync(&h, L.stats, sizeof(StatsDev), cudaMemcpyDeviceToHost, st));
@@ -467,35 +572,27 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
 
 extern "C" int wfpg_profile_enable(int32_t on) {
   using namespace wfpg;
-  g_prof.on = on != 0;
-  g_prof.used = 0;
-  if (g_prof.on) prof_alloc();
-  for (int d = 0; d <= kMaxDepth; ++d) {
-    g_prof.field_ms[d] = 0.0;
-    g_prof.cones[d] = 0.0;
-    g_prof.launches[d] = 0;
-  }
+  if (!g_prof_dev) WFPG_CUDA(cudaMalloc(&g_prof_dev, sizeof(ProfDev)));
+  WFPG_CUDA(cudaDeviceSynchronize());
+  WFPG_CUDA(cudaMemset(g_prof_dev, 0, sizeof(ProfDev)));
+  WFPG_CUDA(cudaDeviceSynchronize());
+  g_prof_on = on != 0;
   return WFPG_OK;
 }
 
-// Synchronises the recorded events and returns per-depth totals since enable.
+// Synchronises the device and returns per-depth totals since enable.
 extern "C" int wfpg_profile_read(double* field_ms, double* cones, int64_t* launches,
                                  int32_t max_depth) {
   using namespace wfpg;
-  for (int i = 0; i < g_prof.used; ++i) {
-    ProfRec& r = g_prof.ring[i];
-    WFPG_CUDA(cudaEventSynchronize(r.b));
-    float ms = 0.f;
-    WFPG_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
-    g_prof.field_ms[r.depth] += ms;
-    g_prof.cones[r.depth] += (double)(*r.nb_host) * r.n * r.n;
-    g_prof.launches[r.depth] += 1;
+  ProfDev h{};
+  if (g_prof_dev) {
+    WFPG_CUDA(cudaDeviceSynchronize());
+    WFPG_CUDA(cudaMemcpy(&h, g_prof_dev, sizeof(ProfDev), cudaMemcpyDeviceToHost));
   }
-  g_prof.used = 0;
   for (int d = 0; d <= max_depth && d <= kMaxDepth; ++d) {
-    field_ms[d] = g_prof.field_ms[d];
-    cones[d] = g_prof.cones[d];
-    launches[d] = g_prof.launches[d];
+    field_ms[d] = h.ms[d];
+    cones[d] = h.cones[d];
+    launches[d] = h.launches[d];
   }
   return WFPG_OK;
 }

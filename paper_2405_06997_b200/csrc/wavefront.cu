@@ -39,7 +39,9 @@ __global__ void k_camera(CameraView c, const uint64_t* __restrict__ keys,
 // Pass initialisation (wavefront.py:211-219): keys, camera rays, ctr = 2,
 // beta = 1, radiance = 0, alive, prev_pdf = -1, records, emitter slots.
 __global__ void k_init_paths(CameraView c, PathsView P, int64_t n_paths, int64_t n_pix,
-                             int64_t n_img, int64_t pix0, int64_t sample0, uint64_t seed) {
+                             int64_t n_img, int64_t pix0, const int64_t* __restrict__ sample_dev,
+                             uint64_t seed) {
+  const int64_t sample0 = *sample_dev;
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_paths;
        p += (int64_t)gridDim.x * blockDim.x) {
     int64_t pix = pix0 + p % n_pix;  // global pixel index
@@ -351,7 +353,7 @@ __global__ void __launch_bounds__(256) k_shade(SceneView s, GuideView g, PathsVi
 // internal launchers
 // ---------------------------------------------------------------------------
 int launch_camera_init(const CameraView& c, const PathsView& P, int64_t n_paths, int64_t n_pix,
-                       int64_t n_img, int64_t pix0, int64_t sample0, uint64_t seed,
+                       int64_t n_img, int64_t pix0, const int64_t* sample0, uint64_t seed,
                        cudaStream_t st) {
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_paths, 256), kNumSMs * 8));
   size_t rec_bytes = sizeof(double) * 3 * (size_t)P.rec_depths * (size_t)n_paths;

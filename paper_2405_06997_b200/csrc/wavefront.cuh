@@ -15,7 +15,7 @@ CameraView make_camera_view(const wfpg_camera* c);
 GuideView make_guide_view(const wfpg_guide* g);
 
 int launch_camera_init(const CameraView& c, const PathsView& P, int64_t n_paths, int64_t n_pix,
-                       int64_t n_img, int64_t pix0, int64_t sample0, uint64_t seed,
+                       int64_t n_img, int64_t pix0, const int64_t* sample0, uint64_t seed,
                        cudaStream_t st);
 int launch_intersect(const SceneView& s, const double* orig, const double* dirs,
                      const int32_t* active, int64_t n_max, const int32_t* n_dev, double tmin,

@@ -164,7 +164,7 @@ class PassRunner:
     nothing.  ``render_pass`` uses a cached runner per (scene, svo, cfg)."""
 
     def __init__(self, scene, svo, cfg, n_samples=1, deterministic=True, pixel_offset=0,
-                 n_pixels=None, leaf_acc=None):
+                 n_pixels=None, leaf_acc=None, use_graph=True):
         cam = scene.camera
         self.scene = scene
         self.svo = svo
@@ -194,6 +194,7 @@ class PassRunner:
         pc.n_pixels = self.n_pix
         self.leaf_acc = leaf_acc
         pc.leaf_acc = leaf_acc.data_ptr() if leaf_acc is not None else None
+        pc.use_graph = 1 if use_graph else 0  # replay the pass as a CUDA graph
         self.svo_abi = svo.abi() if svo is not None else None
         nbytes = _lib.load().wfpg_render_workspace_bytes(
             C.byref(scene.abi()), C.byref(self.svo_abi) if svo is not None else None,

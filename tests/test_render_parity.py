@@ -210,3 +210,28 @@ def test_guided_pass(R, setup, tag, product):
     rel = _rel(st.radiance, R[f"{tag}_radiance"])[ident]
     assert np.mean(rel <= 1e-4) >= 0.99
     np.testing.assert_allclose(frame.mean(), R[f"{tag}_frame"].mean(), rtol=0.05)
+
+
+def test_graph_replay_matches_eager(R, setup):
+    """Passes replayed from a captured CUDA graph are bitwise identical to
+    eagerly enqueued passes (same SVO learning sequence)."""
+    from paper_2405_06997_b200 import wavefront
+
+    sc, tree, c = setup
+    cfg = wavefront.GuidingConfig(max_depth=c["max_depth"], guided_depths=c["max_depth"],
+                                  field_res=c["field_res"], l_min=c["l_min"], c_ray=c["c_ray"],
+                                  seed=c["seed"])
+    results = []
+    for graph in (False, True):
+        _set_svo_state(tree, R, "p0")
+        r = wavefront.PassRunner(sc, tree, cfg, use_graph=graph)
+        frames = []
+        for sample in range(1, 6):  # eager, capture, then three replays
+            r.launch(sample)
+            frames.append(r.frame.cpu().numpy().copy())
+        results.append((frames, tree.mean_a, tree.sum_b))
+    (fe, ma_e, sb_e), (fg, ma_g, sb_g) = results
+    for a, b in zip(fe, fg):
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+    assert np.array_equal(ma_e.view(np.uint64), ma_g.view(np.uint64))
+    assert np.array_equal(sb_e.view(np.uint64), sb_g.view(np.uint64))
