@@ -412,17 +412,20 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
                                                  int32_t* bid) {
   const int lane = threadIdx.x & 31;
   // axis: the centre lane's direction, broadcast as floats (any common axis is
-  // valid); cmin rounded down to float and min-reduced in fp32 (conservative)
-  const double ax = (double)__shfl_sync(0xffffffffu, (float)dx, 12);
-  const double ay = (double)__shfl_sync(0xffffffffu, (float)dy, 12);
-  const double az = (double)__shfl_sync(0xffffffffu, (float)dz, 12);
-  const double al = sqrt(ax * ax + ay * ay + az * az);
-  float cm = __double2float_rd((dx * ax + dy * ay + dz * az) / al);
+  // valid).  The tile bound is evaluated in fp32 and widened by 4e-6 (cos)
+  // and 1e-5 (sin) — far above fp32 rounding — so it stays conservative.
+  const float fax = __shfl_sync(0xffffffffu, (float)dx, 12);
+  const float fay = __shfl_sync(0xffffffffu, (float)dy, 12);
+  const float faz = __shfl_sync(0xffffffffu, (float)dz, 12);
+  const float fal = sqrtf(fax * fax + fay * fay + faz * faz);
+  float cm = ((float)dx * fax + (float)dy * fay + (float)dz * faz) / fal - 4e-6f;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cm = fminf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
-  const double cmin = (double)cm;
-  const bool cull = cmin > 0.0;
-  const double reach = -(sqrt(fmax(1.0 - cmin * cmin, 0.0)) + 1e-6) * al;  // -|a| sin(th) - slack
+  const bool cull = cm > 0.0f;
+  const double ax = fax, ay = fay, az = faz;
+  // -|a| (sin(th) + slack): a ray within th of the axis cannot reach the
+  // inner side of a plane whose normal n has a.n below this
+  const double reach = -(double)((sqrtf(fmaxf(1.0f - cm * cm, 0.0f)) + 1e-5f) * fal);
   double best = 1e300;
   int32_t id = -1;
   for (int g = 0; g < n; g += 32) {

@@ -23,6 +23,8 @@ __device__ __forceinline__ int best_cone_level(double size, int depth, double ar
     if (diff < bd) {
       bd = diff;
       best = lv;
+    } else if (diff > bd) {
+      break;  // past the minimum: shallower levels only grow (unimodal)
     }
   }
   return best;
