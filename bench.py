@@ -320,39 +320,50 @@ def cpu_baseline(args, sc, tree, cfg, stats, seconds=None):
 
 
 def run_reference(args):
-    """--impl reference: the CPU port of the reference's guided pass on the
-    host cores (rank 0 only under torchrun)."""
+    """--impl reference: the CPU port of the reference's guided pass (oracle/,
+    C + OpenMP on every host core; the reference itself is Python/Cython and
+    does not travel to the GPU box).  No CUDA anywhere on this arm.  Setup
+    builds the SVO and runs the PT-first pass with the oracle; each step then
+    times a bounded sample of the guided pass's field generation, scaled to the
+    full pass by its bin counts.  Rank 0 only under torchrun."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import torch
+    from types import SimpleNamespace
 
-    sc, tree, pt_cfg, g_cfg, _ = build_workload(args)
-    from paper_2405_06997_b200 import wavefront
+    from oracle import render as OR
+    from paper_2405_06997_b200 import scene as S
 
-    wavefront.render_pass(sc, tree, pt_cfg, [0])
-    _, stats = wavefront.render_pass(sc, tree, g_cfg, [1])
-    torch.cuda.synchronize()
-    vals = []
-    for _ in range(args.warmup + args.steps):
-        cb = cpu_baseline(args, sc, tree, g_cfg, stats,
-                          seconds=max(5.0, args.cpu_seconds / 2))
-        vals.append(cb)
+    sc = S.load_scene(os.path.join(REPO, "scenes", "cornell.scene"))
+    cam = sc.camera
+    sc.camera = S.Camera(cam.position, cam.target, cam.up, cam.vfov_deg, args.width, args.height)
+    depth = args.svo_res.bit_length() - 1
+    cfg = SimpleNamespace(l_min=min(5, depth - 1), c_ray=512, field_res=args.field_res,
+                          guided_depths=args.depth, max_depth=args.depth, product=args.product,
+                          seed=args.seed, blur_sigma=1.0, epsilon=1e-2)
+    wl = OR.CpuWorkload(sc, args.svo_res, cfg, seed=args.seed)
+    n_paths = args.width * args.height
+    budget = min(10.0, 150.0 / max(1, args.warmup + args.steps))
+    vals, ms = [], []
+    for step in range(args.warmup + args.steps):
+        r = wl.time_pass(n_paths, budget, seed=step)
+        vals.append(r)
     timed = vals[args.warmup:]
     v = statistics.mean(x["value"] for x in timed)
     cb = dict(timed[-1])
     cb["value"] = v
-    n_paths = args.width * args.height
+    cb["sample"] += f"; {budget:.1f} s sample per step; " + cb.pop("setup")
+    cb.pop("pass_seconds", None)
     print(json.dumps({
         "impl": "reference", "metric": "path samples/sec (guided wavefront pass)", "value": v,
         "unit": "path samples/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": n_paths / v * 1e3 if v else None, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"C2: Cornell {args.width}x{args.height}, 1 spp guided pass, "
-                               f"SVO depth {tree.depth}, D={args.depth}"},
+                               f"SVO depth {depth}, D={args.depth}"},
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "path samples/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0}}))
+                "d2h_bytes_per_step": 0}}), flush=True)
 
 
 def main():

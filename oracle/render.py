@@ -407,13 +407,42 @@ def update_exitance(st, svo):
 # ---------------------------------------------------------------------------
 # CPU baseline for bench.py
 # ---------------------------------------------------------------------------
-def time_guided_pass_sample(scene, tree, cfg, stats, n_paths, seconds=20.0):
-    """Time the oracle's field generation on a bounded sample of each depth's
-    bins (OpenMP over every host core) and scale by the pass's bin counts;
-    field generation is >99% of the reference's guided pass."""
+def _time_fields(sc, svo, pts_by_depth, bins_by_depth, field_res, guided_depths, blur_sigma,
+                 epsilon, n_paths, seconds, rng):
+    """Per-bin field time at each depth on a bounded sample (OpenMP over all
+    host cores), scaled by that depth's bin count."""
     cores = os.cpu_count() or 1
+    budget = seconds / max(1, len(bins_by_depth))
+    total, parts = 0.0, []
+    for depth, bins in enumerate(bins_by_depth, start=1):
+        if depth > guided_depths or bins == 0:
+            continue
+        nf = max(8, field_res >> (depth - 1))
+        pts = pts_by_depth[min(depth, len(pts_by_depth)) - 1]
+        k, spent, done = cores, 0.0, 0
+        while spent < budget and done < bins:
+            k = min(k, bins - done)
+            idx = rng.integers(0, len(pts), k)
+            t0 = time.perf_counter()
+            fields(sc, svo, pts[idx], rng.random((k, 2)), nf, blur_sigma, epsilon)
+            spent += time.perf_counter() - t0
+            done += k
+            k *= 2
+        total += spent / max(done, 1) * bins
+        parts.append(f"d{depth}: {done} of {bins} bins at {nf}^2")
+    return {"value": n_paths / total if total > 0 else None, "unit": "path samples/s",
+            "cores": cores, "kind": "port",
+            "sample": "oracle field generation (cone trace + fold blur + floor, C/OpenMP on all "
+                      "host cores) for " + "; ".join(parts) + "; pass time = sum over depths of "
+                      "bins x measured per-bin time (fields are >99% of the reference's guided "
+                      "pass, SURVEY §0)",
+            "pass_seconds": total}
+
+
+def time_guided_pass_sample(scene, tree, cfg, stats, n_paths, seconds=20.0):
+    """CPU baseline next to a device run: the oracle gets the device SVO's
+    structure and exitance state and the device pass's bin counts."""
     sc = Scene(scene)
-    # the oracle SVO gets the device SVO's structure and exitance state
     built = {k: getattr(tree, k) for k in ("level_off", "codes", "child_base", "child_mask",
                                            "parent", "normal")}
     svo = Svo(built, tree.cube_lo, tree.cube_size, tree.resolution)
@@ -427,26 +456,37 @@ def time_guided_pass_sample(scene, tree, cfg, stats, n_paths, seconds=20.0):
     d /= np.linalg.norm(d, axis=1, keepdims=True)
     t, tri = intersect(sc, o, d)
     pts = (o + t[:, None] * d)[tri >= 0]
-    budget = seconds / max(1, len(stats.bins_per_depth))
-    total, parts = 0.0, []
-    for depth, bins in enumerate(stats.bins_per_depth, start=1):
-        if depth > cfg.guided_depths or bins == 0:
-            continue
-        nf = cfg.field_res_at(depth)
-        k, spent, done = max(cores, 1), 0.0, 0
-        while spent < budget and done < bins:
-            idx = rng.integers(0, len(pts), k)
-            t0 = time.perf_counter()
-            fields(sc, svo, pts[idx], rng.random((k, 2)), nf, cfg.blur_sigma, cfg.epsilon)
-            spent += time.perf_counter() - t0
-            done += k
-            k = min(2 * k, bins)
-        per_bin = spent / max(done, 1)
-        total += per_bin * bins
-        parts.append(f"d{depth}: {done} of {bins} bins at {nf}^2")
-    value = n_paths / total if total > 0 else None
-    return {"value": value, "unit": "path samples/s", "cores": cores, "kind": "port",
-            "sample": "oracle field generation (cone trace + blur + floor, C/OpenMP) on "
-                      + "; ".join(parts) + "; pass time = sum over depths of bins x per-bin "
-                      "time (fields are >99% of the reference's guided pass)",
-            "pass_seconds": total}
+    return _time_fields(sc, svo, [pts], stats.bins_per_depth, cfg.field_res, cfg.guided_depths,
+                        cfg.blur_sigma, cfg.epsilon, n_paths, seconds, rng)
+
+
+class CpuWorkload:
+    """The bench workload entirely on the host: oracle SVO build, a PT-first
+    oracle pass (exitance state + bins per depth + hit points per depth)."""
+
+    def __init__(self, scene, resolution, cfg, seed=0):
+        self.sc = Scene(scene)
+        t0 = time.perf_counter()
+        self.svo = Svo.from_scene(scene, resolution, seed)
+        self.build_s = time.perf_counter() - t0
+        stats = {}
+        pt_cfg = dict(max_depth=cfg.max_depth, guided_depths=0, field_res=cfg.field_res,
+                      l_min=cfg.l_min, c_ray=cfg.c_ray, seed=cfg.seed)
+        t0 = time.perf_counter()
+        _, st = render_pass(self.sc, self.svo, pt_cfg, 0, stats)
+        self.pt_s = time.perf_counter() - t0
+        self.bins = stats.get("bins", [])
+        rp, ed = st["rec_pos"], st["emit_depth"]
+        self.pts = []
+        for depth in range(1, cfg.max_depth + 1):
+            hit = np.any(rp[:, depth] != 0.0, axis=1)
+            self.pts.append(rp[hit, depth] if hit.any() else rp[:, 0])
+        self.cfg = cfg
+
+    def time_pass(self, n_paths, seconds, seed=0):
+        c = self.cfg
+        r = _time_fields(self.sc, self.svo, self.pts, self.bins, c.field_res, c.guided_depths,
+                         c.blur_sigma, c.epsilon, n_paths, seconds, np.random.default_rng(seed))
+        r["setup"] = (f"oracle SVO build {self.build_s:.1f} s, PT-first pass {self.pt_s:.1f} s "
+                      f"(bins per depth {self.bins})")
+        return r
