@@ -31,6 +31,8 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 HBM_PEAK_FALLBACK = 6650.0
+SCENES = {"c2": ("cornell.scene", 1024, "C2: Cornell"),
+          "c3": ("c3_two_rooms.scene", 2048, "C3: occluded-light two-room interior")}
 
 
 def parse():
@@ -41,7 +43,10 @@ def parse():
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--width", type=int, default=1920)
     p.add_argument("--height", type=int, default=1080)
-    p.add_argument("--svo-res", type=int, default=1024)
+    p.add_argument("--scene", default="c2", choices=list(SCENES),
+                   help="c2: Cornell box (the headline); c3: occluded-light two-room interior")
+    p.add_argument("--svo-res", type=int, default=None,
+                   help="SVO resolution (default 1024 for c2, 2048 for c3)")
     p.add_argument("--depth", type=int, default=4)
     p.add_argument("--field-res", type=int, default=128)
     p.add_argument("--product", action="store_true")
@@ -50,7 +55,10 @@ def parse():
                    help="budget of the CPU-baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    return p.parse_args()
+    a = p.parse_args()
+    if a.svo_res is None:
+        a.svo_res = SCENES[a.scene][1]
+    return a
 
 
 def peaks():
@@ -143,7 +151,7 @@ def build_workload(args, rank=0, world=1):
 
     from paper_2405_06997_b200 import scene as S, svo, wavefront
 
-    sc = S.load_scene(os.path.join(REPO, "scenes", "cornell.scene"))
+    sc = S.load_scene(os.path.join(REPO, "scenes", SCENES[args.scene][0]))
     cam = sc.camera
     # weak scaling: rank r renders band r of a width x (height * world) image
     sc.camera = S.Camera(cam.position, cam.target, cam.up, cam.vfov_deg, args.width,
@@ -157,6 +165,18 @@ def build_workload(args, rank=0, world=1):
         l_min=lmin, c_ray=512, field_res=args.field_res, guided_depths=g, max_depth=args.depth,
         product=args.product, seed=args.seed)
     return sc, tree, mk(0), mk(args.depth), build_ms
+
+
+def traffic(args):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
+    capture of this workload (profiles/traffic.json), else None."""
+    key = f"{args.scene}:{args.width}x{args.height}:R{args.svo_res}:D{args.depth}:N{args.field_res}"
+    try:
+        with open(os.path.join(REPO, "profiles", "traffic.json")) as fh:
+            t = json.load(fh).get(key)
+        return None if t is None else t["dram_read_bytes"] + t["dram_write_bytes"]
+    except (OSError, ValueError, KeyError):
+        return None
 
 
 def algorithmic_bytes_per_cone(svo_depth):
@@ -253,7 +273,7 @@ def run_b200(args):
                      "graph nodes)",
             "achieved": achieved,
             "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-            "frac": achieved / peak if peak else None, "traffic": None,
+            "frac": achieved / peak if peak else None, "traffic": traffic(args),
             "launch_ms": d1_ms, "bytes_per_launch": d1_bytes,
             "cones_per_launch": cones[1] / max(nl[1], 1), "bytes_per_cone": bpc,
             "gcones_per_s": (cones[1] / max(nl[1], 1)) / (d1_ms / 1e3) / 1e9 if d1_ms else None,
@@ -281,10 +301,10 @@ def run_b200(args):
         "metric": "path samples/sec (guided wavefront pass)",
         "value": value, "unit": "path samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic-free: "
-        "the bundled Cornell scene (pkg/scenes), path samples from the counter RNG",
-        "config": {"workload": f"C2: Cornell {args.width}x{args.height} per GPU, 1 spp guided "
-                               f"pass, SVO depth {tree.depth}, D={D}, G={D}, N0={args.field_res}, "
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic: "
+        f"scenes/{SCENES[args.scene][0]}, path samples from the counter RNG",
+        "config": {"workload": f"{SCENES[args.scene][2]} {args.width}x{args.height} per GPU, "
+                               f"1 spp guided pass, SVO depth {tree.depth}, D={D}, G={D}, N0={args.field_res}, "
                                f"l_min {g_cfg.l_min}, c_ray 512, "
                                f"{'product' if args.product else 'plain'} guiding",
                    "image": [args.width, args.height * world], "svo_nodes": tree.node_count,
@@ -334,7 +354,7 @@ def run_reference(args):
     from oracle import render as OR
     from paper_2405_06997_b200 import scene as S
 
-    sc = S.load_scene(os.path.join(REPO, "scenes", "cornell.scene"))
+    sc = S.load_scene(os.path.join(REPO, "scenes", SCENES[args.scene][0]))
     cam = sc.camera
     sc.camera = S.Camera(cam.position, cam.target, cam.up, cam.vfov_deg, args.width, args.height)
     depth = args.svo_res.bit_length() - 1
@@ -359,7 +379,7 @@ def run_reference(args):
         "unit": "path samples/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": n_paths / v * 1e3 if v else None, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"C2: Cornell {args.width}x{args.height}, 1 spp guided pass, "
+        "config": {"workload": f"{SCENES[args.scene][2]} {args.width}x{args.height}, 1 spp guided pass, "
                                f"SVO depth {depth}, D={args.depth}"},
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "path samples/s", "h2d_bytes_per_step": 0,

@@ -259,6 +259,56 @@ def gen_fields():
     save("fields_golden.npz", **out)
 
 
+# ---------------------------------------------------------------------------
+C3_CFG = dict(W=64, H=36, R=128, svo_seed=2, max_depth=5, field_res=32, l_min=3, c_ray=16,
+              seed=3)
+C3_SCENE = os.path.join(HERE, "..", "..", "scenes", "c3_two_rooms.scene")
+
+
+def gen_c3():
+    """C3 (procedural occluded-light interior, paper_2405_06997_b200/scenegen.py):
+    SVO arrays + digests, a PT-first pass and two guided passes (plain, then
+    product) learning from it, per-path records, bins and SVO state."""
+    c = C3_CFG
+    sc = rscene.load_scene(C3_SCENE)
+    cam = sc.camera
+    sc.camera = rscene.Camera(cam.position, cam.target, cam.up, cam.vfov_deg, c["W"], c["H"])
+    out = {"cfg_keys": np.array(list(c)), "cfg_vals": np.array(list(c.values()))}
+    dig = []
+    for res, seed in ((64, 1), (256, 0), (512, 0)):
+        frags = rsvo.voxelize(sc, res)
+        lo, side = rsvo.scene_cube(sc)
+        tree = rsvo.build_octree(frags, lo, side, res, seed)
+        row = [str(res), str(seed), str(len(frags)), str(tree.node_count),
+               digest(tree.level_off.astype(np.int64)), digest(tree.codes),
+               digest(tree.child_base.astype(np.int64)), digest(tree.child_mask),
+               digest(tree.parent.astype(np.int64)), digest(tree.normal)]
+        dig.append(",".join(row))
+        print(row)
+    out["svo_digests"] = np.array(dig)
+    tree = rsvo.build_from_scene(sc, c["R"], seed=c["svo_seed"])
+    out["svo_level_off"] = tree.level_off
+    out["svo_codes"] = tree.codes
+    out["svo_normal"] = tree.normal
+    passes = (("p0", 0, 0, False), ("p1", 1, c["max_depth"], False),
+              ("p2", 2, c["max_depth"], True))
+    for tag, sample, g, product in passes:
+        cfg = wavefront.GuidingConfig(max_depth=c["max_depth"], guided_depths=g,
+                                      field_res=c["field_res"], l_min=c["l_min"],
+                                      c_ray=c["c_ray"], seed=c["seed"], product=product)
+        f, st, cap = _capture_pass(sc, tree, cfg, sample)
+        out[tag + "_frame"] = f
+        for k in ("radiance", "rec_pos", "emit_depth"):
+            out[f"{tag}_{k}"] = cap["state"][k]
+        for k, v in _svo_state(tree).items():
+            out[f"{tag}_svo_" + k] = v
+        out[tag + "_bins_per_depth"] = np.array(st.bins_per_depth)
+        out[tag + "_rays_per_depth"] = np.array(st.rays_per_depth)
+        print(tag, "bins", st.bins_per_depth, "rays", st.rays_per_depth,
+              "deposits", int(tree.weight_a.sum() + tree.weight_b.sum()))
+    save("c3_golden.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["svo"]
     for w in which:
