@@ -186,6 +186,12 @@ typedef struct wfpg_pass_config {
    * (workspace, configuration, buffers) runs eagerly, the second captures,
    * later calls replay; only sample_index may change between them. */
   int32_t use_graph;
+  /* Optional (n_pixels,) int32 device buffer: the depth-1 bin node of every
+   * pixel, -1 where its depth-1 vertex is not binned (collect_bin_image,
+   * wavefront.py:221,254-256).  With several samples per pass the bin with
+   * the largest node id wins, as the reference's in-order assignment over
+   * node-sorted bins does. */
+  int32_t* bin_image;
 } wfpg_pass_config;
 
 /* Per-pass statistics returned to the host: wavefront.py:81-85 (PassStats). */
@@ -264,6 +270,13 @@ int wfpg_svo_build_sorted(const void* workspace, int64_t n_fragments,
 /* _kernels.pyx:591-658 (descend_point/descend_kernel) -> node, present, deepest. */
 int wfpg_descend(const wfpg_svo* svo, const double* points, int64_t n,
                  int32_t* out_node, uint8_t* out_present, int32_t* out_deepest, void* stream);
+
+/* _kernels.pyx:593-606: points -> int32 leaf coords (F,3) with the compiled
+ * quantisation (truncate (p - lo) * (R / size), clamp to [0, R-1]); cube_lo is
+ * a HOST pointer to 3 doubles.  Feeds wfpg_svo_build_structure for SVOs built
+ * from path vertices / synthetic points. */
+int wfpg_quantise_points(const double* cube_lo, double cube_size, int32_t resolution,
+                         const double* points, int64_t n, int32_t* out_coords, void* stream);
 
 /* svo.py:254-263 (accumulate_batch): deposits applied in input order.
  * deterministic=1 reproduces np.add.at's sequential order (sort + segmented
@@ -363,6 +376,13 @@ size_t wfpg_render_workspace_bytes(const wfpg_scene* scene, const wfpg_svo* svo,
 int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camera* cam,
                      const wfpg_pass_config* cfg, wfpg_paths* paths, double* frame,
                      wfpg_pass_stats* stats, void* workspace, size_t ws_bytes, void* stream);
+
+/* Eq. 7 running sum on the device (accumulation.py:50-60): acc[i] += hw *
+ * frame[i] (product rounded first, as numpy).  Non-finite frame values are
+ * skipped and set *nonfinite_flag (device int32, optional) so the host can
+ * raise like the reference. */
+int wfpg_frame_accumulate(double* acc, const double* frame, int64_t n, double hw,
+                          int32_t* nonfinite_flag, void* stream);
 
 /* Live timing of the per-depth field kernels inside wfpg_render_pass (CUDA
  * events on the pass stream; collected when a pass returns stats).

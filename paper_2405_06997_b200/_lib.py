@@ -82,6 +82,7 @@ class PassConfig(C.Structure):
         ("blur_radius", c_i32), ("blur_w", c_dbl * 33), ("upper_dirs", c_vp),
         ("pixel_offset", c_i64), ("n_pixels", c_i64), ("leaf_acc", c_vp),
         ("use_graph", c_i32),
+        ("bin_image", c_vp),
     ]
 
 
@@ -114,6 +115,8 @@ _SIGS = {
     "wfpg_svo_build_fill": (c_i32, [P(Svo), c_vp, c_vp, c_i64, c_u64, c_vp, c_size, c_vp]),
     "wfpg_svo_build_sorted": (c_i32, [c_vp, c_i64, P(c_vp), P(c_vp)]),
     "wfpg_descend": (c_i32, [P(Svo), c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "wfpg_frame_accumulate": (c_i32, [c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp]),
+    "wfpg_quantise_points": (c_i32, [c_vp, c_dbl, c_i32, c_vp, c_i64, c_vp, c_vp]),
     "wfpg_accumulate_workspace_bytes": (c_size, [c_i64]),
     "wfpg_svo_accumulate": (c_i32, [P(Svo), c_vp, c_vp, c_vp, c_i64, c_vp, c_i32, c_vp, c_size,
                                     c_vp]),

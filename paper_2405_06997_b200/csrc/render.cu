@@ -29,6 +29,23 @@ struct StatsDev {
   int32_t overflow;
 };
 
+// collect_bin_image (wavefront.py:254-256): depth-1 bin node per pixel; over
+// the samples of a multi-sample pass the largest node id wins (the reference
+// assigns bins in ascending node order, so the last write is the largest).
+__global__ void k_bin_image(const int32_t* __restrict__ bin_slot,
+                            const int32_t* __restrict__ bin_node, int64_t n_pix, int64_t n_samp,
+                            int32_t* __restrict__ image) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_pix;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    int32_t v = -1;
+    for (int64_t s = 0; s < n_samp; ++s) {
+      int32_t slot = bin_slot[s * n_pix + p];
+      if (slot >= 0) v = max(v, bin_node[slot]);
+    }
+    image[p] = v;
+  }
+}
+
 __global__ void k_flags_alive(const uint8_t* __restrict__ alive, int64_t n,
                               uint32_t* __restrict__ flags) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -332,13 +349,14 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
                                               L.lam_pos, L.total, L.n_lam, &L.stats->lam[depth]);
       WFPG_CHECK_LAUNCH("k_scatter_lambert");
       const bool guided_depth = depth <= cfg->guided_depths;
-      if (guided_depth) {
+      const bool want_image = depth == 1 && cfg->bin_image;
+      if (guided_depth || want_image) {
         WFPG_CUDA(cudaMemsetAsync(L.bin_slot, 0xFF, sizeof(int32_t) * P, st));
       }
       // bin slots of guided depths are written by the partition itself
       PartitionOut po{L.bin_node, L.bin_start, L.bin_count, nullptr, L.n_bins,
                       &L.stats->overflow, L.cap, nullptr,
-                      guided_depth ? L.bin_slot : nullptr, L.lam};
+                      (guided_depth || want_image) ? L.bin_slot : nullptr, L.lam};
       po.clear_from = svo->level_off[cfg->l_min + 1];
       size_t mark = scratch.off;
       WFPG_TRY(partition_spatial(vv, svo->counter, svo->parent, L.lam_pos, nullptr, P, L.n_lam,
@@ -350,6 +368,12 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
                                          &L.stats->bins[depth]);
       WFPG_CHECK_LAUNCH("k_bin_setup");
       scratch.off = mark;
+      if (want_image) {
+        int igrid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(L.n_pix, 256), kNumSMs * 8));
+        k_bin_image<<<igrid, 256, 0, st>>>(L.bin_slot, L.bin_node, L.n_pix, P / L.n_pix,
+                                           cfg->bin_image);
+        WFPG_CHECK_LAUNCH("k_bin_image");
+      }
       if (guided_depth) {
         const int n = std::max(8, cfg->field_res >> (depth - 1));
         FieldOut fo{L.vals, L.row_sum, L.marg, L.tot, cfg->product ? L.block_sums : nullptr,
@@ -402,6 +426,22 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
   WFPG_CHECK_LAUNCH("k_frame");
 
   return WFPG_OK;
+}
+
+// Eq. 7 running sum (accumulation.py:50-60): acc += hw * frame with the
+// product rounded first, as numpy's `weighted_sum += hw * frame`; flags
+// non-finite frame values (the reference raises on them).
+__global__ void k_frame_accumulate(double* __restrict__ acc, const double* __restrict__ frame,
+                                   int64_t n, double hw, int32_t* __restrict__ nonfinite) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double f = frame[i];
+    if (!isfinite(f)) {
+      if (nonfinite) atomicOr(nonfinite, 1);
+      continue;
+    }
+    acc[i] = __dadd_rn(acc[i], __dmul_rn(hw, f));
+  }
 }
 
 struct GraphEntry {
@@ -594,5 +634,20 @@ extern "C" int wfpg_profile_read(double* field_ms, double* cones, int64_t* launc
     cones[d] = h.cones[d];
     launches[d] = h.launches[d];
   }
+  return WFPG_OK;
+}
+
+extern "C" int wfpg_frame_accumulate(double* acc, const double* frame, int64_t n, double hw,
+                                     int32_t* nonfinite_flag, void* stream) {
+  if (n < 0 || (n > 0 && (!acc || !frame))) {
+    wfpg::set_error("wfpg_frame_accumulate: bad arguments");
+    return WFPG_ERR_ARG;
+  }
+  if (n == 0) return WFPG_OK;
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(wfpg::ceil_div(n, 256),
+                                                         (int64_t)wfpg::kNumSMs * 8));
+  k_frame_accumulate<<<grid, 256, 0, (cudaStream_t)stream>>>(acc, frame, n, hw,
+                                                                   nonfinite_flag);
+  WFPG_CHECK_LAUNCH("k_frame_accumulate");
   return WFPG_OK;
 }

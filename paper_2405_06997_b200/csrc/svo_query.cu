@@ -24,6 +24,19 @@ __global__ void k_descend(SvoView v, const double* __restrict__ pts, int64_t n,
   }
 }
 
+// Quantise points to leaf coordinates with the compiled kernel's formula
+// (_kernels.pyx:593-606): (long)((p - lo) * (R / size)), clamped to [0, R-1].
+__global__ void k_quantise(double lox, double loy, double loz, double scale, int32_t res,
+                           const double* __restrict__ pts, int64_t n,
+                           int32_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    out[3 * i] = quantise(pts[3 * i], lox, scale, res);
+    out[3 * i + 1] = quantise(pts[3 * i + 1], loy, scale, res);
+    out[3 * i + 2] = quantise(pts[3 * i + 2], loz, scale, res);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // exitance splat
 // ---------------------------------------------------------------------------
@@ -368,6 +381,23 @@ extern "C" int wfpg_descend(const wfpg_svo* svo, const double* points, int64_t n
   int grid = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)kNumSMs * 8);
   k_descend<<<grid, 256, 0, as_stream(stream)>>>(v, points, n, out_node, out_present, out_deepest);
   WFPG_CHECK_LAUNCH("k_descend");
+  return WFPG_OK;
+}
+
+extern "C" int wfpg_quantise_points(const double* cube_lo, double cube_size, int32_t resolution,
+                                    const double* points, int64_t n, int32_t* out_coords,
+                                    void* stream) {
+  if (!cube_lo || !(cube_size > 0.0) || resolution < 1 || n < 0 ||
+      (n > 0 && (!points || !out_coords))) {
+    set_error("wfpg_quantise_points: bad arguments");
+    return WFPG_ERR_ARG;
+  }
+  if (n == 0) return WFPG_OK;
+  double scale = (double)resolution / cube_size;
+  int grid = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)kNumSMs * 8);
+  k_quantise<<<grid, 256, 0, as_stream(stream)>>>(cube_lo[0], cube_lo[1], cube_lo[2], scale,
+                                                  resolution, points, n, out_coords);
+  WFPG_CHECK_LAUNCH("k_quantise");
   return WFPG_OK;
 }
 

@@ -417,6 +417,31 @@ def build_octree(fragments, cube_lo, cube_size, resolution, seed=0):
                   seed)
 
 
+def quantise_points(points, cube_lo, cube_size, resolution, out=None):
+    """Device int32 leaf coordinates (n,3) of device fp64 points (n,3), with the
+    compiled quantisation (_kernels.pyx:593-606)."""
+    resolution = _check_resolution(resolution)
+    n = int(points.shape[0])
+    out = _dev.empty((n, 3), np.int32) if out is None else out
+    lo = (_lib.C.c_double * 3)(*[float(x) for x in cube_lo])
+    _lib.call("wfpg_quantise_points", lo, float(cube_size), resolution, _lib.ptr(points), n,
+              _lib.ptr(out), _dev.stream())
+    return out
+
+
+def build_from_points(points, normals, cube_lo, cube_size, resolution, seed=0):
+    """SVO over path vertices / surface points: quantise the
+    device points, then the same Morton -> sort -> unique -> levels -> dual
+    normal build as build_octree with one fragment per point (normal = its
+    own normal, k-means stream ids from the node codes as svo.py:481,497)."""
+    n = int(points.shape[0])
+    if n == 0:
+        raise ValueError("cannot build an octree from an empty fragment list")
+    coords = quantise_points(points, cube_lo, cube_size, resolution)
+    idx = _dev.torch().arange(n, dtype=_dev.torch().int32, device=coords.device)
+    return _build(coords, idx, normals, cube_lo, cube_size, resolution, seed)
+
+
 def build_from_scene(scene, resolution, seed=0):
     """Voxelise + build entirely on the device (no host round trip)."""
     coords, tris = _voxelize_device(scene, resolution)

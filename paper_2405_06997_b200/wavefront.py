@@ -164,7 +164,7 @@ class PassRunner:
     nothing.  ``render_pass`` uses a cached runner per (scene, svo, cfg)."""
 
     def __init__(self, scene, svo, cfg, n_samples=1, deterministic=True, pixel_offset=0,
-                 n_pixels=None, leaf_acc=None, use_graph=True):
+                 n_pixels=None, leaf_acc=None, use_graph=True, collect_bin_image=False):
         cam = scene.camera
         self.scene = scene
         self.svo = svo
@@ -195,6 +195,9 @@ class PassRunner:
         self.leaf_acc = leaf_acc
         pc.leaf_acc = leaf_acc.data_ptr() if leaf_acc is not None else None
         pc.use_graph = 1 if use_graph else 0  # replay the pass as a CUDA graph
+        # depth-1 bin node per pixel (wavefront.py:221,254-256)
+        self.bin_image = _dev.empty((self.n_pix,), np.int32) if collect_bin_image else None
+        pc.bin_image = self.bin_image.data_ptr() if collect_bin_image else None
         self.svo_abi = svo.abi() if svo is not None else None
         nbytes = _lib.load().wfpg_render_workspace_bytes(
             C.byref(scene.abi()), C.byref(self.svo_abi) if svo is not None else None,
@@ -228,12 +231,13 @@ class PassRunner:
 _RUNNERS = {}
 
 
-def _runner(scene, svo, cfg, n_samples):
-    key = (id(scene), id(svo), tuple(sorted(vars(cfg).items())), n_samples)
+def _runner(scene, svo, cfg, n_samples, collect_bin_image=False):
+    key = (id(scene), id(svo), tuple(sorted(vars(cfg).items())), n_samples,
+           bool(collect_bin_image))
     r = _RUNNERS.get(key)
     if r is None or r.scene is not scene or r.svo is not svo:
         _RUNNERS.clear()  # one live configuration at a time keeps HBM bounded
-        r = PassRunner(scene, svo, cfg, n_samples)
+        r = PassRunner(scene, svo, cfg, n_samples, collect_bin_image=collect_bin_image)
         _RUNNERS[key] = r
     return r
 
@@ -255,11 +259,10 @@ def render_pass(scene, svo, cfg, sample_indices, collect_bin_image=False, out=No
         raise ValueError("render_pass needs at least one sample index")
     if np.any(np.diff(samples) != 1):
         raise ValueError("render_pass on the device takes consecutive sample indices")
-    if collect_bin_image:
-        raise NotImplementedError("collect_bin_image is not supported by the device pass yet")
     if svo is not None:
         cfg.validate(svo.depth)
-    r = _runner(scene, svo, cfg, len(samples))
+    collect = bool(collect_bin_image) and svo is not None
+    r = _runner(scene, svo, cfg, len(samples), collect)
     r.launch(int(samples[0]))
     cam = scene.camera
     if out is not None:
@@ -267,8 +270,15 @@ def render_pass(scene, svo, cfg, sample_indices, collect_bin_image=False, out=No
         dst = t.from_numpy(out).view(-1, 3)
         dst.copy_(r.frame, non_blocking=dst.is_pinned())
         t.cuda.current_stream().synchronize()
-        return out, r.pass_stats()
-    frame = _dev.download(r.frame).reshape(cam.height, cam.width, 3)
+        frame = out
+    else:
+        frame = _dev.download(r.frame).reshape(cam.height, cam.width, 3)
+    if collect_bin_image:
+        if collect:
+            img = _dev.download(r.bin_image).astype(np.int64).reshape(cam.height, cam.width)
+        else:
+            img = np.full((cam.height, cam.width), -1, dtype=np.int64)
+        return frame, r.pass_stats(), img
     return frame, r.pass_stats()
 
 

@@ -309,6 +309,45 @@ def gen_c3():
     save("c3_golden.npz", **out)
 
 
+# ---------------------------------------------------------------------------
+def gen_cli():
+    """collect_bin_image of render_pass (1- and 2-sample PT passes) and whole
+    CLI runs (cli.run) on the scene file's own 64x64 camera."""
+    import tempfile
+
+    from wfpg import cli
+
+    c = RENDER_CFG
+    out = {}
+    sc = load_scene("cornell.scene", c["W"], c["H"])
+    tree = rsvo.build_from_scene(sc, c["R"], seed=c["svo_seed"])
+    cfg = wavefront.GuidingConfig(max_depth=c["max_depth"], guided_depths=0,
+                                  field_res=c["field_res"], l_min=c["l_min"], c_ray=c["c_ray"],
+                                  seed=c["seed"])
+    for tag, samples in (("bins1", [0]), ("bins2", [0, 1])):
+        frame, st, img = wavefront.render_pass(sc, tree, cfg, samples, collect_bin_image=True)
+        out[tag + "_image"] = img
+        out[tag + "_frame"] = frame
+        out[tag + "_bins_per_depth"] = np.array(st.bins_per_depth)
+    tmp = tempfile.mkdtemp()
+    runs = (("pt", dict(mode="pt", spp=2)),
+            ("wfpg", dict(mode="wfpg", spp=3, depth=4, svo_res=64, field_res=32, lmin=3,
+                          cray=16, seed=5)),
+            ("prod", dict(mode="wfpg-product", spp=2, depth=3, guided_depths=3, svo_res=32, field_res=16,
+                          lmin=2, cray=8, seed=1, heuristic="linear")))
+    for tag, kw in runs:
+        conf = cli.RunConfig(scene=os.path.join(SCENES, "cornell.scene"),
+                             out=os.path.join(tmp, tag + ".pfm"), **kw)
+        logs = []
+        status, frame = cli.run(conf, log=logs.append)
+        assert status == 0
+        out[f"cli_{tag}_frame"] = frame
+        out[f"cli_{tag}_log"] = np.array([ln for ln in logs if ln.startswith("sample ")])
+        out[f"cli_{tag}_config"] = np.array(conf.to_json())
+        print(tag, frame.mean(), logs[-3:])
+    save("cli_golden.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["svo"]
     for w in which:
