@@ -194,19 +194,29 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    # one GPU per rank; WFPG_DIST_BACKEND=gloo + a shared device lets the
+    # multi-rank path be exercised on a 1-GPU box (functional check only)
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    backend = os.environ.get("WFPG_DIST_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     sc, tree, pt_cfg, g_cfg, build_ms = build_workload(args, rank, world)
     lib = _lib.load()
 
     from paper_2405_06997_b200 import multigpu
 
-    sync_svo = multigpu.ExitanceAllReduce(tree) if world > 1 else None
+    # per-pass SVO sync: every rank exports its deposits, all-gathers the
+    # lists and splats them in global path order (multigpu.DepositExchange)
+    sync_svo = multigpu.DepositExchange(tree) if world > 1 else None
     off, npx = multigpu.band(args.width * args.height * world, rank, world)
-    acc = sync_svo.acc if sync_svo is not None else None
-    pt = wavefront.PassRunner(sc, tree, pt_cfg, pixel_offset=off, n_pixels=npx, leaf_acc=acc)
-    gr = wavefront.PassRunner(sc, tree, g_cfg, pixel_offset=off, n_pixels=npx, leaf_acc=acc)
+    pt = wavefront.PassRunner(sc, tree, pt_cfg, pixel_offset=off, n_pixels=npx,
+                              deposit_sink=sync_svo)
+    gr = wavefront.PassRunner(sc, tree, g_cfg, pixel_offset=off, n_pixels=npx,
+                              deposit_sink=sync_svo)
 
     def one_pass(runner, sample, stats=False):
         runner.launch(sample, want_stats=stats)
@@ -229,7 +239,7 @@ def run_b200(args):
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     stream = torch.cuda.current_stream()
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev) as clocks:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -252,7 +262,8 @@ def run_b200(args):
     lib.wfpg_profile_read(fms, cones, nl, D)
     lib.wfpg_profile_enable(0)
     if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([ms], device="cuda" if backend == "nccl" else "cpu",
+                         dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
@@ -296,6 +307,27 @@ def run_b200(args):
                "h2d_bytes_per_step": C.sizeof(_lib.PassConfig) + C.sizeof(_lib.Camera),
                "d2h_bytes_per_step": frame_bytes + C.sizeof(_lib.PassStats),
                "api": "paper_2405_06997_b200.wavefront.render_pass -> numpy frame"}
+    elif world > 1 and not args.no_e2e:
+        # per rank: pass + deposit exchange + its band of the frame to pinned
+        # host memory; whole-job time = max over ranks
+        host = torch.empty((npx, 3), dtype=torch.float64, pin_memory=True)
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            one_pass(gr, sample)
+            sample += 1
+            host.copy_(gr.frame, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64,
+                             device="cuda" if backend == "nccl" else "cpu")
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+        e2e = {"value": n_paths * world * args.steps / float(e2e_s.item()),
+               "unit": "path samples/s",
+               "h2d_bytes_per_step": C.sizeof(_lib.PassConfig) + C.sizeof(_lib.Camera),
+               "d2h_bytes_per_step": npx * 3 * 8 + 4,
+               "api": "wavefront.PassRunner.launch + multigpu.DepositExchange per rank, "
+                      "band frame -> pinned host; max over ranks"}
 
     out = {
         "metric": "path samples/sec (guided wavefront pass)",
@@ -309,7 +341,8 @@ def run_b200(args):
                                f"{'product' if args.product else 'plain'} guiding",
                    "image": [args.width, args.height * world], "svo_nodes": tree.node_count,
                    "l2": "inputs larger than L2 (path state + guide tables > 126 MB)",
-                   "parallelism": f"image bands x{world}, NCCL all-reduce of leaf exitance"},
+                   "parallelism": f"image bands x{world}" + (
+                       f", per-pass deposit all-gather ({backend})" if world > 1 else "")},
         "bins_per_depth": stats.bins_per_depth, "rays_per_depth": stats.rays_per_depth,
         "svo_build_ms": build_ms,
         "gpu_launches": int(launches),

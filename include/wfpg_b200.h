@@ -192,6 +192,21 @@ typedef struct wfpg_pass_config {
    * the largest node id wins, as the reference's in-order assignment over
    * node-sorted bins does. */
   int32_t* bin_image;
+  /* Optional deposit export for multi-GPU runs (the sparse
+   * alternative to a per-leaf all-reduce).  When dep_leaf is non-NULL the
+   * pass writes its Eq. 5 deposits (leaf id or -1, unit direction, radiance)
+   * in path-major / vertex-ascending order into these device buffers, the
+   * count into *dep_count, and leaves the SVO untouched; dep_capacity must be
+   * >= n_pixels * n_samples * max_depth.  Concatenating the ranks' lists in
+   * band order gives the global path order, so splatting the concatenation
+   * deterministically (wfpg_svo_accumulate) and refreshing
+   * (wfpg_svo_refresh_leaves) reproduces a 1-GPU update of the same paths
+   * bit for bit.  Takes precedence over leaf_acc. */
+  int32_t* dep_leaf;
+  double* dep_dir;
+  double* dep_rad;
+  int32_t* dep_count;
+  int64_t dep_capacity;
 } wfpg_pass_config;
 
 /* Per-pass statistics returned to the host: wavefront.py:81-85 (PassStats). */
@@ -270,6 +285,14 @@ int wfpg_svo_build_sorted(const void* workspace, int64_t n_fragments,
 /* _kernels.pyx:591-658 (descend_point/descend_kernel) -> node, present, deepest. */
 int wfpg_descend(const wfpg_svo* svo, const double* points, int64_t n,
                  int32_t* out_node, uint8_t* out_present, int32_t* out_deepest, void* stream);
+
+/* Bottom-up refresh of the leaves in leaf[0..n) and their ancestors only
+ * (svo.py:265-313 with dirty leaves): leaf means from sum / weight, then the
+ * dirty ancestors level by level; bitwise equal to wfpg_svo_propagate when
+ * the means were consistent before the deposits.  leaf < 0 entries are
+ * ignored.  dirty: n_nodes bytes of device scratch (zeroed here). */
+int wfpg_svo_refresh_leaves(wfpg_svo* svo, const int32_t* leaf, int64_t n, uint8_t* dirty,
+                            void* stream);
 
 /* _kernels.pyx:593-606: points -> int32 leaf coords (F,3) with the compiled
  * quantisation (truncate (p - lo) * (R / size), clamp to [0, R-1]); cube_lo is

@@ -83,6 +83,11 @@ class PassConfig(C.Structure):
         ("pixel_offset", c_i64), ("n_pixels", c_i64), ("leaf_acc", c_vp),
         ("use_graph", c_i32),
         ("bin_image", c_vp),
+        ("dep_leaf", c_vp),
+        ("dep_dir", c_vp),
+        ("dep_rad", c_vp),
+        ("dep_count", c_vp),
+        ("dep_capacity", c_i64),
     ]
 
 
@@ -115,6 +120,7 @@ _SIGS = {
     "wfpg_svo_build_fill": (c_i32, [P(Svo), c_vp, c_vp, c_i64, c_u64, c_vp, c_size, c_vp]),
     "wfpg_svo_build_sorted": (c_i32, [c_vp, c_i64, P(c_vp), P(c_vp)]),
     "wfpg_descend": (c_i32, [P(Svo), c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "wfpg_svo_refresh_leaves": (c_i32, [P(Svo), c_vp, c_i64, c_vp, c_vp]),
     "wfpg_frame_accumulate": (c_i32, [c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp]),
     "wfpg_quantise_points": (c_i32, [c_vp, c_dbl, c_i32, c_vp, c_i64, c_vp, c_vp]),
     "wfpg_accumulate_workspace_bytes": (c_size, [c_i64]),

@@ -86,14 +86,19 @@ size_t update_exitance_ws_bytes(int64_t n_paths, int max_depth) {
 int update_exitance(wfpg_svo* svo, const int32_t* emit_depth, const double* emit_le,
                     const double* rec_T, const double* rec_pos, int rec_depths, int64_t n_paths,
                     int deterministic, int32_t* n_dep_out, Arena& ws, cudaStream_t st,
-                    int propagate, uint8_t* dirty) {
+                    int propagate, uint8_t* dirty, const DepositSink* sink) {
   if (n_paths <= 0) return WFPG_OK;
   const int64_t m = n_paths * (int64_t)(rec_depths - 1 > 0 ? rec_depths - 1 : 1);
+  if (sink && (sink->capacity < m || !sink->leaf || !sink->dir || !sink->rad || !sink->count)) {
+    set_error("update_exitance: deposit sink needs capacity >= n_paths * max_depth (%lld)",
+              (long long)m);
+    return WFPG_ERR_ARG;
+  }
   uint32_t* counts = ws.take<uint32_t>(n_paths + 1);
   uint32_t* offs = ws.take<uint32_t>(n_paths + 1);
-  int32_t* leaf = ws.take<int32_t>(m);
-  double* dirs = ws.take<double>(3 * m);
-  double* rad = ws.take<double>(3 * m);
+  int32_t* leaf = sink ? sink->leaf : ws.take<int32_t>(m);
+  double* dirs = sink ? sink->dir : ws.take<double>(3 * m);
+  double* rad = sink ? sink->rad : ws.take<double>(3 * m);
   uint32_t* total = ws.take<uint32_t>(2);
   if (!ws.ok()) {
     set_error("update_exitance: workspace too small");
@@ -114,6 +119,10 @@ int update_exitance(wfpg_svo* svo, const int32_t* emit_depth, const double* emit
   const int32_t* n_dev = reinterpret_cast<const int32_t*>(total);
   if (n_dep_out)
     WFPG_CUDA(cudaMemcpyAsync(n_dep_out, total, sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+  if (sink) {
+    WFPG_CUDA(cudaMemcpyAsync(sink->count, total, sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    return WFPG_OK;
+  }
   {
     size_t mark = ws.off;
     WFPG_TRY(svo_accumulate(svo, leaf, dirs, rad, m, n_dev, deterministic, ws, st));

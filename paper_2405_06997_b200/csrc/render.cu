@@ -406,7 +406,16 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
                           cfg->russian_roulette != 0, cfg->rr_depth, st));
   }
 
-  if (svo && cfg->leaf_acc) {
+  if (svo && cfg->dep_leaf) {
+    // multi-GPU: export this rank's deposits; the caller gathers every rank's
+    // lists and splats them in global path order (wfpg_svo_accumulate +
+    // wfpg_svo_refresh_leaves), so all ranks end with the same SVO
+    DepositSink sink{cfg->dep_leaf, cfg->dep_dir, cfg->dep_rad, cfg->dep_count,
+                     cfg->dep_capacity};
+    WFPG_TRY(update_exitance(svo, paths->emit_depth, paths->emit_le, paths->rec_T,
+                             paths->rec_pos, cfg->max_depth + 1, P, cfg->deterministic,
+                             &L.stats->deposits, scratch, st, 0, nullptr, &sink));
+  } else if (svo && cfg->leaf_acc) {
     int64_t nleaf = svo->level_off[svo->depth + 1] - svo->level_off[svo->depth];
     WFPG_CUDA(cudaMemsetAsync(cfg->leaf_acc, 0, sizeof(double) * 8 * nleaf, st));
     wfpg_svo acc_view = leaf_acc_view(svo, cfg->leaf_acc);

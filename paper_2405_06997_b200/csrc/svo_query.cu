@@ -384,6 +384,17 @@ extern "C" int wfpg_descend(const wfpg_svo* svo, const double* points, int64_t n
   return WFPG_OK;
 }
 
+extern "C" int wfpg_svo_refresh_leaves(wfpg_svo* svo, const int32_t* leaf, int64_t n,
+                                       uint8_t* dirty, void* stream) {
+  if (!svo_ok(svo) || n < 0 || (n > 0 && !leaf) || !dirty) {
+    set_error("wfpg_svo_refresh_leaves: bad arguments");
+    return WFPG_ERR_ARG;
+  }
+  cudaStream_t st = as_stream(stream);
+  WFPG_CUDA(cudaMemsetAsync(dirty, 0, (size_t)svo->n_nodes, st));
+  return svo_propagate_dirty(svo, leaf, n, nullptr, dirty, st);
+}
+
 extern "C" int wfpg_quantise_points(const double* cube_lo, double cube_size, int32_t resolution,
                                     const double* points, int64_t n, int32_t* out_coords,
                                     void* stream) {

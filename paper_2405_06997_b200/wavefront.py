@@ -164,7 +164,8 @@ class PassRunner:
     nothing.  ``render_pass`` uses a cached runner per (scene, svo, cfg)."""
 
     def __init__(self, scene, svo, cfg, n_samples=1, deterministic=True, pixel_offset=0,
-                 n_pixels=None, leaf_acc=None, use_graph=True, collect_bin_image=False):
+                 n_pixels=None, leaf_acc=None, use_graph=True, collect_bin_image=False,
+                 deposit_sink=None):
         cam = scene.camera
         self.scene = scene
         self.svo = svo
@@ -198,6 +199,11 @@ class PassRunner:
         # depth-1 bin node per pixel (wavefront.py:221,254-256)
         self.bin_image = _dev.empty((self.n_pix,), np.int32) if collect_bin_image else None
         pc.bin_image = self.bin_image.data_ptr() if collect_bin_image else None
+        # multi-GPU: export the pass's deposits instead of splatting them
+        # (multigpu.DepositExchange); needs capacity P * max_depth
+        self.deposit_sink = deposit_sink
+        if deposit_sink is not None:
+            deposit_sink.bind(pc, self.P * int(cfg.max_depth))
         self.svo_abi = svo.abi() if svo is not None else None
         nbytes = _lib.load().wfpg_render_workspace_bytes(
             C.byref(scene.abi()), C.byref(self.svo_abi) if svo is not None else None,

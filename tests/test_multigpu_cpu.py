@@ -94,3 +94,54 @@ def test_summed_deposits_equal_single_rank_deposits(world):
         np.add.at(wacc, leaf[p][s], 1.0)
     assert np.array_equal(wacc, wfull)
     np.testing.assert_allclose(acc, full, rtol=1e-13)
+
+
+def _gather_worker(rank, world, port, sizes, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(200 + rank)
+    n = sizes[rank]
+    leaf = torch.from_numpy(rng.integers(-1, 1000, n).astype(np.int32))
+    dirs = torch.from_numpy(rng.random((n, 3)))
+    rad = torch.from_numpy(rng.random((n, 3)))
+    g = multigpu.DepositExchange.gather(leaf, dirs, rad)
+    out[rank] = tuple(t.numpy().copy() for t in g)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("sizes", [(5, 3), (0, 4), (7, 0), (0, 0)])
+def test_deposit_gather_is_rank_ordered_concatenation(sizes):
+    """DepositExchange.gather returns every rank's list in rank order (= global
+    path order for contiguous bands), bit-exact, whatever the lengths."""
+    world = len(sizes)
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_gather_worker, args=(world, port, sizes, out), nprocs=world, join=True)
+        res = [out[r] for r in range(world)]
+    exp = []
+    for r, n in enumerate(sizes):
+        rng = np.random.default_rng(200 + r)
+        exp.append((rng.integers(-1, 1000, n).astype(np.int32), rng.random((n, 3)),
+                    rng.random((n, 3))))
+    for k in range(3):
+        want = np.concatenate([e[k] for e in exp])
+        for r in range(world):
+            assert np.array_equal(res[r][k], want)
+    assert res[0][0].dtype == np.int32
+
+
+def test_rank_ordered_deposits_reproduce_the_single_rank_splat():
+    """np.add.at over the rank-ordered concatenation IS the single-rank splat
+    (same order, same arithmetic) — bitwise, unlike summed partial sums."""
+    rng = np.random.default_rng(9)
+    n_leaves, m = 40, 3000
+    leaf = rng.integers(0, n_leaves, m)
+    rad = rng.random((m, 3)) * 1e3
+    full = np.zeros((n_leaves, 3))
+    np.add.at(full, leaf, rad)
+    parts = np.array_split(np.arange(m), 3)
+    cat = np.concatenate(parts)
+    acc = np.zeros((n_leaves, 3))
+    np.add.at(acc, leaf[cat], rad[cat])
+    assert np.array_equal(acc.view(np.uint64), full.view(np.uint64))
