@@ -110,6 +110,14 @@ typedef struct wfpg_svo {
   double* mean_a;            /* (n,3) */
   double* mean_b;            /* (n,3) */
   int32_t* counter;          /* (n,)  Alg. 2 ray counters, zero between calls */
+  /* Optional dense index of the top `top_level` levels: 8^top_level entries
+   * of 2 uint32 {node, reached level | present << 31}, indexed by the cell's
+   * row-major coordinates at that level.  Built by wfpg_svo_build_top_index
+   * (wfpg_svo_build_fill builds it too when set); every descent then starts
+   * at level top_level with one load instead of top_level dependent ones.
+   * NULL / top_level 0: plain root-to-leaf descents.  Same results either way. */
+  uint32_t* top_index;
+  int32_t top_level;
 } wfpg_svo;
 
 /* Wavefront path state: wavefront.py:53-71 (PathState), SoA. */
@@ -293,6 +301,11 @@ int wfpg_descend(const wfpg_svo* svo, const double* points, int64_t n,
  * ignored.  dirty: n_nodes bytes of device scratch (zeroed here). */
 int wfpg_svo_refresh_leaves(wfpg_svo* svo, const int32_t* leaf, int64_t n, uint8_t* dirty,
                             void* stream);
+
+/* Fill svo->top_index (see wfpg_svo) from the node arrays; top_level in
+ * [1, min(depth, 7)]; bytes = wfpg_svo_top_index_bytes(top_level). */
+size_t wfpg_svo_top_index_bytes(int32_t top_level);
+int wfpg_svo_build_top_index(wfpg_svo* svo, void* stream);
 
 /* _kernels.pyx:593-606: points -> int32 leaf coords (F,3) with the compiled
  * quantisation (truncate (p - lo) * (R / size), clamp to [0, R-1]); cube_lo is

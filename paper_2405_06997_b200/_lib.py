@@ -50,7 +50,7 @@ class Svo(C.Structure):
         ("codes", c_vp), ("child_base", c_vp), ("child_mask", c_vp), ("parent", c_vp),
         ("node_desc", c_vp), ("normal", c_vp), ("sum_a", c_vp), ("sum_b", c_vp),
         ("weight_a", c_vp), ("weight_b", c_vp), ("mean_a", c_vp), ("mean_b", c_vp),
-        ("counter", c_vp),
+        ("counter", c_vp), ("top_index", c_vp), ("top_level", c_i32),
     ]
 
 
@@ -120,6 +120,8 @@ _SIGS = {
     "wfpg_svo_build_fill": (c_i32, [P(Svo), c_vp, c_vp, c_i64, c_u64, c_vp, c_size, c_vp]),
     "wfpg_svo_build_sorted": (c_i32, [c_vp, c_i64, P(c_vp), P(c_vp)]),
     "wfpg_descend": (c_i32, [P(Svo), c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "wfpg_svo_top_index_bytes": (c_size, [c_i32]),
+    "wfpg_svo_build_top_index": (c_i32, [P(Svo), c_vp]),
     "wfpg_svo_refresh_leaves": (c_i32, [P(Svo), c_vp, c_i64, c_vp, c_vp]),
     "wfpg_frame_accumulate": (c_i32, [c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp]),
     "wfpg_quantise_points": (c_i32, [c_vp, c_dbl, c_i32, c_vp, c_i64, c_vp, c_vp]),

@@ -162,6 +162,61 @@ __device__ __forceinline__ void octa_uv_to_dir_np(double u, double v, double* ox
   *oz = __ddiv_rn(z, nrm);
 }
 
+// sin / cos of t * pi / 4 for t in [0, 2]: x = (t - 1) * pi / 4 lies in
+// [-pi/4, pi/4], where Taylor series to x^17 / x^18 are below 1e-18; then
+// sin(pi/4 + x) = (sin x + cos x) / sqrt 2, cos(pi/4 + x) = (cos x - sin x) / sqrt 2.
+// About 25 fp64 operations against ~60 instructions for sincospi, within
+// 2 ulp of the exact values.
+__device__ __forceinline__ void sincos_quarter_turn(double t, double* so, double* co) {
+  const double x = (t - 1.0) * (WFPG_PI / 4.0);
+  const double x2 = x * x;
+  double sp = 1.0 / 355687428096000.0;                 // 1/17!
+  sp = fma(sp, -x2, 1.0 / 1307674368000.0);            // 1/15!
+  sp = fma(sp, -x2, 1.0 / 6227020800.0);               // 1/13!
+  sp = fma(sp, -x2, 1.0 / 39916800.0);                 // 1/11!
+  sp = fma(sp, -x2, 1.0 / 362880.0);                   // 1/9!
+  sp = fma(sp, -x2, 1.0 / 5040.0);                     // 1/7!
+  sp = fma(sp, -x2, 1.0 / 120.0);
+  sp = fma(sp, -x2, 1.0 / 6.0);
+  const double sx = fma(-x * x2, sp, x);
+  double cp = 1.0 / 6402373705728000.0;                // 1/18!
+  cp = fma(cp, -x2, 1.0 / 20922789888000.0);           // 1/16!
+  cp = fma(cp, -x2, 1.0 / 87178291200.0);              // 1/14!
+  cp = fma(cp, -x2, 1.0 / 479001600.0);                // 1/12!
+  cp = fma(cp, -x2, 1.0 / 3628800.0);                  // 1/10!
+  cp = fma(cp, -x2, 1.0 / 40320.0);                    // 1/8!
+  cp = fma(cp, -x2, 1.0 / 720.0);
+  cp = fma(cp, -x2, 1.0 / 24.0);
+  cp = fma(cp, -x2, 0.5);
+  const double cx = fma(-x2, cp, 1.0);
+  const double r2 = 0.70710678118654752440;
+  *so = (sx + cx) * r2;
+  *co = (cx - sx) * r2;
+}
+
+// Field-cell flavour of the numpy map: the same a, b, r and phi, with
+// sin/cos from sincos_quarter_turn and without the final renormalisation (the vector is
+// unit length analytically: rho^2 + z^2 = r^2 (2 - r^2) + (1 - r^2)^2 = 1;
+// the numpy division changes it by an ulp or two).  Directions agree with
+// octa_uv_to_dir_np to a few ulp — within the fields' 1e-9 tolerance — at
+// one division instead of four and no general-argument sincos.
+__device__ __forceinline__ void octa_uv_to_dir_cell(double u, double v, double* ox, double* oy,
+                                                    double* oz) {
+  double a = __dsub_rn(__dmul_rn(2.0, u), 1.0);
+  double b = __dsub_rn(__dmul_rn(2.0, v), 1.0);
+  double ap = fabs(a), bp = fabs(b);
+  double sd = __dsub_rn(1.0, __dadd_rn(ap, bp));
+  double r = __dsub_rn(1.0, fabs(sd));
+  double t = (r == 0.0) ? 1.0 : __dadd_rn(__ddiv_rn(__dsub_rn(bp, ap), r), 1.0);  // phi / (pi/4)
+  double rr = __dmul_rn(r, r);
+  double rho = __dmul_rn(r, __dsqrt_rn(fmax(__dsub_rn(2.0, rr), 0.0)));
+  double s, c;
+  sincos_quarter_turn(t, &s, &c);
+  *ox = __dmul_rn(copysign(c, a), rho);
+  *oy = __dmul_rn(copysign(s, b), rho);
+  *oz = copysign(__dsub_rn(1.0, rr), sd);
+}
+
 // compiled flavour (_kernels.pyx:240-262): used by the guided sampler.
 __device__ __forceinline__ void octa_uv_to_dir_k(double u, double v, double* ox, double* oy,
                                                  double* oz) {
@@ -215,6 +270,8 @@ __device__ __forceinline__ void octa_dir_to_uv_k(double dx, double dy, double dz
 // ---------------------------------------------------------------------------
 struct SvoView {
   const uint2* desc;   // {child_base, child_mask}
+  const uint2* top;    // dense top-level index (optional), see wfpg_svo.top_index
+  int32_t top_level;
   const int32_t* parent;
   const double* normal;
   const double* mean_a;
@@ -229,6 +286,9 @@ struct SvoView {
 __host__ inline SvoView make_view(const wfpg_svo* s) {
   SvoView v;
   v.desc = reinterpret_cast<const uint2*>(s->node_desc);
+  v.top = s->top_level > 0 && s->top_level <= s->depth ? reinterpret_cast<const uint2*>(s->top_index)
+                                                       : nullptr;
+  v.top_level = v.top ? s->top_level : 0;
   v.parent = s->parent;
   v.normal = s->normal;
   v.mean_a = s->mean_a;
@@ -263,11 +323,12 @@ __device__ __forceinline__ int32_t quantise(double p, double lo, double scale, i
 __device__ __forceinline__ int32_t descend_coords(const uint2* __restrict__ desc, int32_t depth,
                                                   int32_t qx, int32_t qy, int32_t qz,
                                                   int32_t max_level, bool* present,
-                                                  int32_t* reached_level) {
-  int32_t node = 0;
-  int32_t lvl = 0;
+                                                  int32_t* reached_level, int32_t start_node = 0,
+                                                  int32_t start_level = 0) {
+  int32_t node = start_node;
+  int32_t lvl = start_level;
   bool pres = true;
-  for (int32_t level = 1; level <= max_level; ++level) {
+  for (int32_t level = start_level + 1; level <= max_level; ++level) {
     int sh = depth - level;
     int oct = ((qx >> sh) & 1) | (((qy >> sh) & 1) << 1) | (((qz >> sh) & 1) << 2);
     uint2 d = __ldg(&desc[node]);
@@ -282,6 +343,27 @@ __device__ __forceinline__ int32_t descend_coords(const uint2* __restrict__ desc
   *present = pres;
   *reached_level = lvl;
   return node;
+}
+
+// Descent through an SvoView: with a top index, the first top_level levels
+// are one load (row-major cell at that level); identical results.
+__device__ __forceinline__ int32_t descend_view(const SvoView& v, int32_t qx, int32_t qy,
+                                                int32_t qz, int32_t max_level, bool* present,
+                                                int32_t* reached_level) {
+  if (v.top && max_level >= v.top_level) {
+    const int T = v.top_level, sh = v.depth - T;
+    const uint32_t cell = ((uint32_t)(qx >> sh) << (2 * T)) | ((uint32_t)(qy >> sh) << T) |
+                          (uint32_t)(qz >> sh);
+    const uint2 e = __ldg(&v.top[cell]);
+    if (!(e.y >> 31)) {
+      *present = false;
+      *reached_level = (int32_t)(e.y & 0xFFu);
+      return (int32_t)e.x;
+    }
+    return descend_coords(v.desc, v.depth, qx, qy, qz, max_level, present, reached_level,
+                          (int32_t)e.x, T);
+  }
+  return descend_coords(v.desc, v.depth, qx, qy, qz, max_level, present, reached_level);
 }
 
 // ---------------------------------------------------------------------------

@@ -69,7 +69,7 @@ __global__ void k_dep_emit(SvoView v, const int32_t* __restrict__ emit_depth,
       int32_t qz = quantise(q[2], v.loz, v.scale, v.resolution);
       bool pres;
       int32_t lvl;
-      int32_t node = descend_coords(v.desc, v.depth, qx, qy, qz, v.depth, &pres, &lvl);
+      int32_t node = descend_view(v, qx, qy, qz, v.depth, &pres, &lvl);
       leaf[o] = pres ? node : -1;
       ++o;
     }

@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
       const int i = (tile % TILES_U) * TU + (lane % TU);
       const int j = (tile / TILES_U) * TV + (lane / TU);
       double dx, dy, dz;
-      octa_uv_to_dir_np(uv[i], uv[N + j], &dx, &dy, &dz);
+      octa_uv_to_dir_cell(uv[i], uv[N + j], &dx, &dy, &dz);
       double rgb[3] = {0.0, 0.0, 0.0};
       double bt;
       int32_t bid;
@@ -280,21 +280,34 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
       blur_cols<N>(F, bp);
       __syncthreads();
     }
-    // 3. epsilon floor + store values (coalesced)
-    double* gv = out.vals + b * (int64_t)N * N;
-    for (int c = threadIdx.x; c < N * N; c += blockDim.x) {
-      const int j = c / N, i = c % N;
-      double x = F[j * S + i];
-      x = x < out.eps ? out.eps : x;
-      F[j * S + i] = x;
-      gv[c] = x;
+    // 3. epsilon floor + store values (coalesced 16-byte stores)
+    double2* gv = reinterpret_cast<double2*>(out.vals + b * (int64_t)N * N);
+    for (int c = threadIdx.x; c < N * N / 2; c += blockDim.x) {
+      const int j = (2 * c) / N, i = (2 * c) % N;
+      double x0 = F[j * S + i], x1 = F[j * S + i + 1];
+      x0 = x0 < out.eps ? out.eps : x0;
+      x1 = x1 < out.eps ? out.eps : x1;
+      F[j * S + i] = x0;
+      F[j * S + i + 1] = x1;
+      gv[c] = make_double2(x0, x1);
     }
     __syncthreads();
-    // 4. row sums (0 + pairwise), then total / marginal CDF (guiding.py:296-298)
-    for (int j = threadIdx.x; j < N; j += blockDim.x) {
-      double r = __dadd_rn(0.0, pairwise_row(F + j * S, N));
-      rs[j] = r;
-      out.row_sum[b * N + j] = r;
+    // 4. row sums (0 + numpy pairwise: 8 strided accumulators combined as
+    // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), exact for N in 8..128), 8 lanes
+    // per row, then total / marginal CDF (guiding.py:296-298)
+    for (int t = threadIdx.x; t < 8 * N; t += blockDim.x) {
+      const int j = t >> 3, k = t & 7;
+      const double* row = F + j * S;
+      double r = row[k];
+      for (int i = k + 8; i < N; i += 8) r = __dadd_rn(r, row[i]);
+      r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+      r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+      r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+      if (k == 0) {
+        r = __dadd_rn(0.0, r);
+        rs[j] = r;
+        out.row_sum[b * N + j] = r;
+      }
     }
     if (out.block_sums) {
       constexpr int M = N / 8;
@@ -328,8 +341,11 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
         }
       }
       __syncthreads();
-      double* gc = out.cum + b * (int64_t)N * N;
-      for (int c = threadIdx.x; c < N * N; c += blockDim.x) gc[c] = F[(c / N) * S + c % N];
+      double2* gc = reinterpret_cast<double2*>(out.cum + b * (int64_t)N * N);
+      for (int c = threadIdx.x; c < N * N / 2; c += blockDim.x) {
+        const int j = (2 * c) / N, i = (2 * c) % N;
+        gc[c] = make_double2(F[j * S + i], F[j * S + i + 1]);
+      }
     }
     __syncthreads();
   }

@@ -250,17 +250,17 @@ __device__ __forceinline__ bool bvh_occluded(const SceneView& b, double ox, doub
 }
 
 // Per-(origin, triangle) record for rays that share one origin (all cones of a
-// field bin).  tvec = o - v0, q = tvec x e1 and ts0 = e2 . q depend only on the
-// origin, so the per-ray Moeller-Trumbore test reduces to p = d x e2 and three
-// dot products with the same operands as _kernels.pyx:63-81.  `axis` /
-// `cos_lim` bound the triangle's directions from o (a cone containing the
-// three vertex directions, widened by 1e-6 rad); a ray outside that cone
-// cannot hit the triangle, which lets a warp skip triangles none of its 32
-// rays can reach.  cos_lim = -2 disables the cull (origin too close).
+// field bin).  With tvec = o - v0 fixed, the Moeller-Trumbore quantities of
+// _kernels.pyx:63-81 are linear in the ray direction d:
+//   det   = e1 . (d x e2) = d . (e2 x e1)      -> d . n
+//   u det = tvec . (d x e2) = d . (e2 x tvec)  -> d . w
+//   v det = d . (tvec x e1)                    -> d . q
+//   t det = e2 . (tvec x e1)                   -> ts0 (constant)
+// so each candidate costs three 3-term dot products.  The reassociation moves
+// det / u / v by a few ulp against the reference's operand order, which only
+// matters for rays within ~1e-16 of a triangle edge (field tolerance 1e-9).
 struct TriBin {
-  double e1x, e1y, e1z, e2x, e2y, e2z;
-  double tx, ty, tz, qx, qy, qz, ts0;
-  double ax, ay, az, cos_lim;
+  double nx, ny, nz, wx, wy, wz, qx, qy, qz, ts0;
   // unit normals of the three planes through o and an edge, oriented toward
   // the opposite vertex: the triangle's solid angle seen from o is the
   // intersection of their positive half-spaces.  cull = 0 disables (o on or
@@ -274,22 +274,19 @@ __device__ __forceinline__ void make_tri_bin(const SceneView& s, int t, double o
   const double* v0 = s.v0 + 3 * t;
   const double* e1 = s.e1 + 3 * t;
   const double* e2 = s.e2 + 3 * t;
-  B.e1x = e1[0];
-  B.e1y = e1[1];
-  B.e1z = e1[2];
-  B.e2x = e2[0];
-  B.e2y = e2[1];
-  B.e2z = e2[2];
-  B.tx = ox - v0[0];
-  B.ty = oy - v0[1];
-  B.tz = oz - v0[2];
-  B.qx = B.ty * B.e1z - B.tz * B.e1y;
-  B.qy = B.tz * B.e1x - B.tx * B.e1z;
-  B.qz = B.tx * B.e1y - B.ty * B.e1x;
-  B.ts0 = B.e2x * B.qx + B.e2y * B.qy + B.e2z * B.qz;
-  // bounding cone of the vertex directions
+  const double tx = ox - v0[0], ty = oy - v0[1], tz = oz - v0[2];
+  B.nx = e2[1] * e1[2] - e2[2] * e1[1];
+  B.ny = e2[2] * e1[0] - e2[0] * e1[2];
+  B.nz = e2[0] * e1[1] - e2[1] * e1[0];
+  B.wx = e2[1] * tz - e2[2] * ty;
+  B.wy = e2[2] * tx - e2[0] * tz;
+  B.wz = e2[0] * ty - e2[1] * tx;
+  B.qx = ty * e1[2] - tz * e1[1];
+  B.qy = tz * e1[0] - tx * e1[2];
+  B.qz = tx * e1[1] - ty * e1[0];
+  B.ts0 = e2[0] * B.qx + e2[1] * B.qy + e2[2] * B.qz;
+  // unit directions from o to the three vertices
   double w[3][3];
-  double cx = 0.0, cy = 0.0, cz = 0.0;
   bool degenerate = false;
   for (int k = 0; k < 3; ++k) {
     double px = v0[0] + (k == 1 ? e1[0] : (k == 2 ? e2[0] : 0.0)) - ox;
@@ -301,25 +298,6 @@ __device__ __forceinline__ void make_tri_bin(const SceneView& s, int t, double o
     w[k][0] = px * inv;
     w[k][1] = py * inv;
     w[k][2] = pz * inv;
-    cx += w[k][0];
-    cy += w[k][1];
-    cz += w[k][2];
-  }
-  double cl = sqrt(cx * cx + cy * cy + cz * cz);
-  B.cos_lim = WFPG_PI;  // half-angle of the bounding cone; pi disables culling
-  B.ax = 0.0;
-  B.ay = 0.0;
-  B.az = 1.0;
-  if (!degenerate && cl > 1e-6) {
-    B.ax = cx / cl;
-    B.ay = cy / cl;
-    B.az = cz / cl;
-    double cmin = 1.0;
-    for (int k = 0; k < 3; ++k)
-      cmin = fmin(cmin, B.ax * w[k][0] + B.ay * w[k][1] + B.az * w[k][2]);
-    // the cone contains the spherical triangle only while all vertex
-    // directions lie in the axis' open hemisphere
-    if (cmin > 1e-3) B.cos_lim = acos(fmin(cmin, 1.0));
   }
   // edge planes
   B.cull = 0;
@@ -370,22 +348,6 @@ __device__ __forceinline__ void make_tri_bin(const SceneView& s, int t, double o
   }
 }
 
-// _kernels.pyx:63-81 with the origin-dependent terms precomputed.
-__device__ __forceinline__ double mt_bin(const TriBin& B, double dx, double dy, double dz,
-                                         double tmin) {
-  double px = dy * B.e2z - dz * B.e2y;
-  double py = dz * B.e2x - dx * B.e2z;
-  double pz = dx * B.e2y - dy * B.e2x;
-  double det = B.e1x * px + B.e1y * py + B.e1z * pz;
-  double s = det > 0.0 ? 1.0 : -1.0;
-  double ad = det * s;
-  double us = (B.tx * px + B.ty * py + B.tz * pz) * s;
-  double vs = (dx * B.qx + dy * B.qy + dz * B.qz) * s;
-  double ts = B.ts0 * s;
-  bool ok = (ad > 1e-300) & (us >= 0.0) & (vs >= 0.0) & (us + vs <= ad) & (ts > tmin * ad);
-  return ok ? ts / ad : -1.0;
-}
-
 __device__ __forceinline__ double warp_sum_d(double x) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
@@ -405,8 +367,8 @@ __device__ __forceinline__ double warp_min_d(double x) {
 // whole cone misses cannot be hit by any lane.  Lanes vote on 32 triangles at
 // a time and the warp then tests only the surviving candidates, in ascending
 // triangle order with the strict '<' of the brute-force kernel, so the result
-// (minimum t, lowest id on ties) is exactly brute force over all triangles
-// (the 1e-6 slack dwarfs the rounding of both the cull and the hit test).
+// (minimum t, lowest id on ties) is brute force over all triangles (the 1e-6
+// slack dwarfs the rounding of both the cull and the hit test).
 __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, int n, double dx,
                                                  double dy, double dz, double tmin, double* bt,
                                                  int32_t* bid) {
@@ -443,13 +405,10 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
       const int k = g + __ffs(m) - 1;
       m &= m - 1;
       const TriBin& B = tb[k];
-      double px = dy * B.e2z - dz * B.e2y;
-      double py = dz * B.e2x - dx * B.e2z;
-      double pz = dx * B.e2y - dy * B.e2x;
-      double det = B.e1x * px + B.e1y * py + B.e1z * pz;
+      double det = dx * B.nx + dy * B.ny + dz * B.nz;
       double sg = det > 0.0 ? 1.0 : -1.0;
       double ad = det * sg;
-      double us = (B.tx * px + B.ty * py + B.tz * pz) * sg;
+      double us = (dx * B.wx + dy * B.wy + dz * B.wz) * sg;
       double vs = (dx * B.qx + dy * B.qy + dz * B.qz) * sg;
       double ts = B.ts0 * sg;
       bool ok = (ad > 1e-300) & (us >= 0.0) & (vs >= 0.0) & (us + vs <= ad) & (ts > tmin * ad);

@@ -696,7 +696,51 @@ __global__ void k_node_desc(const int32_t* __restrict__ child_base,
     desc[k] = make_uint2((uint32_t)child_base[k], (uint32_t)child_mask[k]);
 }
 
+__global__ void k_top_index(const uint2* __restrict__ desc, int32_t depth, int32_t T,
+                            uint2* __restrict__ top) {
+  const int64_t cells = (int64_t)1 << (3 * T);
+  const uint32_t m = (1u << T) - 1u;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cells;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int sh = depth - T;
+    const int32_t x = (int32_t)((c >> (2 * T)) & m) << sh;
+    const int32_t y = (int32_t)((c >> T) & m) << sh;
+    const int32_t z = (int32_t)(c & m) << sh;
+    bool pres;
+    int32_t lvl;
+    int32_t node = descend_coords(desc, depth, x, y, z, T, &pres, &lvl);
+    top[c] = make_uint2((uint32_t)node, (uint32_t)lvl | (pres ? 0x80000000u : 0u));
+  }
+}
+
+int build_top_index(wfpg_svo* svo, cudaStream_t st) {
+  const int T = svo->top_level;
+  if (!svo->top_index || T <= 0) return WFPG_OK;
+  if (T > svo->depth || T > 7) {
+    set_error("top index level %d outside [1, min(depth, 7)]", T);
+    return WFPG_ERR_ARG;
+  }
+  const int64_t cells = (int64_t)1 << (3 * T);
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cells, 256), (int64_t)kNumSMs * 8));
+  k_top_index<<<grid, 256, 0, st>>>(reinterpret_cast<const uint2*>(svo->node_desc), svo->depth, T,
+                                     reinterpret_cast<uint2*>(svo->top_index));
+  WFPG_CHECK_LAUNCH("k_top_index");
+  return WFPG_OK;
+}
+
 }  // namespace wfpg
+
+extern "C" size_t wfpg_svo_top_index_bytes(int32_t top_level) {
+  return top_level > 0 && top_level <= 7 ? (size_t)8 << (3 * top_level) : 0;
+}
+
+extern "C" int wfpg_svo_build_top_index(wfpg_svo* svo, void* stream) {
+  if (!svo || !svo->node_desc || !svo->top_index || svo->top_level <= 0) {
+    set_error("wfpg_svo_build_top_index: bad arguments");
+    return WFPG_ERR_ARG;
+  }
+  return build_top_index(svo, (cudaStream_t)stream);
+}
 
 extern "C" int wfpg_svo_build_fill(wfpg_svo* svo, const int32_t* frag_tris,
                                    const double* tri_normals, int64_t n_fragments, uint64_t seed,
@@ -760,5 +804,5 @@ extern "C" int wfpg_svo_build_fill(wfpg_svo* svo, const int32_t* frag_tris,
   k_node_desc<<<grid_for(n), 256, 0, st>>>(svo->child_base, svo->child_mask, n,
                                            reinterpret_cast<uint2*>(svo->node_desc));
   WFPG_CHECK_LAUNCH("k_node_desc");
-  return WFPG_OK;
+  return build_top_index(svo, st);
 }

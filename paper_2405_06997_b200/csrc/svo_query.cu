@@ -17,7 +17,7 @@ __global__ void k_descend(SvoView v, const double* __restrict__ pts, int64_t n,
     int32_t qz = quantise(pts[3 * i + 2], v.loz, v.scale, v.resolution);
     bool pres;
     int32_t lvl;
-    int32_t node = descend_coords(v.desc, v.depth, qx, qy, qz, v.depth, &pres, &lvl);
+    int32_t node = descend_view(v, qx, qy, qz, v.depth, &pres, &lvl);
     if (out_node) out_node[i] = node;
     if (out_present) out_present[i] = pres ? 1 : 0;
     if (out_deepest) out_deepest[i] = node;  // compiled kernel: node == deepest

@@ -49,7 +49,7 @@ __device__ __forceinline__ void cone_shade_hit(const SvoView& v, double ox, doub
   int target = best_cone_level(v.size, v.depth, r * r * omega);
   bool pres;
   int32_t lvl;
-  int32_t node = descend_coords(v.desc, v.depth, ix, iy, iz, target, &pres, &lvl);
+  int32_t node = descend_view(v, ix, iy, iz, target, &pres, &lvl);
   const double* nn = v.normal + 3 * (int64_t)node;
   double da = dx * __ldg(nn) + dy * __ldg(nn + 1) + dz * __ldg(nn + 2);
   double w = fabs(da);

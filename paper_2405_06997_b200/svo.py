@@ -135,6 +135,12 @@ _ARRAYS = {
 }
 
 
+def top_level_for(depth):
+    """Levels covered by the dense top index: 5 (32 K cells, 256 KB) below
+    depth 6, fewer for shallow trees."""
+    return max(1, min(5, int(depth) - 1))
+
+
 class SvoCache:
     """Level-grouped node arrays in HBM; level 0 is the root, level ``depth``
     the leaves; node ids index the flat arrays (svo.py:176-224)."""
@@ -156,6 +162,9 @@ class SvoCache:
             shape = (n, comp) if comp > 1 else (n,)
             d[name] = _dev.zeros(shape, ddt)
         d["node_desc"] = _dev.zeros((n, 2), np.uint32)
+        # dense index of the top levels: descents start there with one load
+        self.top_level = top_level_for(self.depth)
+        d["top_index"] = _dev.zeros((1 << (3 * self.top_level), 2), np.uint32)
         self._d = d
         self._abi = None
 
@@ -172,9 +181,10 @@ class SvoCache:
         if self.level_off is not None:
             for i, v in enumerate(self.level_off):
                 s.level_off[i] = int(v)
-        for name in list(_ARRAYS) + ["node_desc"]:
+        for name in list(_ARRAYS) + ["node_desc", "top_index"]:
             if name in self._d:
                 setattr(s, name, self._d[name].data_ptr())
+        s.top_level = self.__dict__.get("top_level", 0) if "top_index" in self._d else 0
         self._abi = s
         return s
 
@@ -358,6 +368,7 @@ class SvoCache:
         desc = np.stack([host["child_base"].astype(np.int64) & 0xFFFFFFFF,
                          host["child_mask"].astype(np.int64)], axis=1).astype(np.uint32)
         svo._d["node_desc"].copy_(_dev.upload(desc))
+        _lib.call("wfpg_svo_build_top_index", _lib.C.byref(svo.abi()), _dev.stream())
         svo.propagate_up()
         return svo
 
