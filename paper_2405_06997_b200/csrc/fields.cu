@@ -25,6 +25,14 @@ __device__ __forceinline__ int fold_index(int raw, int n, bool* flip) {
   return raw;
 }
 
+// one reflection suffices when the blur radius is below n (the fixed-radius
+// kernels): branch-free form of fold_index
+__device__ __forceinline__ int fold_once(int raw, int n, bool* flip) {
+  const bool lo = raw < 0, hi = raw >= n;
+  *flip = lo | hi;
+  return lo ? -1 - raw : (hi ? 2 * n - 1 - raw : raw);
+}
+
 template <int N>
 struct FieldCfg {
   static constexpr int kStride = N + 1;  // padded rows: conflict-free column walks
@@ -122,6 +130,7 @@ __device__ void blur_cols(double* F, const BlurParams& bp) {
 // edge take the fold path.  Same taps, same order, same rounding.
 template <int N, int R>
 __device__ void blur_rows_r(double* F, const BlurParams& bp) {
+  static_assert(R < N, "fold_once needs the radius below the grid size");
   constexpr int S = FieldCfg<N>::kStride;
   constexpr int PL = FieldCfg<N>::kPerLane;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -147,7 +156,7 @@ __device__ void blur_rows_r(double* F, const BlurParams& bp) {
 #pragma unroll
         for (int k = 0; k <= 2 * R; ++k) {
           bool f;
-          const int c = fold_index(i + k - R, N, &f);
+          const int c = fold_once(i + k - R, N, &f);
           a = __dadd_rn(a, __dmul_rn(w[k], f ? B[c] : A[c]));
           b = __dadd_rn(b, __dmul_rn(w[k], f ? A[c] : B[c]));
         }
@@ -170,6 +179,7 @@ __device__ void blur_rows_r(double* F, const BlurParams& bp) {
 
 template <int N, int R>
 __device__ void blur_cols_r(double* F, const BlurParams& bp) {
+  static_assert(R < N, "fold_once needs the radius below the grid size");
   constexpr int S = FieldCfg<N>::kStride;
   constexpr int PL = FieldCfg<N>::kPerLane;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -194,7 +204,7 @@ __device__ void blur_cols_r(double* F, const BlurParams& bp) {
 #pragma unroll
         for (int k = 0; k <= 2 * R; ++k) {
           bool f;
-          const int rr = fold_index(j + k - R, N, &f);
+          const int rr = fold_once(j + k - R, N, &f);
           const double* row = F + rr * S;
           a = __dadd_rn(a, __dmul_rn(w[k], f ? row[ip] : row[i]));
           b = __dadd_rn(b, __dmul_rn(w[k], f ? row[i] : row[ip]));

@@ -265,7 +265,8 @@ struct TriBin {
   // the opposite vertex: the triangle's solid angle seen from o is the
   // intersection of their positive half-spaces.  cull = 0 disables (o on or
   // near the triangle's plane / an edge line).
-  double n0x, n0y, n0z, n1x, n1y, n1z, n2x, n2y, n2z;
+  // (fp32: the cull carries a 1e-5 slack, far above their rounding)
+  float n0x, n0y, n0z, n1x, n1y, n1z, n2x, n2y, n2z;
   int cull;
 };
 
@@ -334,15 +335,15 @@ __device__ __forceinline__ void make_tri_bin(const SceneView& s, int t, double o
       nrm[e][2] = nz;
     }
     if (ok) {
-      B.n0x = nrm[0][0];
-      B.n0y = nrm[0][1];
-      B.n0z = nrm[0][2];
-      B.n1x = nrm[1][0];
-      B.n1y = nrm[1][1];
-      B.n1z = nrm[1][2];
-      B.n2x = nrm[2][0];
-      B.n2y = nrm[2][1];
-      B.n2z = nrm[2][2];
+      B.n0x = (float)nrm[0][0];
+      B.n0y = (float)nrm[0][1];
+      B.n0z = (float)nrm[0][2];
+      B.n1x = (float)nrm[1][0];
+      B.n1y = (float)nrm[1][1];
+      B.n1z = (float)nrm[1][2];
+      B.n2x = (float)nrm[2][0];
+      B.n2y = (float)nrm[2][1];
+      B.n2z = (float)nrm[2][2];
       B.cull = 1;
     }
   }
@@ -374,8 +375,9 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
                                                  int32_t* bid) {
   const int lane = threadIdx.x & 31;
   // axis: the centre lane's direction, broadcast as floats (any common axis is
-  // valid).  The tile bound is evaluated in fp32 and widened by 4e-6 (cos)
-  // and 1e-5 (sin) — far above fp32 rounding — so it stays conservative.
+  // valid).  The tile bound and the plane tests are evaluated in fp32 and
+  // widened by 4e-6 (cos) and 1e-5 (sin) — far above fp32 rounding (~1e-7)
+  // — so the cull stays conservative.
   const float fax = __shfl_sync(0xffffffffu, (float)dx, 12);
   const float fay = __shfl_sync(0xffffffffu, (float)dy, 12);
   const float faz = __shfl_sync(0xffffffffu, (float)dz, 12);
@@ -384,10 +386,9 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cm = fminf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
   const bool cull = cm > 0.0f;
-  const double ax = fax, ay = fay, az = faz;
   // -|a| (sin(th) + slack): a ray within th of the axis cannot reach the
   // inner side of a plane whose normal n has a.n below this
-  const double reach = -(double)((sqrtf(fmaxf(1.0f - cm * cm, 0.0f)) + 1e-5f) * fal);
+  const float reach = -(sqrtf(fmaxf(1.0f - cm * cm, 0.0f)) + 1e-5f) * fal;
   double best = 1e300;
   int32_t id = -1;
   for (int g = 0; g < n; g += 32) {
@@ -396,9 +397,9 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
     if (cand && cull) {
       const TriBin& B = tb[t];
       if (B.cull)
-        cand = (ax * B.n0x + ay * B.n0y + az * B.n0z >= reach) &&
-               (ax * B.n1x + ay * B.n1y + az * B.n1z >= reach) &&
-               (ax * B.n2x + ay * B.n2y + az * B.n2z >= reach);
+        cand = (fax * B.n0x + fay * B.n0y + faz * B.n0z >= reach) &&
+               (fax * B.n1x + fay * B.n1y + faz * B.n1z >= reach) &&
+               (fax * B.n2x + fay * B.n2y + faz * B.n2z >= reach);
     }
     unsigned m = __ballot_sync(0xffffffffu, cand);
     while (m) {

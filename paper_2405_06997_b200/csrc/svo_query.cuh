@@ -43,9 +43,11 @@ __device__ __forceinline__ void cone_shade_hit(const SvoView& v, double ox, doub
   qx = fmin(fmax(qx, v.clo[0]), v.chi[0]);
   qy = fmin(fmax(qy, v.clo[1]), v.chi[1]);
   qz = fmin(fmax(qz, v.clo[2]), v.chi[2]);
-  int32_t ix = quantise(qx, v.lox, v.scale, v.resolution);
-  int32_t iy = quantise(qy, v.loy, v.scale, v.resolution);
-  int32_t iz = quantise(qz, v.loz, v.scale, v.resolution);
+  // q is clamped into [lo + tiny, lo + size - tiny], so (q - lo) * scale lies
+  // in (0, R): the compiled (long) truncation is a plain round-toward-zero
+  int32_t ix = min(__double2int_rz(__dmul_rn(__dsub_rn(qx, v.lox), v.scale)), v.resolution - 1);
+  int32_t iy = min(__double2int_rz(__dmul_rn(__dsub_rn(qy, v.loy), v.scale)), v.resolution - 1);
+  int32_t iz = min(__double2int_rz(__dmul_rn(__dsub_rn(qz, v.loz), v.scale)), v.resolution - 1);
   int target = best_cone_level(v.size, v.depth, r * r * omega);
   bool pres;
   int32_t lvl;
