@@ -32,6 +32,32 @@ __device__ __forceinline__ int upper_bound_d(const double* cdf, int n, double u)
   return lo > n - 1 ? n - 1 : lo;
 }
 
+// Number of leading elements of the non-decreasing row a[0..n) that satisfy
+// `a[i] <= x` (strict = false) or `a[i] < x` (strict = true) — the
+// upper_bound / lower_bound index — in two dependent rounds of independent
+// loads instead of log2(n) dependent ones: 8 probes at the ends of n/8
+// blocks, then the block that holds the boundary (16-byte loads).  n must be
+// a multiple of 8 and a 16-byte aligned.  Same index as the binary search.
+template <bool strict>
+__device__ __forceinline__ int count_leading(const double* __restrict__ a, int n, double x) {
+  const int B = n >> 3;
+  int k = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const double v = __ldg(a + j * B + B - 1);
+    k += strict ? (v < x) : (v <= x);
+  }
+  if (k == 8 || B == 1) return k * B;
+  const double2* blk = reinterpret_cast<const double2*>(a + k * B);
+  int c = 0;
+#pragma unroll 4
+  for (int i = 0; i < (B >> 1); ++i) {
+    const double2 v = __ldg(blk + i);
+    c += strict ? (v.x < x) + (v.y < x) : (v.x <= x) + (v.y <= x);
+  }
+  return k * B + c;
+}
+
 __device__ __forceinline__ double residual(double u, double lo, double hi) {
   double span = hi - lo;
   double f = span > 0.0 ? (u - lo) / span : 0.0;
@@ -43,6 +69,15 @@ __device__ __forceinline__ double residual(double u, double lo, double hi) {
 // invert_cdf over a stored CDF (_kernels.pyx:815-827)
 __device__ __forceinline__ int invert_cdf(const double* cdf, int n, double u, double* frac) {
   int i = upper_bound_d(cdf, n, u);
+  double lo = i > 0 ? cdf[i - 1] : 0.0;
+  *frac = residual(u, lo, cdf[i]);
+  return i;
+}
+
+// invert_cdf over a guide-table row in global memory (n a multiple of 8)
+__device__ __forceinline__ int invert_cdf_row(const double* cdf, int n, double u, double* frac) {
+  int i = count_leading<false>(cdf, n, u);
+  i = i > n - 1 ? n - 1 : i;
   double lo = i > 0 ? cdf[i - 1] : 0.0;
   *frac = residual(u, lo, cdf[i]);
   return i;
@@ -75,14 +110,7 @@ __device__ __forceinline__ int invert_cumsum(const double* v, int stride, int n,
 __device__ __forceinline__ int invert_prefix(const double* cum, int n, double denom, double u,
                                              double* frac) {
   const double thr = u * denom * (1.0 - 1e-12);
-  int lo = 0, hi = n;  // first index with cum >= thr
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (cum[mid] < thr)
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
+  const int lo = count_leading<true>(cum, n, thr);  // first index with cum >= thr
   int i = lo < n ? lo : n - 1;
   double cur = __ddiv_rn(cum[i], denom);
   while (!(cur > u) && i < n - 1) {
@@ -152,7 +180,7 @@ __device__ __forceinline__ void sample_plain(const GuideView& g, int slot, doubl
                                              double* wx, double* wy, double* wz) {
   const int n = g.n;
   double fv, fu;
-  int gj = invert_cdf(g.marg + (int64_t)slot * n, n, s1, &fv);
+  int gj = invert_cdf_row(g.marg + (int64_t)slot * n, n, s1, &fv);
   const double denom = g.row_sum[(int64_t)slot * n + gj];
   int gi = g.cum ? invert_prefix(g.cum + ((int64_t)slot * n + gj) * n, n, denom, s2, &fu)
                  : invert_cumsum(g.vals + ((int64_t)slot * n + gj) * n, 1, n, denom, s2, &fu);

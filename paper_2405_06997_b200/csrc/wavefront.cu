@@ -334,7 +334,7 @@ __device__ void shade_path(int64_t p, int depth, const SceneView& sa, const Guid
   P.ctr[p] = c;
 }
 
-__global__ void __launch_bounds__(256) k_shade(SceneView s, GuideView g, PathsView P, int depth,
+__global__ void __launch_bounds__(256, 3) k_shade(SceneView s, GuideView g, PathsView P, int depth,
                                                const int32_t* __restrict__ active, int64_t n_max,
                                                const int32_t* __restrict__ n_dev,
                                                const double* __restrict__ hit_t,
