@@ -119,41 +119,36 @@ __global__ void __launch_bounds__(kSortBlock) k_sort_hist(const uint64_t* __rest
     if (i < n) atomicAdd(&cnt[(keys[i] >> shift) & 255u], 1u);
   }
   __syncthreads();
-  if (base < n) hist[(int64_t)blockIdx.x * 256 + threadIdx.x] = cnt[threadIdx.x];  // block-major
+  // digit-major (stride = worst-case tile count): each digit's tile counts
+  // are contiguous for the per-digit scan
+  if (base < n) hist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = cnt[threadIdx.x];
 }
 
-// Digit offsets for the active tiles only (ceil(n / tile) of them, n from the
-// device): 4 threads per digit split the tiles, exclusive prefix over tiles
-// per digit, then the exclusive prefix of the digit totals.  Replaces a full
-// scan of 256 x (worst-case tiles) entries.
-constexpr int kOffThreads = 1024;
+// Digit offsets: one block per digit scans that digit's counts over the
+// active tiles (ceil(n / tile), n from the device) in place and writes the
+// digit total; the scatter blocks turn the 256 totals into digit bases.
+constexpr int kOffThreads = 256;
 __global__ void __launch_bounds__(kOffThreads) k_sort_offsets(uint32_t* __restrict__ hist,
                                                               int64_t n_max,
                                                               const int32_t* __restrict__ n_dev,
-                                                              uint32_t* __restrict__ dbase) {
-  __shared__ uint32_t seg_tot[4][256];
+                                                              int64_t nblocks,
+                                                              uint32_t* __restrict__ dtot) {
   __shared__ uint32_t sw[kOffThreads / 32 + 1];
   const int64_t n = dev_count(n_max, n_dev);
   const int64_t nb = (n + kSortTile - 1) / kSortTile;
-  const int d = threadIdx.x & 255, sgi = threadIdx.x >> 8;
-  const int64_t per = (nb + 3) / 4, b0 = sgi * per, b1 = b0 + per < nb ? b0 + per : nb;
+  uint32_t* h = hist + (int64_t)blockIdx.x * nblocks;
+  const int64_t per = (nb + kOffThreads - 1) / kOffThreads;
+  const int64_t b0 = (int64_t)threadIdx.x * per, b1 = b0 + per < nb ? b0 + per : nb;
   uint32_t s = 0;
-#pragma unroll 8
-  for (int64_t b = b0; b < b1; ++b) s += hist[b * 256 + d];
-  seg_tot[sgi][d] = s;
-  __syncthreads();
-  uint32_t run = 0;
-  for (int g = 0; g < sgi; ++g) run += seg_tot[g][d];
-  uint32_t total = seg_tot[0][d] + seg_tot[1][d] + seg_tot[2][d] + seg_tot[3][d];
-#pragma unroll 8
+  for (int64_t b = b0; b < b1; ++b) s += h[b];
+  uint32_t total;
+  uint32_t run = block_exclusive_scan<kOffThreads>(s, sw, &total);
   for (int64_t b = b0; b < b1; ++b) {
-    uint32_t h = hist[b * 256 + d];
-    hist[b * 256 + d] = run;
-    run += h;
+    const uint32_t c = h[b];
+    h[b] = run;
+    run += c;
   }
-  // exclusive prefix of the digit totals (threads 0..255 carry them)
-  uint32_t ex = block_exclusive_scan<kOffThreads>(sgi == 0 ? total : 0u, sw, nullptr);
-  if (sgi == 0) dbase[d] = ex;
+  if (threadIdx.x == 0) dtot[blockIdx.x] = total;
 }
 
 __global__ void __launch_bounds__(kSortBlock) k_sort_scatter(
@@ -162,11 +157,14 @@ __global__ void __launch_bounds__(kSortBlock) k_sort_scatter(
     int64_t nblocks, const uint32_t* __restrict__ offs, const uint32_t* __restrict__ dbase) {
   __shared__ uint32_t whist[kSortWarps][256];
   __shared__ uint32_t goff[256];
+  __shared__ uint32_t sw[kSortBlock / 32 + 1];
   const int64_t n = dev_count(n_max, n_dev);
   if ((int64_t)blockIdx.x * kSortTile >= n) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < kSortWarps * 256; i += kSortBlock) (&whist[0][0])[i] = 0;
-  goff[threadIdx.x] = dbase[threadIdx.x] + offs[(int64_t)blockIdx.x * 256 + threadIdx.x];
+  // digit base = exclusive prefix of the digit totals (thread t = digit t)
+  const uint32_t base_t = block_exclusive_scan<kSortBlock>(dbase[threadIdx.x], sw, nullptr);
+  goff[threadIdx.x] = base_t + offs[(int64_t)threadIdx.x * nblocks + blockIdx.x];
   __syncthreads();
 
   const int64_t wbase = (int64_t)blockIdx.x * kSortTile + (int64_t)warp * 32 * kSortIpt;
@@ -250,7 +248,7 @@ int sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n_max, const int32_t* n_d
     int shift = 8 * p;
     k_sort_hist<<<(unsigned)nb, kSortBlock, 0, st>>>(ka, n_max, n_dev, shift, nb, hist);
     WFPG_CHECK_LAUNCH("k_sort_hist");
-    k_sort_offsets<<<1, kOffThreads, 0, st>>>(hist, n_max, n_dev, dbase);
+    k_sort_offsets<<<256, kOffThreads, 0, st>>>(hist, n_max, n_dev, nb, dbase);
     WFPG_CHECK_LAUNCH("k_sort_offsets");
     k_sort_scatter<<<(unsigned)nb, kSortBlock, 0, st>>>(ka, va, kb, vb, n_max, n_dev, shift, nb,
                                                          hist, dbase);
