@@ -244,7 +244,8 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
   const int64_t nb = dev_count(nb_max, nb_dev);
   const double omega = 4.0 * WFPG_PI / (double)(N * N);  // guiding.py:246
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+  __shared__ int64_t next_bin;
+  for (int64_t b = blockIdx.x; b < nb;) {
     const double ox = origins[3 * b], oy = origins[3 * b + 1], oz = origins[3 * b + 2];
     // u = i/n + ju/n, v = j/n + jv/n (guiding.py:239-244), once per bin
     for (int k = threadIdx.x; k < 2 * N; k += blockDim.x) {
@@ -357,7 +358,13 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
         gc[c] = make_double2(F[j * S + i], F[j * S + i + 1]);
       }
     }
+    if (out.bin_ctr) {
+      if (threadIdx.x == 0) next_bin = (int64_t)atomicAdd(out.bin_ctr, 1) + gridDim.x;
+    } else if (threadIdx.x == 0) {
+      next_bin = b + gridDim.x;
+    }
     __syncthreads();
+    b = next_bin;
   }
 }
 

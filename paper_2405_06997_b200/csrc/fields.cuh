@@ -16,6 +16,9 @@ struct FieldOut {
   double* block_sums;  // NULL unless product mode
   double eps;
   double* cum = nullptr;  // optional (B,n,n) row prefix sums
+  // optional zeroed device counter: bins after each CTA's first are handed
+  // out dynamically (bin costs vary; static striding left SMs idle at the end)
+  int32_t* bin_ctr = nullptr;
 };
 
 int launch_fields(const SceneView& s, const SvoView& v, const double* origins,

@@ -187,6 +187,7 @@ struct PassLayout {
   double* tot;
   double* block_sums;
   double* cum;
+  int32_t* bin_ctr;  // dynamic bin scheduling of the field kernels
   uint8_t* dirty;
   double* upper_dirs;
   StatsDev* stats;
@@ -238,6 +239,7 @@ static void carve_pass(Arena& a, const wfpg_svo* svo, const wfpg_camera* cam,
       L.tot = a.take<double>(L.cap);
       L.block_sums = cfg->product ? a.take<double>(L.cap * 64) : nullptr;
       L.cum = a.take<double>(L.cap * (int64_t)L.n0 * L.n0);
+      L.bin_ctr = a.take<int32_t>(4);
     }
   }
   L.scratch_off = a.off;
@@ -377,7 +379,8 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
       if (guided_depth) {
         const int n = std::max(8, cfg->field_res >> (depth - 1));
         FieldOut fo{L.vals, L.row_sum, L.marg, L.tot, cfg->product ? L.block_sums : nullptr,
-                    cfg->epsilon, L.cum};
+                    cfg->epsilon, L.cum, L.bin_ctr};
+        WFPG_CUDA(cudaMemsetAsync(L.bin_ctr, 0, sizeof(int32_t), st));
         if (prof) {
           k_stamp_begin<<<1, 1, 0, st>>>(prof, depth);
           WFPG_CHECK_LAUNCH("k_stamp_begin");
