@@ -331,8 +331,13 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
     k_scatter_alive<<<grid, 256, 0, st>>>(L.flags, L.scan, P, L.active, L.total, L.n_active,
                                           &L.stats->live[depth]);
     WFPG_CHECK_LAUNCH("k_scatter_alive");
-    WFPG_TRY(launch_intersect(sv, paths->ray_o, paths->ray_d, L.active, P, L.n_active,
-                              scene->ray_eps, L.hit_t, L.hit_tri, false, st));
+    if (depth == 1 && sv.brute) {  // primary rays share the camera position
+      WFPG_TRY(launch_intersect_origin(sv, cam->position, paths->ray_d, L.active, P, L.n_active,
+                                       scene->ray_eps, L.hit_t, L.hit_tri, st));
+    } else {
+      WFPG_TRY(launch_intersect(sv, paths->ray_o, paths->ray_d, L.active, P, L.n_active,
+                                scene->ray_eps, L.hit_t, L.hit_tri, false, st));
+    }
 
     GuideView gv{};
     gv.mode = 0;

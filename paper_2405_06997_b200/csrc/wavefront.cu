@@ -349,6 +349,49 @@ __global__ void __launch_bounds__(256, 3) k_shade(SceneView s, GuideView g, Path
   }
 }
 
+// Nearest hit of rays that all start at one point (the pinhole camera's
+// primary rays): the per-(origin, triangle) records are built once per block
+// and each warp culls triangles against the bounding cone of its 32 rays
+// (warp_nearest_bin, the field kernel's tracer).  Consecutive pixels share a
+// warp, so most triangles are rejected without a ray test.  Small scenes only
+// (records in shared memory).
+__global__ void __launch_bounds__(256) k_intersect_origin(SceneView s, double ox, double oy,
+                                                          double oz,
+                                                          const double* __restrict__ dirs,
+                                                          const int32_t* __restrict__ active,
+                                                          int64_t n_max,
+                                                          const int32_t* __restrict__ n_dev,
+                                                          double tmin, double* __restrict__ out_t,
+                                                          int32_t* __restrict__ out_tri) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TriBin* tb = reinterpret_cast<TriBin*>(smem_raw);
+  for (int t = threadIdx.x; t < s.n_tris; t += blockDim.x) make_tri_bin(s, t, ox, oy, oz, tb[t]);
+  __syncthreads();
+  const int64_t n = dev_count(n_max, n_dev);
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = (int64_t)gridDim.x * blockDim.x;
+  // whole warps iterate together (warp_nearest_bin shuffles over all lanes);
+  // lanes past the end borrow lane 0's ray and write nothing
+  for (int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) - lane; w0 < n;
+       w0 += wstride) {
+    const int64_t i = w0 + lane;
+    const bool valid = i < n;
+    const int64_t r = valid ? (active ? active[i] : i) : 0;
+    double dx = valid ? dirs[3 * r] : 0.0, dy = valid ? dirs[3 * r + 1] : 0.0,
+           dz = valid ? dirs[3 * r + 2] : 0.0;
+    dx = __shfl_sync(0xffffffffu, dx, valid ? lane : 0);
+    dy = __shfl_sync(0xffffffffu, dy, valid ? lane : 0);
+    dz = __shfl_sync(0xffffffffu, dz, valid ? lane : 0);
+    double bt;
+    int32_t id;
+    warp_nearest_bin(tb, s.n_tris, dx, dy, dz, tmin, &bt, &id);
+    if (valid) {
+      out_t[r] = bt;
+      out_tri[r] = id;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // internal launchers
 // ---------------------------------------------------------------------------
@@ -373,6 +416,21 @@ int launch_intersect(const SceneView& s, const double* orig, const double* dirs,
   k_intersect<<<grid, 256, smem, st>>>(s, orig, dirs, active, n_max, n_dev, tmin, out_t, out_tri,
                                        inf_on_miss ? 1 : 0);
   WFPG_CHECK_LAUNCH("k_intersect");
+  return WFPG_OK;
+}
+
+int launch_intersect_origin(const SceneView& s, const double* origin, const double* dirs,
+                            const int32_t* active, int64_t n_max, const int32_t* n_dev,
+                            double tmin, double* out_t, int32_t* out_tri, cudaStream_t st) {
+  if (n_max <= 0) return WFPG_OK;
+  if (!s.brute)
+    return launch_intersect(s, nullptr, dirs, active, n_max, n_dev, tmin, out_t, out_tri, false,
+                            st);
+  size_t smem = sizeof(TriBin) * s.n_tris;
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_max, 256), kNumSMs * 8));
+  k_intersect_origin<<<grid, 256, smem, st>>>(s, origin[0], origin[1], origin[2], dirs, active,
+                                              n_max, n_dev, tmin, out_t, out_tri);
+  WFPG_CHECK_LAUNCH("k_intersect_origin");
   return WFPG_OK;
 }
 

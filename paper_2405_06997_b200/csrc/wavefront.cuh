@@ -17,6 +17,12 @@ GuideView make_guide_view(const wfpg_guide* g);
 int launch_camera_init(const CameraView& c, const PathsView& P, int64_t n_paths, int64_t n_pix,
                        int64_t n_img, int64_t pix0, const int64_t* sample0, uint64_t seed,
                        cudaStream_t st);
+// primary rays from one origin (host pointer to 3 doubles); brute-force scenes
+// use the warp-culled tracer, others fall back to launch_intersect (which
+// then needs per-ray origins: only call it with brute scenes)
+int launch_intersect_origin(const SceneView& s, const double* origin, const double* dirs,
+                            const int32_t* active, int64_t n_max, const int32_t* n_dev,
+                            double tmin, double* out_t, int32_t* out_tri, cudaStream_t st);
 int launch_intersect(const SceneView& s, const double* orig, const double* dirs,
                      const int32_t* active, int64_t n_max, const int32_t* n_dev, double tmin,
                      double* out_t, int32_t* out_tri, bool inf_on_miss, cudaStream_t st);
