@@ -37,10 +37,12 @@ template <int N>
 struct FieldCfg {
   static constexpr int kStride = N + 1;  // padded rows: conflict-free column walks
   // one warp per 8x4-cell tile at most: N=8 has 2 tiles, N=16 8, N=32 32.
+  // Smaller CTAs for N <= 64 (measured: 256 / 128 / 64 threads beat 512 /
+  // 256 / 128 and 128 / 64 / 32) keep more bins in flight per SM.
   // kThreads * kMinBlocks = 1024 -> a 64-register budget and 32+ warps per SM;
   // several CTAs (bins) per SM overlap one bin's barrier phases with
   // another's cone tracing
-  static constexpr int kThreads = N >= 128 ? 1024 : (N == 64 ? 512 : (N == 32 ? 256 : (N == 16 ? 128 : 64)));
+  static constexpr int kThreads = N >= 128 ? 1024 : (N == 64 ? 256 : (N == 32 ? 128 : 64));
   static constexpr int kMinBlocks = 1024 / kThreads;
   static constexpr int kPerLane = (N + 31) / 32;
 };
