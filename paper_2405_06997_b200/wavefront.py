@@ -288,6 +288,66 @@ def render_pass(scene, svo, cfg, sample_indices, collect_bin_image=False, out=No
     return frame, r.pass_stats()
 
 
+class FramePipeline:
+    """Consecutive single-sample passes whose frames arrive in page-locked host
+    memory, with the device-to-host copy of pass i overlapped with pass i+1.
+
+    Two PassRunners alternate (two frame buffers, two path states), the copy
+    runs on its own stream after an event recorded at the end of each pass,
+    and a runner only writes its frame again once that frame's previous copy
+    has finished.  Passes still run back to back on the caller's stream, so
+    the SVO learning sequence is exactly that of calling render_pass once per
+    sample.  ``run(samples)`` yields (sample_index, frame, stats) with the
+    frame an (H, W, 3) view of a pinned buffer that stays valid until the
+    iterator advances twice more; stats are collected only if want_stats.
+    """
+
+    def __init__(self, scene, svo, cfg, want_stats=False):
+        t = _dev.torch()
+        if svo is not None:
+            cfg.validate(svo.depth)
+        self.scene, self.svo, self.cfg = scene, svo, cfg
+        self.want_stats = want_stats
+        self.runners = [PassRunner(scene, svo, cfg) for _ in range(2)]
+        self.host = [pinned_frame(scene) for _ in range(2)]
+        self.copy_stream = t.cuda.Stream()
+        self.pass_done = [t.cuda.Event() for _ in range(2)]
+        self.copy_done = [t.cuda.Event() for _ in range(2)]
+        self.copied = [False, False]
+
+    def _submit(self, k, sample):
+        t = _dev.torch()
+        cur = t.cuda.current_stream()
+        slot = k % 2
+        r = self.runners[slot]
+        if self.copied[slot]:  # frame buffer of this runner still being read?
+            cur.wait_event(self.copy_done[slot])
+        r.launch(int(sample), want_stats=self.want_stats)
+        self.pass_done[slot].record(cur)
+        self.copy_stream.wait_event(self.pass_done[slot])
+        with t.cuda.stream(self.copy_stream):
+            dst = t.from_numpy(self.host[slot]).view(-1, 3)
+            dst.copy_(r.frame, non_blocking=True)
+        self.copy_done[slot].record(self.copy_stream)
+        self.copied[slot] = True
+        return slot
+
+    def _deliver(self, slot, sample):
+        self.copy_done[slot].synchronize()
+        stats = self.runners[slot].pass_stats() if self.want_stats else None
+        return int(sample), self.host[slot], stats
+
+    def run(self, sample_indices):
+        pending = None
+        for k, s in enumerate(sample_indices):
+            slot = self._submit(k, s)
+            if pending is not None:
+                yield self._deliver(*pending)
+            pending = (slot, s)
+        if pending is not None:
+            yield self._deliver(*pending)
+
+
 def render_sample(scene, svo, cfg, sample_index):
     frame, _ = render_pass(scene, svo, cfg, [sample_index])
     return frame

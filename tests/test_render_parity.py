@@ -235,3 +235,25 @@ def test_graph_replay_matches_eager(R, setup):
         assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
     assert np.array_equal(ma_e.view(np.uint64), ma_g.view(np.uint64))
     assert np.array_equal(sb_e.view(np.uint64), sb_g.view(np.uint64))
+
+
+def test_frame_pipeline_matches_render_pass(R, setup):
+    """FramePipeline (two alternating runners, overlapped frame copies) gives
+    the same frames and the same SVO learning sequence as render_pass."""
+    from paper_2405_06997_b200 import wavefront
+
+    sc, tree, c = setup
+    cfg = wavefront.GuidingConfig(max_depth=c["max_depth"], guided_depths=c["max_depth"],
+                                  field_res=c["field_res"], l_min=c["l_min"], c_ray=c["c_ray"],
+                                  seed=c["seed"])
+    _set_svo_state(tree, R, "p0")
+    ref = [wavefront.render_pass(sc, tree, cfg, [s])[0].copy() for s in range(1, 6)]
+    ref_mean = tree.mean_a
+    _set_svo_state(tree, R, "p0")
+    pipe = wavefront.FramePipeline(sc, tree, cfg, want_stats=True)
+    got = [(s, f.copy(), st) for s, f, st in pipe.run(range(1, 6))]
+    assert [s for s, _, _ in got] == [1, 2, 3, 4, 5]
+    for (_, f, st), r in zip(got, ref):
+        assert np.array_equal(f.view(np.uint64), r.view(np.uint64))
+        assert st.bins_per_depth
+    assert np.array_equal(tree.mean_a.view(np.uint64), ref_mean.view(np.uint64))
