@@ -19,26 +19,41 @@ __global__ void k_part_count(SvoView v, int32_t* __restrict__ counter,
                              const int32_t* __restrict__ n_dev, int l_min,
                              int32_t* __restrict__ start, int8_t* __restrict__ start_lev) {
   const int64_t n = dev_count(n_max, n_dev);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t qx = quantise(pos[3 * i], v.lox, v.scale, v.resolution);
-    int32_t qy = quantise(pos[3 * i + 1], v.loy, v.scale, v.resolution);
-    int32_t qz = quantise(pos[3 * i + 2], v.loz, v.scale, v.resolution);
+  const int lane = threadIdx.x & 31;
+  // whole warps iterate together so the counter updates can be aggregated:
+  // neighbouring paths (pixel order) share most of their ancestors, and one
+  // atomic per distinct node and warp replaces up to 32 contended ones
+  for (int64_t w0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; w0 < n;
+       w0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = w0 + lane;
+    const bool valid = i < n;
     int32_t node = 0, lvl = 0;
     int32_t chain[22];
     chain[0] = 0;
-    for (int level = 1; level <= v.depth; ++level) {
-      int sh = v.depth - level;
-      int oct = ((qx >> sh) & 1) | (((qy >> sh) & 1) << 1) | (((qz >> sh) & 1) << 2);
-      uint2 d = __ldg(&v.desc[node]);
-      if (!((d.y >> oct) & 1u)) break;
-      node = (int32_t)d.x + __popc(d.y & ((1u << oct) - 1u));
-      lvl = level;
-      chain[level] = node;
+    if (valid) {
+      int32_t qx = quantise(pos[3 * i], v.lox, v.scale, v.resolution);
+      int32_t qy = quantise(pos[3 * i + 1], v.loy, v.scale, v.resolution);
+      int32_t qz = quantise(pos[3 * i + 2], v.loz, v.scale, v.resolution);
+      for (int level = 1; level <= v.depth; ++level) {
+        int sh = v.depth - level;
+        int oct = ((qx >> sh) & 1) | (((qy >> sh) & 1) << 1) | (((qz >> sh) & 1) << 2);
+        uint2 d = __ldg(&v.desc[node]);
+        if (!((d.y >> oct) & 1u)) break;
+        node = (int32_t)d.x + __popc(d.y & ((1u << oct) - 1u));
+        lvl = level;
+        chain[level] = node;
+      }
+      start[i] = node;
+      start_lev[i] = (int8_t)lvl;
     }
-    start[i] = node;
-    start_lev[i] = (int8_t)lvl;
-    for (int l = lvl; l > l_min; --l) atomicAdd(&counter[chain[l]], 1);
+    int top = valid ? lvl : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) top = max(top, __shfl_xor_sync(0xffffffffu, top, o));
+    for (int l = top; l > l_min; --l) {
+      const int32_t a = (valid && l <= lvl) ? chain[l] : -1;
+      const unsigned grp = __match_any_sync(0xffffffffu, a);
+      if (a >= 0 && lane == __ffs(grp) - 1) atomicAdd(&counter[a], __popc(grp));
+    }
   }
 }
 
