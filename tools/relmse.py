@@ -3,15 +3,15 @@
 B200 (BASELINE metric "relMSE at equal time").
 
 1. Reference: --ref-spp samples of unguided path tracing (independent seed).
-2. Guided (pt-first, Eq. 7 "pt-first" heuristic, the CLI's default) and
-   unguided PT, each accumulated on the device through cli.render's loop;
-   at every power-of-two spp the running image is resolved and compared with
-   the reference (relMSE = mean((x - r)^2 / (r^2 + 1e-2)), plus the
-   tone-mapped MSE of accumulation.mse).  Device time (CUDA events, resolves
-   excluded) is accumulated per curve; the guided time includes its SVO
-   build.
-3. Equal time: PT keeps rendering until it has used the guided run's total
-   time; the relMSE of both at that time is the headline pair.
+2. Costs: steady-state device time of one guided pass and one unguided pass
+   (CUDA-graph replay, CUDA events, after eager + capture warm-up) and of the
+   SVO build.
+3. Guided (pt-first, Eq. 7 "pt-first" heuristic, the CLI's default) and
+   unguided PT, each accumulated on the device; at every power-of-two spp
+   the running image is compared with the reference (relMSE = mean((x - r)^2
+   / (r^2 + 1e-2)), plus the tone-mapped MSE of accumulation.mse).
+4. Equal time: PT renders as many samples as cost the guided run's time
+   (build + spp x guided pass); the relMSE of both is the headline pair.
 
 Prints one JSON line per scene (and appends it to --out).
 
@@ -32,14 +32,9 @@ sys.path.insert(0, REPO)
 SCENES = {"c2": ("cornell.scene", 1024), "c3": ("c3_two_rooms.scene", 2048)}
 
 
-def curve(scene, svo, conf, max_spp, checkpoints, ref, time_budget_ms=None, extra_ms=0.0):
-    """Accumulate passes; returns [(spp, device ms, relMSE, mse)] at checkpoints
-    (and at the time budget when given)."""
-    import torch
+def _runners(scene, svo, conf):
+    from paper_2405_06997_b200 import cli, wavefront
 
-    from paper_2405_06997_b200 import accumulation as A, cli, wavefront
-
-    cam = scene.camera
     guided = conf.guided_depths if conf.mode != "pt" else 0
     pt_first = conf.heuristic == "pt-first" and conf.mode != "pt"
     runners = {}
@@ -52,35 +47,43 @@ def curve(scene, svo, conf, max_spp, checkpoints, ref, time_budget_ms=None, extr
             runners[g] = wavefront.PassRunner(scene, svo, c, 1)
         return runners[g]
 
+    return lambda i: runner(0 if (pt_first and i == 1) else guided)
+
+
+def pass_ms(scene, svo, conf, reps=10):
+    """Steady-state device time of one pass (graph replay), CUDA events."""
+    import torch
+
+    get = _runners(scene, svo, conf)
+    r = get(2)  # a guided pass (or the PT pass in pt mode)
+    for k in range(3):  # eager, capture, replay
+        r.launch(k + 2, want_stats=False)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for k in range(reps):
+        r.launch(k + 5, want_stats=False)
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def curve(scene, svo, conf, max_spp, checkpoints, ref):
+    """Accumulate passes 1..max_spp; [(spp, relMSE, mse)] at the checkpoints
+    and at max_spp (the accumulated frame when ref is None)."""
+    from paper_2405_06997_b200 import accumulation as A
+
+    cam = scene.camera
+    get = _runners(scene, svo, conf)
     buf = A.AccumulationBuffer(cam.height, cam.width, conf.heuristic)
     out = []
-    ms = extra_ms
-    cur = torch.cuda.current_stream()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(cur)
-    i = 0
-    while True:
-        i += 1
-        g = 0 if (pt_first and i == 1) else guided
-        r = runner(g)
+    for i in range(1, max_spp + 1):
+        r = get(i)
         r.launch(i - 1, want_stats=False)
         buf.add_sample(r.frame, i)
-        at_cp = i in checkpoints
-        over = time_budget_ms is not None and i % 8 == 0
-        if at_cp or over or i == max_spp:
-            e1.record(cur)
-            torch.cuda.synchronize()
-            ms += e0.elapsed_time(e1)
-            if at_cp or i == max_spp or (time_budget_ms is not None and ms >= time_budget_ms):
-                if ref is None:
-                    out.append((i, ms, None, None))
-                else:
-                    f = buf.resolve()
-                    out.append((i, ms, A.rel_mse(f, ref), A.mse(f, ref)))
-            if i >= max_spp or (time_budget_ms is not None and ms >= time_budget_ms):
-                break
-            e0.record(cur)
+        if ref is not None and (i in checkpoints or i == max_spp):
+            f = buf.resolve()
+            out.append((i, A.rel_mse(f, ref), A.mse(f, ref)))
     return out, buf
 
 
@@ -95,12 +98,17 @@ def main():
     ap.add_argument("--ref-spp", type=int, default=16384)
     ap.add_argument("--mode", default="wfpg", choices=["wfpg", "wfpg-product"])
     ap.add_argument("--out", default=None)
-    ap.add_argument("--save-ref", default=None, help="write the reference frame (PFM)")
+    ap.add_argument("--save-ref", default=None, help="write the reference frame (.npy)")
+    ap.add_argument("--ref-file", default=None,
+                    help="reuse a reference frame written by --save-ref (same scene/size/depth)")
+    ap.add_argument("--guided-depths", type=int, default=4)
+    ap.add_argument("--field-res", type=int, default=128)
+    ap.add_argument("--skip-pt", action="store_true", help="guided curve only")
     args = ap.parse_args()
 
     import torch
 
-    from paper_2405_06997_b200 import cli, imageio, scene as S, svo as svo_mod
+    from paper_2405_06997_b200 import cli, scene as S, svo as svo_mod
 
     name, res = SCENES[args.scene]
     res = args.svo_res or res
@@ -110,41 +118,56 @@ def main():
     path = os.path.join(REPO, "scenes", name)
     t0 = time.perf_counter()
     # reference: unguided, independent seed, only the final image
-    ref_conf = cli.RunConfig(path, mode="pt", spp=args.ref_spp, depth=args.depth, seed=1_000_003)
-    ref_pts, ref_buf = curve(sc, None, ref_conf, args.ref_spp, set(), None)
-    ref_ms = ref_pts[-1][1]
-    ref = ref_buf.resolve()
-    del ref_buf
-    if args.save_ref:
-        imageio.write_pfm(args.save_ref, ref)
+    if args.ref_file and os.path.exists(args.ref_file):
+        ref = np.load(args.ref_file)
+    else:
+        ref_conf = cli.RunConfig(path, mode="pt", spp=args.ref_spp, depth=args.depth,
+                                 seed=1_000_003)
+        _, ref_buf = curve(sc, None, ref_conf, args.ref_spp, set(), None)
+        ref = ref_buf.resolve()
+        del ref_buf
+        if args.save_ref:
+            np.save(args.save_ref, ref)
     cps = {1 << k for k in range(0, 20)}
-    # guided (SVO build timed with events and charged to the guided curve)
     g_conf = cli.RunConfig(path, mode=args.mode, spp=args.spp, depth=args.depth, svo_res=res,
-                           seed=7)
+                           seed=7, guided_depths=min(args.guided_depths, args.depth),
+                           field_res=args.field_res)
+    p_conf = cli.RunConfig(path, mode="pt", spp=1 << 30, depth=args.depth, seed=7)
+    # steady-state costs: SVO build, guided pass (on a scratch SVO), PT pass
     cur = torch.cuda.current_stream()
     b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    svo_mod.build_from_scene(sc, res, seed=g_conf.seed)  # warm-up
     b0.record(cur)
-    tree = svo_mod.build_from_scene(sc, res, seed=g_conf.seed)
+    scratch = svo_mod.build_from_scene(sc, res, seed=g_conf.seed)
     b1.record(cur)
     torch.cuda.synchronize()
     build_ms = b0.elapsed_time(b1)
-    g_pts, _ = curve(sc, tree, g_conf, args.spp, cps, ref, extra_ms=build_ms)
-    g_ms = g_pts[-1][1]
-    # unguided at equal spp, continuing to equal time
-    p_conf = cli.RunConfig(path, mode="pt", spp=1 << 30, depth=args.depth, seed=7)
-    p_pts, _ = curve(sc, None, p_conf, 1 << 30, cps, ref, time_budget_ms=g_ms)
+    g_ms = pass_ms(sc, scratch, g_conf)
+    p_ms = pass_ms(sc, None, p_conf)
+    del scratch
+    # quality: guided to spp; unguided to the spp that costs the same time
+    tree = svo_mod.build_from_scene(sc, res, seed=g_conf.seed)
+    g_pts, _ = curve(sc, tree, g_conf, args.spp, cps, ref)
+    budget = build_ms + args.spp * g_ms
+    pt_spp = max(args.spp, int(budget / p_ms))
+    p_pts = [(0, float("nan"), float("nan"))] if args.skip_pt else \
+        curve(sc, None, p_conf, pt_spp, cps | {args.spp}, ref)[0]
     eq_spp = [p for p in p_pts if p[0] == args.spp]
     line = {
         "bench": "relmse", "scene": args.scene, "image": [args.width, args.height],
         "svo_res": res, "max_depth": args.depth, "mode": args.mode,
-        "reference": {"spp": args.ref_spp, "device_ms": ref_ms, "seed": 1_000_003},
-        "svo_build_ms": build_ms,
-        "guided": [{"spp": s, "ms": m, "rel_mse": r, "mse": e} for s, m, r, e in g_pts],
-        "pt": [{"spp": s, "ms": m, "rel_mse": r, "mse": e} for s, m, r, e in p_pts],
-        "equal_spp": {"spp": args.spp, "guided_rel_mse": g_pts[-1][2],
-                      "pt_rel_mse": eq_spp[0][2] if eq_spp else None},
-        "equal_time": {"ms": g_ms, "guided_rel_mse": g_pts[-1][2], "pt_spp": p_pts[-1][0],
-                       "pt_rel_mse": p_pts[-1][2]},
+        "guided_depths": g_conf.guided_depths, "field_res": g_conf.field_res,
+        "reference": {"spp": args.ref_spp, "seed": 1_000_003, "kind": "unguided PT"},
+        "svo_build_ms": build_ms, "guided_pass_ms": g_ms, "pt_pass_ms": p_ms,
+        "guided": [{"spp": s_, "ms": build_ms + s_ * g_ms, "rel_mse": r, "mse": e}
+                   for s_, r, e in g_pts],
+        "pt": [{"spp": s_, "ms": s_ * p_ms, "rel_mse": r, "mse": e} for s_, r, e in p_pts],
+        "equal_spp": {"spp": args.spp, "guided_rel_mse": g_pts[-1][1],
+                      "pt_rel_mse": eq_spp[0][1] if eq_spp else None},
+        "equal_time": {"ms": budget, "guided_rel_mse": g_pts[-1][1], "pt_spp": p_pts[-1][0],
+                       "pt_rel_mse": p_pts[-1][1]},
+        "timing": "steady-state device pass times (CUDA-graph replay, CUDA events); "
+                  "curves rendered separately, so image resolves cost nothing",
         "wall_s": time.perf_counter() - t0,
     }
     print(json.dumps(line), flush=True)
