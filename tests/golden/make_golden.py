@@ -348,6 +348,34 @@ def gen_cli():
     save("cli_golden.npz", **out)
 
 
+# ---------------------------------------------------------------------------
+RELMSE_RUNS = dict(spp=32, depth=5, svo_res=64, field_res=32, lmin=3, cray=16)
+
+
+def gen_relmse():
+    """Equal-spp relMSE protocol of SURVEY.md 8(d) at reduced size: the
+    reference CLI renders cornell_enclosed (64x64) with 32 spp guided (wfpg,
+    pt-first) and unguided (pt) for seeds 1..3; the GPU tests render the same
+    runs and compare both against a high-spp reference."""
+    import tempfile
+
+    from wfpg import cli
+
+    tmp = tempfile.mkdtemp()
+    out = {"cfg_keys": np.array(list(RELMSE_RUNS)),
+           "cfg_vals": np.array(list(RELMSE_RUNS.values()))}
+    scene_file = os.path.join(HERE, "..", "..", "scenes", "cornell_enclosed.scene")
+    for mode in ("wfpg", "pt"):
+        for seed in (1, 2, 3):
+            conf = cli.RunConfig(scene=scene_file, mode=mode, seed=seed,
+                                 out=os.path.join(tmp, f"{mode}{seed}.pfm"), **RELMSE_RUNS)
+            status, frame = cli.run(conf, log=lambda *_: None)
+            assert status == 0
+            out[f"{mode}_{seed}"] = frame
+            print(mode, seed, frame.mean())
+    save("relmse_golden.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["svo"]
     for w in which:
