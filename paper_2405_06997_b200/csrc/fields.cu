@@ -228,6 +228,19 @@ __device__ void blur_cols_r(double* F, const BlurParams& bp) {
   }
 }
 
+#ifdef WFPG_FIELD_PHASES
+// phase profiling build: cycles between the phase boundaries of thread 0,
+// summed over bins and CTAs (phase 0 = setup, 1 trace, 2 blur, 3 floor +
+// values, 4 row sums + marginal, 5 prefix sums + stores)
+__device__ unsigned long long g_field_phase[8];
+__device__ __forceinline__ void ph_mark(int k) {
+  static __shared__ long long last;
+  long long now = clock64();
+  if (k > 0) atomicAdd(&g_field_phase[k - 1], (unsigned long long)(now - last));
+  last = now;
+}
+#endif
+
 template <int N>
 __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks)
     k_fields(SceneView s, SvoView v, const double* __restrict__ origins,
@@ -247,18 +260,29 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
   const double omega = 4.0 * WFPG_PI / (double)(N * N);  // guiding.py:246
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   __shared__ int64_t next_bin;
+  __shared__ double tot_sh;
   for (int64_t b = blockIdx.x; b < nb;) {
     const double ox = origins[3 * b], oy = origins[3 * b + 1], oz = origins[3 * b + 2];
+#ifdef WFPG_FIELD_PHASES
+    if (threadIdx.x == 0) ph_mark(0);
+#endif
     // u = i/n + ju/n, v = j/n + jv/n (guiding.py:239-244), once per bin
     for (int k = threadIdx.x; k < 2 * N; k += blockDim.x) {
       const int i = k < N ? k : k - N;
       const double jit = __ddiv_rn(jitters[2 * b + (k < N ? 0 : 1)], (double)N);
       uv[k] = __dadd_rn(__ddiv_rn((double)i, (double)N), jit);
     }
-    if (s.brute)
-      for (int t = threadIdx.x; t < s.n_tris; t += blockDim.x) make_tri_bin(s, t, ox, oy, oz, tb[t]);
+    if (s.brute) {  // three threads per triangle record (one edge plane each)
+      for (int t = threadIdx.x; t < s.n_tris; t += blockDim.x) tb[t].cull = 0;
+      __syncthreads();
+      for (int k = threadIdx.x; k < 3 * s.n_tris; k += blockDim.x)
+        make_tri_bin_part(s, k / 3, k % 3, ox, oy, oz, tb[k / 3]);
+    }
     if (threadIdx.x == 0) tile_ctr = nwarps;
     __syncthreads();
+#ifdef WFPG_FIELD_PHASES
+    if (threadIdx.x == 0) ph_mark(1);
+#endif
     // 1. cone-trace every cell; tiles are handed out dynamically (cull
     // candidates and hit depths vary per tile, static striping left warps
     // idling at the barrier)
@@ -281,6 +305,9 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
       tile = __shfl_sync(0xffffffffu, next, 0);
     }
     __syncthreads();
+#ifdef WFPG_FIELD_PHASES
+    if (threadIdx.x == 0) ph_mark(2);
+#endif
     // 2. fold-aware separable blur, horizontal then vertical (core.py:185-195)
     if (bp.radius == 3 && N > 8) {
       blur_rows_r<N, 3>(F, bp);
@@ -293,6 +320,9 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
       blur_cols<N>(F, bp);
       __syncthreads();
     }
+#ifdef WFPG_FIELD_PHASES
+    if (threadIdx.x == 0) ph_mark(3);
+#endif
     // 3. epsilon floor + store values (coalesced 16-byte stores)
     double2* gv = reinterpret_cast<double2*>(out.vals + b * (int64_t)N * N);
     for (int c = threadIdx.x; c < N * N / 2; c += blockDim.x) {
@@ -305,6 +335,9 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
       gv[c] = make_double2(x0, x1);
     }
     __syncthreads();
+#ifdef WFPG_FIELD_PHASES
+    if (threadIdx.x == 0) ph_mark(4);
+#endif
     // 4. row sums (0 + numpy pairwise: 8 strided accumulators combined as
     // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), exact for N in 8..128), 8 lanes
     // per row, then total / marginal CDF (guiding.py:296-298)
@@ -333,15 +366,23 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
       }
     }
     __syncthreads();
+    // total, then the sequential running sum (np.cumsum order) in place by one
+    // thread; the N divisions of the marginal CDF run in parallel
     if (threadIdx.x == 0) {
-      double tot = __dadd_rn(0.0, pairwise_row(rs, N));
+      const double tot = __dadd_rn(0.0, pairwise_row(rs, N));
       out.total[b] = tot;
-      double run = 0.0;
-      for (int j = 0; j < N; ++j) {
-        run = j == 0 ? rs[0] : __dadd_rn(run, rs[j]);
-        out.marg[b * N + j] = __ddiv_rn(run, tot);
+      tot_sh = tot;
+      double run = rs[0];
+      for (int j = 1; j < N; ++j) {
+        run = __dadd_rn(run, rs[j]);
+        rs[j] = run;
       }
     }
+    __syncthreads();
+    for (int j = threadIdx.x; j < N; j += blockDim.x) out.marg[b * N + j] = __ddiv_rn(rs[j], tot_sh);
+#ifdef WFPG_FIELD_PHASES
+    if (threadIdx.x == 0) ph_mark(5);
+#endif
     // 5. unnormalised row prefix sums (np.cumsum order) for the samplers:
     // cond[j, i] = cum[j, i] / row_sum[j] is then one division at the picked
     // cell instead of a division per scanned cell
@@ -360,6 +401,9 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
         gc[c] = make_double2(F[j * S + i], F[j * S + i + 1]);
       }
     }
+#ifdef WFPG_FIELD_PHASES
+    if (threadIdx.x == 0) ph_mark(6);
+#endif
     if (out.bin_ctr) {
       if (threadIdx.x == 0) next_bin = (int64_t)atomicAdd(out.bin_ctr, 1) + gridDim.x;
     } else if (threadIdx.x == 0) {
@@ -561,3 +605,15 @@ extern "C" int wfpg_guide_expand(const wfpg_guide* guide, int64_t n_bins, double
   WFPG_CHECK_LAUNCH("k_guide_expand");
   return WFPG_OK;
 }
+
+#ifdef WFPG_FIELD_PHASES
+extern "C" int wfpg_field_phases(unsigned long long* out, int reset) {
+  WFPG_CUDA(cudaDeviceSynchronize());
+  WFPG_CUDA(cudaMemcpyFromSymbol(out, wfpg::g_field_phase, sizeof(unsigned long long) * 8));
+  if (reset) {
+    unsigned long long z[8] = {0};
+    WFPG_CUDA(cudaMemcpyToSymbol(wfpg::g_field_phase, z, sizeof(z)));
+  }
+  return 0;
+}
+#endif

@@ -263,29 +263,37 @@ struct TriBin {
   double nx, ny, nz, wx, wy, wz, qx, qy, qz, ts0;
   // unit normals of the three planes through o and an edge, oriented toward
   // the opposite vertex: the triangle's solid angle seen from o is the
-  // intersection of their positive half-spaces.  cull = 0 disables (o on or
-  // near the triangle's plane / an edge line).
+  // intersection of their positive half-spaces.  cull: one bit per valid
+  // plane; culling only with all three (o on or near the triangle's plane /
+  // an edge line disables it).
   // (fp32: the cull carries a 1e-5 slack, far above their rounding)
   float n0x, n0y, n0z, n1x, n1y, n1z, n2x, n2y, n2z;
   int cull;
 };
 
-__device__ __forceinline__ void make_tri_bin(const SceneView& s, int t, double ox, double oy,
-                                             double oz, TriBin& B) {
+// One third of a triangle's record: part e computes the edge plane through o
+// and edge e (and, for e = 0, the Moeller-Trumbore terms), so three threads
+// build a record.  Edge planes that come out degenerate leave their bit of
+// `cull` clear; culling applies only when all three bits are set.  `cull`
+// must be zeroed beforehand (bits are OR-ed in from the three parts).
+__device__ __forceinline__ void make_tri_bin_part(const SceneView& s, int t, int e, double ox,
+                                                  double oy, double oz, TriBin& B) {
   const double* v0 = s.v0 + 3 * t;
   const double* e1 = s.e1 + 3 * t;
   const double* e2 = s.e2 + 3 * t;
-  const double tx = ox - v0[0], ty = oy - v0[1], tz = oz - v0[2];
-  B.nx = e2[1] * e1[2] - e2[2] * e1[1];
-  B.ny = e2[2] * e1[0] - e2[0] * e1[2];
-  B.nz = e2[0] * e1[1] - e2[1] * e1[0];
-  B.wx = e2[1] * tz - e2[2] * ty;
-  B.wy = e2[2] * tx - e2[0] * tz;
-  B.wz = e2[0] * ty - e2[1] * tx;
-  B.qx = ty * e1[2] - tz * e1[1];
-  B.qy = tz * e1[0] - tx * e1[2];
-  B.qz = tx * e1[1] - ty * e1[0];
-  B.ts0 = e2[0] * B.qx + e2[1] * B.qy + e2[2] * B.qz;
+  if (e == 0) {
+    const double tx = ox - v0[0], ty = oy - v0[1], tz = oz - v0[2];
+    B.nx = e2[1] * e1[2] - e2[2] * e1[1];
+    B.ny = e2[2] * e1[0] - e2[0] * e1[2];
+    B.nz = e2[0] * e1[1] - e2[1] * e1[0];
+    B.wx = e2[1] * tz - e2[2] * ty;
+    B.wy = e2[2] * tx - e2[0] * tz;
+    B.wz = e2[0] * ty - e2[1] * tx;
+    B.qx = ty * e1[2] - tz * e1[1];
+    B.qy = tz * e1[0] - tx * e1[2];
+    B.qz = tx * e1[1] - ty * e1[0];
+    B.ts0 = e2[0] * B.qx + e2[1] * B.qy + e2[2] * B.qz;
+  }
   // unit directions from o to the three vertices
   double w[3][3];
   bool degenerate = false;
@@ -300,53 +308,38 @@ __device__ __forceinline__ void make_tri_bin(const SceneView& s, int t, double o
     w[k][1] = py * inv;
     w[k][2] = pz * inv;
   }
-  // edge planes
-  B.cull = 0;
-  if (!degenerate) {
-    double nrm[3][3];
-    bool ok = true;
-    for (int e = 0; e < 3 && ok; ++e) {
-      const double* a = w[e];
-      const double* b = w[(e + 1) % 3];
-      const double* c = w[(e + 2) % 3];
-      double nx = a[1] * b[2] - a[2] * b[1];
-      double ny = a[2] * b[0] - a[0] * b[2];
-      double nz = a[0] * b[1] - a[1] * b[0];
-      double len = sqrt(nx * nx + ny * ny + nz * nz);
-      if (!(len > 1e-9)) {
-        ok = false;
-        break;
-      }
-      nx /= len;
-      ny /= len;
-      nz /= len;
-      double side = nx * c[0] + ny * c[1] + nz * c[2];
-      if (fabs(side) < 1e-9) {  // origin (nearly) in the triangle's plane
-        ok = false;
-        break;
-      }
-      if (side < 0.0) {
-        nx = -nx;
-        ny = -ny;
-        nz = -nz;
-      }
-      nrm[e][0] = nx;
-      nrm[e][1] = ny;
-      nrm[e][2] = nz;
-    }
-    if (ok) {
-      B.n0x = (float)nrm[0][0];
-      B.n0y = (float)nrm[0][1];
-      B.n0z = (float)nrm[0][2];
-      B.n1x = (float)nrm[1][0];
-      B.n1y = (float)nrm[1][1];
-      B.n1z = (float)nrm[1][2];
-      B.n2x = (float)nrm[2][0];
-      B.n2y = (float)nrm[2][1];
-      B.n2z = (float)nrm[2][2];
-      B.cull = 1;
-    }
+  if (degenerate) return;
+  // the plane through o and edge e, oriented toward the opposite vertex
+  const double* a = w[e];
+  const double* b = w[(e + 1) % 3];
+  const double* c = w[(e + 2) % 3];
+  double nx = a[1] * b[2] - a[2] * b[1];
+  double ny = a[2] * b[0] - a[0] * b[2];
+  double nz = a[0] * b[1] - a[1] * b[0];
+  double len = sqrt(nx * nx + ny * ny + nz * nz);
+  if (!(len > 1e-9)) return;
+  nx /= len;
+  ny /= len;
+  nz /= len;
+  double side = nx * c[0] + ny * c[1] + nz * c[2];
+  if (fabs(side) < 1e-9) return;  // origin (nearly) in the triangle's plane
+  if (side < 0.0) {
+    nx = -nx;
+    ny = -ny;
+    nz = -nz;
   }
+  float* nb = &B.n0x + 3 * e;
+  nb[0] = (float)nx;
+  nb[1] = (float)ny;
+  nb[2] = (float)nz;
+  atomicOr(&B.cull, 1 << e);
+}
+
+// Whole record by one thread.
+__device__ __forceinline__ void make_tri_bin(const SceneView& s, int t, double ox, double oy,
+                                             double oz, TriBin& B) {
+  B.cull = 0;
+  for (int e = 0; e < 3; ++e) make_tri_bin_part(s, t, e, ox, oy, oz, B);
 }
 
 __device__ __forceinline__ double warp_sum_d(double x) {
@@ -396,7 +389,7 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
     bool cand = t < n;
     if (cand && cull) {
       const TriBin& B = tb[t];
-      if (B.cull)
+      if (B.cull == 7)
         cand = (fax * B.n0x + fay * B.n0y + faz * B.n0z >= reach) &&
                (fax * B.n1x + fay * B.n1y + faz * B.n1z >= reach) &&
                (fax * B.n2x + fay * B.n2y + faz * B.n2z >= reach);
