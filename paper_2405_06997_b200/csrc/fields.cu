@@ -366,8 +366,11 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
       }
     }
     __syncthreads();
-    // total, then the sequential running sum (np.cumsum order) in place by one
-    // thread; the N divisions of the marginal CDF run in parallel
+    // total and the sequential running sum of the row sums (np.cumsum order,
+    // in place) by thread 0, while the other warps turn each row of F into
+    // its unnormalised prefix sums (np.cumsum order) for the samplers:
+    // cond[j, i] = cum[j, i] / row_sum[j] is then one division at the picked
+    // cell instead of a division per scanned cell
     if (threadIdx.x == 0) {
       const double tot = __dadd_rn(0.0, pairwise_row(rs, N));
       out.total[b] = tot;
@@ -377,24 +380,22 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
         run = __dadd_rn(run, rs[j]);
         rs[j] = run;
       }
-    }
-    __syncthreads();
-    for (int j = threadIdx.x; j < N; j += blockDim.x) out.marg[b * N + j] = __ddiv_rn(rs[j], tot_sh);
-#ifdef WFPG_FIELD_PHASES
-    if (threadIdx.x == 0) ph_mark(5);
-#endif
-    // 5. unnormalised row prefix sums (np.cumsum order) for the samplers:
-    // cond[j, i] = cum[j, i] / row_sum[j] is then one division at the picked
-    // cell instead of a division per scanned cell
-    if (out.cum) {
-      for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    } else if (out.cum && threadIdx.x >= 32) {
+      for (int j = threadIdx.x - 32; j < N; j += blockDim.x - 32) {
         double run = F[j * S];
         for (int i = 1; i < N; ++i) {
           run = __dadd_rn(run, F[j * S + i]);
           F[j * S + i] = run;
         }
       }
-      __syncthreads();
+    }
+    __syncthreads();
+#ifdef WFPG_FIELD_PHASES
+    if (threadIdx.x == 0) ph_mark(5);
+#endif
+    // 5. marginal CDF divisions and the prefix-sum table stores, in parallel
+    for (int j = threadIdx.x; j < N; j += blockDim.x) out.marg[b * N + j] = __ddiv_rn(rs[j], tot_sh);
+    if (out.cum) {
       double2* gc = reinterpret_cast<double2*>(out.cum + b * (int64_t)N * N);
       for (int c = threadIdx.x; c < N * N / 2; c += blockDim.x) {
         const int j = (2 * c) / N, i = (2 * c) % N;
