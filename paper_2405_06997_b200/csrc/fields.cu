@@ -261,23 +261,31 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   __shared__ int64_t next_bin;
   __shared__ double tot_sh;
-  for (int64_t b = blockIdx.x; b < nb;) {
+  // per-bin tables: u = i/n + ju/n, v = j/n + jv/n (guiding.py:239-244) and
+  // the triangle records for the bin's origin (three threads per triangle).
+  // The next bin's tables are built during this bin's blur (they are free
+  // once the cone tracing is done), off the critical path.
+  auto setup = [&](int64_t bb) {
+    const double sx = origins[3 * bb], sy = origins[3 * bb + 1], sz = origins[3 * bb + 2];
+    const int n_tb = s.brute ? 3 * s.n_tris : 0;
+    for (int k = threadIdx.x; k < 2 * N + n_tb; k += blockDim.x) {
+      if (k < 2 * N) {
+        const int i = k < N ? k : k - N;
+        const double jit = __ddiv_rn(jitters[2 * bb + (k < N ? 0 : 1)], (double)N);
+        uv[k] = __dadd_rn(__ddiv_rn((double)i, (double)N), jit);
+      } else {
+        const int q = k - 2 * N;
+        make_tri_bin_part(s, q / 3, q % 3, sx, sy, sz, tb[q / 3]);
+      }
+    }
+  };
+  int64_t b = blockIdx.x;
+  if (b < nb) setup(b);
+  for (; b < nb;) {
     const double ox = origins[3 * b], oy = origins[3 * b + 1], oz = origins[3 * b + 2];
 #ifdef WFPG_FIELD_PHASES
     if (threadIdx.x == 0) ph_mark(0);
 #endif
-    // u = i/n + ju/n, v = j/n + jv/n (guiding.py:239-244), once per bin
-    for (int k = threadIdx.x; k < 2 * N; k += blockDim.x) {
-      const int i = k < N ? k : k - N;
-      const double jit = __ddiv_rn(jitters[2 * b + (k < N ? 0 : 1)], (double)N);
-      uv[k] = __dadd_rn(__ddiv_rn((double)i, (double)N), jit);
-    }
-    if (s.brute) {  // three threads per triangle record (one edge plane each)
-      for (int t = threadIdx.x; t < s.n_tris; t += blockDim.x) tb[t].cull = 0;
-      __syncthreads();
-      for (int k = threadIdx.x; k < 3 * s.n_tris; k += blockDim.x)
-        make_tri_bin_part(s, k / 3, k % 3, ox, oy, oz, tb[k / 3]);
-    }
     if (threadIdx.x == 0) tile_ctr = nwarps;
     __syncthreads();
 #ifdef WFPG_FIELD_PHASES
@@ -304,7 +312,11 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
       if (lane == 0) next = atomicAdd(&tile_ctr, 1);
       tile = __shfl_sync(0xffffffffu, next, 0);
     }
+    if (threadIdx.x == 0)
+      next_bin = out.bin_ctr ? (int64_t)atomicAdd(out.bin_ctr, 1) + gridDim.x : b + gridDim.x;
     __syncthreads();
+    const int64_t b_next = next_bin;
+    if (b_next < nb) setup(b_next);  // overlaps the blur below
 #ifdef WFPG_FIELD_PHASES
     if (threadIdx.x == 0) ph_mark(2);
 #endif
@@ -405,13 +417,8 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
 #ifdef WFPG_FIELD_PHASES
     if (threadIdx.x == 0) ph_mark(6);
 #endif
-    if (out.bin_ctr) {
-      if (threadIdx.x == 0) next_bin = (int64_t)atomicAdd(out.bin_ctr, 1) + gridDim.x;
-    } else if (threadIdx.x == 0) {
-      next_bin = b + gridDim.x;
-    }
     __syncthreads();
-    b = next_bin;
+    b = b_next;
   }
 }
 

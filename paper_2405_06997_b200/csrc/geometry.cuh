@@ -263,19 +263,19 @@ struct TriBin {
   double nx, ny, nz, wx, wy, wz, qx, qy, qz, ts0;
   // unit normals of the three planes through o and an edge, oriented toward
   // the opposite vertex: the triangle's solid angle seen from o is the
-  // intersection of their positive half-spaces.  cull: one bit per valid
-  // plane; culling only with all three (o on or near the triangle's plane /
-  // an edge line disables it).
+  // intersection of their positive half-spaces.  A degenerate plane (o on
+  // or near the triangle's plane / an edge line) disables the cull.
   // (fp32: the cull carries a 1e-5 slack, far above their rounding)
   float n0x, n0y, n0z, n1x, n1y, n1z, n2x, n2y, n2z;
-  int cull;
+  // per-plane validity, one byte per part so the three builders write
+  // without atomics; the warp culls only when all three are set
+  unsigned char plane_ok[4];
 };
 
 // One third of a triangle's record: part e computes the edge plane through o
 // and edge e (and, for e = 0, the Moeller-Trumbore terms), so three threads
-// build a record.  Edge planes that come out degenerate leave their bit of
-// `cull` clear; culling applies only when all three bits are set.  `cull`
-// must be zeroed beforehand (bits are OR-ed in from the three parts).
+// build a record.  Degenerate edge planes clear their plane_ok byte; culling
+// applies only when all three are set.
 __device__ __forceinline__ void make_tri_bin_part(const SceneView& s, int t, int e, double ox,
                                                   double oy, double oz, TriBin& B) {
   const double* v0 = s.v0 + 3 * t;
@@ -308,6 +308,7 @@ __device__ __forceinline__ void make_tri_bin_part(const SceneView& s, int t, int
     w[k][1] = py * inv;
     w[k][2] = pz * inv;
   }
+  B.plane_ok[e] = 0;
   if (degenerate) return;
   // the plane through o and edge e, oriented toward the opposite vertex
   const double* a = w[e];
@@ -332,13 +333,12 @@ __device__ __forceinline__ void make_tri_bin_part(const SceneView& s, int t, int
   nb[0] = (float)nx;
   nb[1] = (float)ny;
   nb[2] = (float)nz;
-  atomicOr(&B.cull, 1 << e);
+  B.plane_ok[e] = 1;
 }
 
 // Whole record by one thread.
 __device__ __forceinline__ void make_tri_bin(const SceneView& s, int t, double ox, double oy,
                                              double oz, TriBin& B) {
-  B.cull = 0;
   for (int e = 0; e < 3; ++e) make_tri_bin_part(s, t, e, ox, oy, oz, B);
 }
 
@@ -389,7 +389,7 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
     bool cand = t < n;
     if (cand && cull) {
       const TriBin& B = tb[t];
-      if (B.cull == 7)
+      if (B.plane_ok[0] & B.plane_ok[1] & B.plane_ok[2])
         cand = (fax * B.n0x + fay * B.n0y + faz * B.n0z >= reach) &&
                (fax * B.n1x + fay * B.n1y + faz * B.n1z >= reach) &&
                (fax * B.n2x + fay * B.n2y + faz * B.n2z >= reach);
