@@ -113,7 +113,8 @@ __global__ void k_occluded(SceneView s, const double* __restrict__ orig,
 // ---------------------------------------------------------------------------
 __device__ void shade_path(int64_t p, int depth, const SceneView& sa, const GuideView& g,
                            const PathsView& P, const double* hit_t, const int32_t* hit_tri,
-                           const int32_t* bin_slot, bool rr_enabled, int rr_depth) {
+                           const int32_t* bin_slot, bool rr_enabled, int rr_depth,
+                           const TriRec* smt) {
   int32_t tri = hit_tri[p];
   if (tri < 0) {
     P.alive[p] = 0;
@@ -244,7 +245,12 @@ __device__ void shade_path(int64_t p, int depth, const SceneView& sa, const Guid
       double cos_s = nsx * lx + nsy * ly + nsz * lz;
       if (cos_l > 1e-9 && cos_s > 0.0 && !grazing && le[0] + le[1] + le[2] > 0.0) {
         double pl = dist * dist / (sa.em_area * cos_l);
-        bool blocked = bvh_occluded(sa, px, py, pz, lx, ly, lz, sa.ray_eps, dist - sa.ray_eps);
+        // any-hit: brute force over the triangles in shared memory for small
+        // scenes (the hit / no-hit answer does not depend on the traversal)
+        bool blocked = smt ? brute_occluded(smt, sa.n_tris, px, py, pz, lx, ly, lz, sa.ray_eps,
+                                            dist - sa.ray_eps)
+                           : bvh_occluded(sa, px, py, pz, lx, ly, lz, sa.ray_eps,
+                                          dist - sa.ray_eps);
         if (!blocked) {
           double p_cont;
           if (guided) {
@@ -341,11 +347,15 @@ __global__ void __launch_bounds__(256, 3) k_shade(SceneView s, GuideView g, Path
                                                const int32_t* __restrict__ hit_tri,
                                                const int32_t* __restrict__ bin_slot, int rr,
                                                int rr_depth) {
+  extern __shared__ TriRec smt_shade[];
+  if (s.brute) load_tris_smem(s, smt_shade);
+  __syncthreads();
   const int64_t n = dev_count(n_max, n_dev);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int64_t p = active ? active[i] : i;
-    shade_path(p, depth, s, g, P, hit_t, hit_tri, bin_slot, rr != 0, rr_depth);
+    shade_path(p, depth, s, g, P, hit_t, hit_tri, bin_slot, rr != 0, rr_depth,
+               s.brute ? smt_shade : nullptr);
   }
 }
 
@@ -440,8 +450,9 @@ int launch_shade(const SceneView& s, const GuideView& g, const PathsView& P, int
                  cudaStream_t st) {
   if (n_max <= 0) return WFPG_OK;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_max, 256), kNumSMs * 8));
-  k_shade<<<grid, 256, 0, st>>>(s, g, P, depth, active, n_max, n_dev, hit_t, hit_tri, bin_slot,
-                                rr ? 1 : 0, rr_depth);
+  const size_t smem = s.brute ? sizeof(TriRec) * s.n_tris : 0;
+  k_shade<<<grid, 256, smem, st>>>(s, g, P, depth, active, n_max, n_dev, hit_t, hit_tri,
+                                   bin_slot, rr ? 1 : 0, rr_depth);
   WFPG_CHECK_LAUNCH("k_shade");
   return WFPG_OK;
 }
