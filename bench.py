@@ -32,7 +32,8 @@ sys.path.insert(0, REPO)
 
 HBM_PEAK_FALLBACK = 6650.0
 SCENES = {"c2": ("cornell.scene", 1024, "C2: Cornell"),
-          "c3": ("c3_two_rooms.scene", 2048, "C3: occluded-light two-room interior")}
+          "c3": ("c3_two_rooms.scene", 2048, "C3: occluded-light two-room interior"),
+          "tess": ("cornell_tess.scene", 1024, "Cornell tessellated to 2,304 triangles (BVH)")}
 
 
 def parse():
@@ -44,7 +45,8 @@ def parse():
     p.add_argument("--width", type=int, default=1920)
     p.add_argument("--height", type=int, default=1080)
     p.add_argument("--scene", default="c2", choices=list(SCENES),
-                   help="c2: Cornell box (the headline); c3: occluded-light two-room interior")
+                   help="c2: Cornell box (the headline); c3: occluded-light two-room "
+                        "interior; tess: Cornell with 2,304 triangles (BVH paths)")
     p.add_argument("--svo-res", type=int, default=None,
                    help="SVO resolution (default 1024 for c2, 2048 for c3)")
     p.add_argument("--depth", type=int, default=4)

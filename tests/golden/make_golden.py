@@ -349,6 +349,52 @@ def gen_cli():
 
 
 # ---------------------------------------------------------------------------
+TESS_CFG = dict(W=32, H=32, R=64, svo_seed=0, max_depth=4, field_res=32, l_min=3, c_ray=16,
+                seed=7)
+
+
+def gen_tess():
+    """BVH-path scene (scenegen.write_tessellated_cornell, 2,304 triangles):
+    SVO digests, intersection queries, a PT-first and a guided pass."""
+    c = TESS_CFG
+    sc = rscene.load_scene(os.path.join(HERE, "..", "..", "scenes", "cornell_tess.scene"))
+    cam = sc.camera
+    sc.camera = rscene.Camera(cam.position, cam.target, cam.up, cam.vfov_deg, c["W"], c["H"])
+    out = {"cfg_keys": np.array(list(c)), "cfg_vals": np.array(list(c.values()))}
+    dig = []
+    for res, seed in ((64, 0), (128, 1)):
+        frags = rsvo.voxelize(sc, res)
+        lo, side = rsvo.scene_cube(sc)
+        tree = rsvo.build_octree(frags, lo, side, res, seed)
+        dig.append(",".join([str(res), str(seed), str(len(frags)), str(tree.node_count),
+                             digest(tree.level_off.astype(np.int64)), digest(tree.codes),
+                             digest(tree.child_base.astype(np.int64)), digest(tree.child_mask),
+                             digest(tree.parent.astype(np.int64)), digest(tree.normal)]))
+    out["svo_digests"] = np.array(dig)
+    rng = np.random.default_rng(13)
+    lo, hi = sc.bbox_lo, sc.bbox_hi
+    org = lo + (hi - lo) * (0.05 + 0.9 * rng.random((4096, 3)))
+    dirs = rng.standard_normal((4096, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    t, tri = sc.intersect_batch(org, dirs)
+    out.update(isect_o=org, isect_d=dirs, isect_t=t, isect_tri=tri)
+    tree = rsvo.build_from_scene(sc, c["R"], seed=c["svo_seed"])
+    for tag, sample, g in (("p0", 0, 0), ("p1", 1, c["max_depth"])):
+        cfg = wavefront.GuidingConfig(max_depth=c["max_depth"], guided_depths=g,
+                                      field_res=c["field_res"], l_min=c["l_min"],
+                                      c_ray=c["c_ray"], seed=c["seed"])
+        f, st, cap = _capture_pass(sc, tree, cfg, sample)
+        out[tag + "_frame"] = f
+        for k in ("radiance", "rec_pos", "emit_depth"):
+            out[f"{tag}_{k}"] = cap["state"][k]
+        for k, v in _svo_state(tree).items():
+            out[f"{tag}_svo_" + k] = v
+        out[tag + "_bins_per_depth"] = np.array(st.bins_per_depth)
+        print(tag, "bins", st.bins_per_depth)
+    save("tess_golden.npz", **out)
+
+
+# ---------------------------------------------------------------------------
 RELMSE_RUNS = dict(spp=32, depth=5, svo_res=64, field_res=32, lmin=3, cray=16)
 
 
