@@ -34,7 +34,19 @@ __global__ void k_part_count(SvoView v, int32_t* __restrict__ counter,
       int32_t qx = quantise(pos[3 * i], v.lox, v.scale, v.resolution);
       int32_t qy = quantise(pos[3 * i + 1], v.loy, v.scale, v.resolution);
       int32_t qz = quantise(pos[3 * i + 2], v.loz, v.scale, v.resolution);
-      for (int level = 1; level <= v.depth; ++level) {
+      int level0 = 1;
+      if (v.top && v.top_level <= l_min + 1) {
+        // the dense top index gives the level-T ancestor in one load; only
+        // levels above l_min enter the counts, so the skipped chain is unused
+        const int T = v.top_level, sh = v.depth - T;
+        const uint2 e = __ldg(&v.top[((uint32_t)(qx >> sh) << (2 * T)) |
+                                     ((uint32_t)(qy >> sh) << T) | (uint32_t)(qz >> sh)]);
+        node = (int32_t)e.x;
+        lvl = (int32_t)(e.y & 0xFFu);
+        chain[lvl] = node;
+        level0 = (e.y >> 31) ? T + 1 : v.depth + 1;  // absent below: the chain ends at lvl
+      }
+      for (int level = level0; level <= v.depth; ++level) {
         int sh = v.depth - level;
         int oct = ((qx >> sh) & 1) | (((qy >> sh) & 1) << 1) | (((qz >> sh) & 1) << 2);
         uint2 d = __ldg(&v.desc[node]);

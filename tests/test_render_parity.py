@@ -257,3 +257,30 @@ def test_frame_pipeline_matches_render_pass(R, setup):
         assert np.array_equal(f.view(np.uint64), r.view(np.uint64))
         assert st.bins_per_depth
     assert np.array_equal(tree.mean_a.view(np.uint64), ref_mean.view(np.uint64))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("res,l_min,c_ray", [(256, 5, 512), (256, 3, 16), (1024, 5, 512)])
+def test_partition_matches_oracle_at_scale(scene_path, res, l_min, c_ray):
+    """Alg. 2 on the device (incl. the dense top-index start when l_min is
+    deep enough) against the CPU oracle, 200k hit points on the Cornell walls."""
+    from oracle import render as OR
+    from paper_2405_06997_b200 import scene as S, svo, wavefront
+
+    sc0 = S.load_scene(scene_path("cornell.scene"))
+    tree = svo.build_from_scene(sc0, res, seed=0)
+    osc = OR.Scene(sc0)
+    built = {k: getattr(tree, k) for k in ("level_off", "codes", "child_base", "child_mask",
+                                           "parent", "normal")}
+    osvo = OR.Svo(built, tree.cube_lo, tree.cube_size, tree.resolution)
+    rng = np.random.default_rng(res + l_min)
+    o = np.tile(sc0.camera.position, (200000, 1))
+    d = rng.standard_normal((200000, 3))
+    d[:, 2] = np.abs(d[:, 2]) + 0.5
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    t, tri = OR.intersect(osc, o, d)
+    pos = (o + t[:, None] * d)[tri >= 0]
+    nodes, members = OR.partition(osvo, pos, l_min, c_ray)
+    bins = wavefront.partition_spatial(tree, pos, np.arange(len(pos)), l_min, c_ray)
+    assert [b.node for b in bins] == list(nodes)
+    assert all(np.array_equal(b.members, m) for b, m in zip(bins, members))
