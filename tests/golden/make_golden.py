@@ -349,6 +349,20 @@ def gen_cli():
 
 
 # ---------------------------------------------------------------------------
+def gen_dump():
+    """WFPGSVO1 dumps written by the reference (svo.py:344-362): a fresh
+    Cornell build at R=16 (seed 0) and the same tree after a 16x16 PT-first
+    pass (exitance state)."""
+    sc = load_scene("cornell.scene", 16, 16)
+    tree = rsvo.build_from_scene(sc, 16, seed=0)
+    tree.dump(os.path.join(HERE, "svo_cornell_r16_fresh.wfpgsvo"))
+    cfg = wavefront.GuidingConfig(max_depth=4, guided_depths=0, l_min=2, c_ray=8, seed=3)
+    wavefront.render_pass(sc, tree, cfg, [0])
+    tree.dump(os.path.join(HERE, "svo_cornell_r16_pt.wfpgsvo"))
+    print("nodes", tree.node_count, "weights", tree.weight_a.sum() + tree.weight_b.sum())
+
+
+# ---------------------------------------------------------------------------
 TESS_CFG = dict(W=32, H=32, R=64, svo_seed=0, max_depth=4, field_res=32, l_min=3, c_ray=16,
                 seed=7)
 
