@@ -169,15 +169,22 @@ def build_workload(args, rank=0, world=1):
     return sc, tree, mk(0), mk(args.depth), build_ms
 
 
-def traffic(args):
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
-    capture of this workload (profiles/traffic.json), else None."""
+def _traffic_entry(args):
     key = f"{args.scene}:{args.width}x{args.height}:R{args.svo_res}:D{args.depth}:N{args.field_res}"
     try:
         with open(os.path.join(REPO, "profiles", "traffic.json")) as fh:
-            t = json.load(fh).get(key)
+            return json.load(fh).get(key)
+    except (OSError, ValueError):
+        return None
+
+
+def traffic(args):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
+    capture of this workload (profiles/traffic.json), else None."""
+    t = _traffic_entry(args)
+    try:
         return None if t is None else t["dram_read_bytes"] + t["dram_write_bytes"]
-    except (OSError, ValueError, KeyError):
+    except KeyError:
         return None
 
 
@@ -290,7 +297,8 @@ def run_b200(args):
             "launch_ms": d1_ms, "bytes_per_launch": d1_bytes,
             "cones_per_launch": cones[1] / max(nl[1], 1), "bytes_per_cone": bpc,
             "gcones_per_s": (cones[1] / max(nl[1], 1)) / (d1_ms / 1e3) / 1e9 if d1_ms else None,
-            "field_share_of_step": field_ms_step / ms_step}
+            "field_share_of_step": field_ms_step / ms_step,
+            "limiter": (_traffic_entry(args) or {}).get("limiter")}
 
     # e2e through the public API: every pass's frame delivered to pinned host
     # memory by wavefront.FramePipeline (D2H of pass i overlapped with pass i+1)
