@@ -267,9 +267,15 @@ struct TriBin {
   // or near the triangle's plane / an edge line) disables the cull.
   // (fp32: the cull carries a 1e-5 slack, far above their rounding)
   float n0x, n0y, n0z, n1x, n1y, n1z, n2x, n2y, n2z;
+  // unit normal of the triangle's own plane; `flat` when o lies within
+  // 1e-5 * tmin of that plane (bin origins are hit points on surfaces): a
+  // ray can then only hit the triangle beyond tmin if it is within 1e-5 of
+  // parallel to the plane, so tiles that stay away from that band skip it
+  float pnx, pny, pnz;
   // per-plane validity, one byte per part so the three builders write
   // without atomics; the warp culls only when all three are set
-  unsigned char plane_ok[4];
+  unsigned char plane_ok[3];
+  unsigned char flat;
 };
 
 // One third of a triangle's record: part e computes the edge plane through o
@@ -293,6 +299,12 @@ __device__ __forceinline__ void make_tri_bin_part(const SceneView& s, int t, int
     B.qy = tz * e1[0] - tx * e1[2];
     B.qz = tx * e1[1] - ty * e1[0];
     B.ts0 = e2[0] * B.qx + e2[1] * B.qy + e2[2] * B.qz;
+    // |ts0| = |tvec . (e1 x e2)| = plane distance * |n|
+    const double nl = sqrt(B.nx * B.nx + B.ny * B.ny + B.nz * B.nz);
+    B.pnx = (float)(B.nx / nl);
+    B.pny = (float)(B.ny / nl);
+    B.pnz = (float)(B.nz / nl);
+    B.flat = fabs(B.ts0) < 1e-5 * s.ray_eps * nl ? 1 : 0;
   }
   // unit directions from o to the three vertices
   double w[3][3];
@@ -382,6 +394,10 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
   // -|a| (sin(th) + slack): a ray within th of the axis cannot reach the
   // inner side of a plane whose normal n has a.n below this
   const float reach = -(sqrtf(fmaxf(1.0f - cm * cm, 0.0f)) + 1e-5f) * fal;
+  // every ray of the tile is within 2 sin(th/2) = sqrt(2 - 2 cos th) of the
+  // unit axis, so |d.n| >= |a.n| - that: tiles clear of a flat triangle's
+  // grazing band (|d.n| <= 1e-5, plus fp32 slack) cannot hit it past tmin
+  const float graze = (sqrtf(fmaxf(2.0f - 2.0f * cm, 0.0f)) + 3e-5f) * fal;
   double best = 1e300;
   int32_t id = -1;
   for (int g = 0; g < n; g += 32) {
@@ -393,6 +409,8 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
         cand = (fax * B.n0x + fay * B.n0y + faz * B.n0z >= reach) &&
                (fax * B.n1x + fay * B.n1y + faz * B.n1z >= reach) &&
                (fax * B.n2x + fay * B.n2y + faz * B.n2z >= reach);
+      else if (B.flat)
+        cand = fabsf(fax * B.pnx + fay * B.pny + faz * B.pnz) <= graze;
     }
     unsigned m = __ballot_sync(0xffffffffu, cand);
     while (m) {
