@@ -413,6 +413,12 @@ int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camera* 
                      const wfpg_pass_config* cfg, wfpg_paths* paths, double* frame,
                      wfpg_pass_stats* stats, void* workspace, size_t ws_bytes, void* stream);
 
+/* Drop the captured CUDA graph (and the seen-once key) of passes that ran
+ * on `workspace` (NULL: all); call before freeing a workspace that was used
+ * with use_graph = 1.  The render entry points serialise on an internal lock
+ * for the graph cache. */
+int wfpg_graph_release(const void* workspace);
+
 /* Eq. 7 running sum on the device (accumulation.py:50-60): acc[i] += hw *
  * frame[i] (product rounded first, as numpy).  Non-finite frame values are
  * skipped and set *nonfinite_flag (device int32, optional) so the host can

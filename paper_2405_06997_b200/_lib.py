@@ -123,6 +123,7 @@ _SIGS = {
     "wfpg_svo_top_index_bytes": (c_size, [c_i32]),
     "wfpg_svo_build_top_index": (c_i32, [P(Svo), c_vp]),
     "wfpg_svo_refresh_leaves": (c_i32, [P(Svo), c_vp, c_i64, c_vp, c_vp]),
+    "wfpg_graph_release": (c_i32, [c_vp]),
     "wfpg_frame_accumulate": (c_i32, [c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp]),
     "wfpg_quantise_points": (c_i32, [c_vp, c_dbl, c_i32, c_vp, c_i64, c_vp, c_vp]),
     "wfpg_accumulate_workspace_bytes": (c_size, [c_i64]),

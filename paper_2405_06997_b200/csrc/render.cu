@@ -5,6 +5,7 @@
 // the worst case, so the whole pass is a single stream of launches with one
 // host synchronisation at the end (to return PassStats).
 #include <cstring>
+#include <mutex>
 #include <utility>
 #include <vector>
 
@@ -467,8 +468,12 @@ struct GraphEntry {
   cudaGraphExec_t exec;
   uint64_t kernels;
 };
+// Graph cache: at most one captured graph and one "seen once" key per
+// workspace (a new configuration on the same workspace replaces them);
+// wfpg_graph_release drops a workspace's entries when its owner frees it.
 static std::vector<GraphEntry> g_graphs;
 static std::vector<std::pair<const void*, uint64_t>> g_seen;
+static std::mutex g_graph_mu;
 
 static uint64_t fnv(uint64_t h, const void* p, size_t n) {
   const unsigned char* b = static_cast<const unsigned char*>(p);
@@ -542,6 +547,7 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
     WFPG_TRY(enqueue_pass(scene, svo, cam, cfg, paths, frame, workspace, ws_bytes, L, prof, st));
   } else {
     const uint64_t key = pass_key(scene, svo, cam, cfg, paths, frame, ws_bytes, prof);
+    std::lock_guard<std::mutex> lock(g_graph_mu);
     GraphEntry* ge = nullptr;
     for (auto& e : g_graphs)
       if (e.ws == workspace && e.key == key) ge = &e;
@@ -570,6 +576,11 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
     } else if (!seen) {
       // first pass of this configuration runs eagerly (one-time kernel attribute
       // setup happens outside any capture); the next one is captured
+      for (size_t i = 0; i < g_seen.size(); ++i)
+        if (g_seen[i].first == workspace) {
+          g_seen.erase(g_seen.begin() + i);
+          break;
+        }
       g_seen.push_back({workspace, key});
       WFPG_TRY(enqueue_pass(scene, svo, cam, cfg, paths, frame, workspace, ws_bytes, L, prof, st));
     } else {
@@ -666,5 +677,24 @@ extern "C" int wfpg_frame_accumulate(double* acc, const double* frame, int64_t n
   k_frame_accumulate<<<grid, 256, 0, (cudaStream_t)stream>>>(acc, frame, n, hw,
                                                                    nonfinite_flag);
   WFPG_CHECK_LAUNCH("k_frame_accumulate");
+  return WFPG_OK;
+}
+
+extern "C" int wfpg_graph_release(const void* workspace) {
+  std::lock_guard<std::mutex> lock(g_graph_mu);
+  for (size_t i = 0; i < g_graphs.size();) {
+    if (!workspace || g_graphs[i].ws == workspace) {
+      cudaGraphExecDestroy(g_graphs[i].exec);
+      g_graphs.erase(g_graphs.begin() + i);
+    } else {
+      ++i;
+    }
+  }
+  for (size_t i = 0; i < g_seen.size();) {
+    if (!workspace || g_seen[i].first == workspace)
+      g_seen.erase(g_seen.begin() + i);
+    else
+      ++i;
+  }
   return WFPG_OK;
 }

@@ -158,6 +158,13 @@ def bin_stream(cfg_seed, sample_index, depth, node_id):
     return core.RngStream(cfg_seed, bin_stream_id(sample_index, depth, node_id))
 
 
+def _release_graph(ptr):
+    try:
+        _lib.load().wfpg_graph_release(_lib.C.c_void_p(ptr))
+    except Exception:  # interpreter shutdown
+        pass
+
+
 class PassRunner:
     """Owns the device buffers of repeated passes with one configuration
     (path state, frame, workspace) so that steady-state rendering allocates
@@ -210,6 +217,10 @@ class PassRunner:
             C.byref(self.cam), C.byref(pc))
         self.ws = _dev.workspace(nbytes)
         self.stats = _lib.PassStats()
+        # drop this workspace's captured graph when the runner goes away
+        import weakref
+
+        weakref.finalize(self, _release_graph, self.ws.data_ptr())
 
     def launch(self, sample_index, want_stats=True):
         """Enqueue one pass; with want_stats the call synchronises and fills self.stats."""
