@@ -329,6 +329,31 @@ def gen_cli():
         out[tag + "_image"] = img
         out[tag + "_frame"] = frame
         out[tag + "_bins_per_depth"] = np.array(st.bins_per_depth)
+    # a guided pass over two consecutive samples (bins pool both samples'
+    # paths; bin streams use the first sample index, wavefront.py:249)
+    gcfg = wavefront.GuidingConfig(max_depth=c["max_depth"], guided_depths=c["max_depth"],
+                                   field_res=c["field_res"], l_min=c["l_min"], c_ray=c["c_ray"],
+                                   seed=c["seed"])
+    wavefront.render_pass(sc, tree, cfg, [5])  # some exitance state first
+    for k, v in _svo_state(tree).items():
+        out["multi_pre_" + k] = v
+    cap = {}
+    orig_update = wavefront.update_exitance
+
+    def upd(state, svo):
+        cap["state"] = {k: getattr(state, k).copy() for k in ("radiance", "rec_pos",
+                                                               "emit_depth")}
+        return orig_update(state, svo)
+
+    wavefront.update_exitance = upd
+    try:
+        fm, stm = wavefront.render_pass(sc, tree, gcfg, [1, 2])
+    finally:
+        wavefront.update_exitance = orig_update
+    out["multi_frame"] = fm
+    out["multi_bins_per_depth"] = np.array(stm.bins_per_depth)
+    for k, v in cap["state"].items():
+        out["multi_" + k] = v
     tmp = tempfile.mkdtemp()
     runs = (("pt", dict(mode="pt", spp=2)),
             ("wfpg", dict(mode="wfpg", spp=3, depth=4, svo_res=64, field_res=32, lmin=3,

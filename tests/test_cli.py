@@ -163,3 +163,31 @@ def test_cli_run_matches_reference(G, scene_path, tmp_path, tag, kw):
         assert len(got) == len(want)
         # the first pass (and its bins) is identical
         assert got[0] == want[0]
+
+
+@pytest.mark.gpu
+def test_two_sample_guided_pass_matches_reference(G, golden, scene_path):
+    """render_pass over consecutive samples [1, 2] with guiding: bins pool both
+    samples' paths and bin streams use the first index (wavefront.py:249)."""
+    from paper_2405_06997_b200 import scene as S, svo, wavefront
+
+    R = golden("render_golden.npz")
+    c = dict(zip([str(k) for k in R["cfg_keys"]], [int(v) for v in R["cfg_vals"]]))
+    sc = S.load_scene(scene_path("cornell.scene"))
+    cam = sc.camera
+    sc.camera = S.Camera(cam.position, cam.target, cam.up, cam.vfov_deg, c["W"], c["H"])
+    tree = svo.build_from_scene(sc, c["R"], seed=c["svo_seed"])
+    for k in ("sum_a", "sum_b", "weight_a", "weight_b"):
+        setattr(tree, k, G["multi_pre_" + k])
+    tree.propagate_up()
+    cfg = wavefront.GuidingConfig(max_depth=c["max_depth"], guided_depths=c["max_depth"],
+                                  field_res=c["field_res"], l_min=c["l_min"], c_ray=c["c_ray"],
+                                  seed=c["seed"])
+    frame, st = wavefront.render_pass(sc, tree, cfg, [1, 2])
+    assert list(st.bins_per_depth)[:1] == list(G["multi_bins_per_depth"])[:1]
+    state = wavefront._RUNNERS[next(iter(wavefront._RUNNERS))].state
+    assert state.n == 2 * c["W"] * c["H"]
+    same = state.emit_depth == G["multi_emit_depth"]
+    same &= np.abs(state.rec_pos - G["multi_rec_pos"]).max(axis=(1, 2)) <= 1e-5 * sc.diagonal
+    assert same.mean() >= 0.98, same.mean()
+    np.testing.assert_allclose(frame.mean(), G["multi_frame"].mean(), rtol=0.05)
