@@ -259,7 +259,7 @@ __device__ __forceinline__ bool bvh_occluded(const SceneView& b, double ox, doub
 // so each candidate costs three 3-term dot products.  The reassociation moves
 // det / u / v by a few ulp against the reference's operand order, which only
 // matters for rays within ~1e-16 of a triangle edge (field tolerance 1e-9).
-struct TriBin {
+struct __align__(16) TriBin {
   double nx, ny, nz, wx, wy, wz, qx, qy, qz, ts0;
   // unit normals of the three planes through o and an edge, oriented toward
   // the opposite vertex: the triangle's solid angle seen from o is the
