@@ -404,13 +404,15 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
     const int t = g + lane;
     bool cand = t < n;
     if (cand && cull) {
+      // branch-free per lane (each lane holds a different triangle)
       const TriBin& B = tb[t];
-      if (B.plane_ok[0] & B.plane_ok[1] & B.plane_ok[2])
-        cand = (fax * B.n0x + fay * B.n0y + faz * B.n0z >= reach) &&
-               (fax * B.n1x + fay * B.n1y + faz * B.n1z >= reach) &&
-               (fax * B.n2x + fay * B.n2y + faz * B.n2z >= reach);
-      else if (B.flat)
-        cand = fabsf(fax * B.pnx + fay * B.pny + faz * B.pnz) <= graze;
+      const float d0 = fax * B.n0x + fay * B.n0y + faz * B.n0z;
+      const float d1 = fax * B.n1x + fay * B.n1y + faz * B.n1z;
+      const float d2 = fax * B.n2x + fay * B.n2y + faz * B.n2z;
+      const float dp = fabsf(fax * B.pnx + fay * B.pny + faz * B.pnz);
+      const bool planes = B.plane_ok[0] & B.plane_ok[1] & B.plane_ok[2];
+      const bool inside = (d0 >= reach) & (d1 >= reach) & (d2 >= reach);
+      cand = planes ? inside : (!B.flat | (dp <= graze));
     }
     unsigned m = __ballot_sync(0xffffffffu, cand);
     while (m) {
