@@ -386,18 +386,24 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
   const float fax = __shfl_sync(0xffffffffu, (float)dx, 12);
   const float fay = __shfl_sync(0xffffffffu, (float)dy, 12);
   const float faz = __shfl_sync(0xffffffffu, (float)dz, 12);
-  const float fal = sqrtf(fax * fax + fay * fay + faz * faz);
-  float cm = ((float)dx * fax + (float)dy * fay + (float)dz * faz) / fal - 4e-6f;
+  // (MUFU reciprocal square roots: their ~1e-7 relative error sits far
+  // inside the slacks)
+  const float fal2 = fax * fax + fay * fay + faz * faz;
+  const float inv_fal = rsqrtf(fal2);
+  const float fal = fal2 * inv_fal;
+  float cm = ((float)dx * fax + (float)dy * fay + (float)dz * faz) * inv_fal - 4e-6f;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cm = fminf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
   const bool cull = cm > 0.0f;
   // -|a| (sin(th) + slack): a ray within th of the axis cannot reach the
   // inner side of a plane whose normal n has a.n below this
-  const float reach = -(sqrtf(fmaxf(1.0f - cm * cm, 0.0f)) + 1e-5f) * fal;
+  const float s2 = fmaxf(1.0f - cm * cm, 1e-30f);
+  const float reach = -(s2 * rsqrtf(s2) + 1e-5f) * fal;
   // every ray of the tile is within 2 sin(th/2) = sqrt(2 - 2 cos th) of the
   // unit axis, so |d.n| >= |a.n| - that: tiles clear of a flat triangle's
   // grazing band (|d.n| <= 1e-5, plus fp32 slack) cannot hit it past tmin
-  const float graze = (sqrtf(fmaxf(2.0f - 2.0f * cm, 0.0f)) + 3e-5f) * fal;
+  const float g2 = fmaxf(2.0f - 2.0f * cm, 1e-30f);
+  const float graze = (g2 * rsqrtf(g2) + 3e-5f) * fal;
   double best = 1e300;
   int32_t id = -1;
   for (int g = 0; g < n; g += 32) {
