@@ -162,6 +162,34 @@ __device__ __forceinline__ void octa_uv_to_dir_np(double u, double v, double* ox
   *oz = __ddiv_rn(z, nrm);
 }
 
+// Division / square root without the IEEE slow-path checks, for values that
+// only need to be within a few ulp (the field-cell map and hit distances,
+// compared to the reference with a 1e-9 tolerance): hardware approximation
+// refined by Newton steps.  Arguments must be normal, positive where noted.
+__device__ __forceinline__ double fast_div(double a, double b) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+  double e = fma(-b, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-b, r, 1.0);
+  r = fma(r, e, r);
+  double q = a * r;
+  return fma(fma(-b, q, a), r, q);
+}
+__device__ __forceinline__ double fast_sqrt(double x) {  // x > 0
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double h = 0.5 * y;
+  double g = x * y;
+  double e = fma(-g, h, 0.5);  // Goldschmidt / Newton on (g, h) -> (sqrt x, 1/(2 sqrt x))
+  g = fma(g, e, g);
+  h = fma(h, e, h);
+  e = fma(-g, h, 0.5);
+  g = fma(g, e, g);
+  h = fma(h, e, h);
+  return fma(fma(-g, g, x), h, g);
+}
+
 // sin / cos of t * pi / 4 for t in [0, 2]: x = (t - 1) * pi / 4 lies in
 // [-pi/4, pi/4], where Taylor series to x^17 / x^18 are below 1e-18; then
 // sin(pi/4 + x) = (sin x + cos x) / sqrt 2, cos(pi/4 + x) = (cos x - sin x) / sqrt 2.
@@ -207,9 +235,9 @@ __device__ __forceinline__ void octa_uv_to_dir_cell(double u, double v, double* 
   double ap = fabs(a), bp = fabs(b);
   double sd = __dsub_rn(1.0, __dadd_rn(ap, bp));
   double r = __dsub_rn(1.0, fabs(sd));
-  double t = (r == 0.0) ? 1.0 : __dadd_rn(__ddiv_rn(__dsub_rn(bp, ap), r), 1.0);  // phi / (pi/4)
+  double t = (r == 0.0) ? 1.0 : fast_div(bp - ap, r) + 1.0;  // phi / (pi/4)
   double rr = __dmul_rn(r, r);
-  double rho = __dmul_rn(r, __dsqrt_rn(fmax(__dsub_rn(2.0, rr), 0.0)));
+  double rho = r * fast_sqrt(fmax(2.0 - rr, 1.0));  // 2 - r^2 is in [1, 2]
   double s, c;
   sincos_quarter_turn(t, &s, &c);
   *ox = __dmul_rn(copysign(c, a), rho);

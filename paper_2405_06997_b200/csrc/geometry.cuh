@@ -433,7 +433,7 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
       double ts = B.ts0 * sg;
       bool ok = (ad > 1e-300) & (us >= 0.0) & (vs >= 0.0) & (us + vs <= ad) & (ts > tmin * ad);
       if (__any_sync(0xffffffffu, ok)) {  // the division only when some lane hits
-        double h = ts / ad;
+        double h = fast_div(ts, ad);  // ad > 1e-300 on the lanes that use it
         if (ok && h < best) {
           best = h;
           id = k;
