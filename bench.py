@@ -52,6 +52,10 @@ def parse():
     p.add_argument("--depth", type=int, default=4)
     p.add_argument("--field-res", type=int, default=128)
     p.add_argument("--product", action="store_true")
+    p.add_argument("--tiled", action="store_true",
+                   help="C4: --width x --height is the whole image, split into one band per "
+                        "GPU (strong scaling); default: every GPU renders its own "
+                        "width x height band of a taller image (weak scaling)")
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--cpu-seconds", type=float, default=20.0,
                    help="budget of the CPU-baseline sample")
@@ -148,6 +152,10 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def image_height(args, world):
+    return args.height if args.tiled else args.height * world
+
+
 def build_workload(args, rank=0, world=1):
     import torch
 
@@ -155,9 +163,10 @@ def build_workload(args, rank=0, world=1):
 
     sc = S.load_scene(os.path.join(REPO, "scenes", SCENES[args.scene][0]))
     cam = sc.camera
-    # weak scaling: rank r renders band r of a width x (height * world) image
+    # weak scaling: rank r renders band r of a width x (height * world) image;
+    # --tiled (C4): the width x height image is split into world bands
     sc.camera = S.Camera(cam.position, cam.target, cam.up, cam.vfov_deg, args.width,
-                         args.height * world)
+                         image_height(args, world))
     t0 = time.perf_counter()
     tree = svo.build_from_scene(sc, args.svo_res, seed=args.seed)
     torch.cuda.synchronize()
@@ -221,7 +230,8 @@ def run_b200(args):
     # per-pass SVO sync: every rank exports its deposits, all-gathers the
     # lists and splats them in global path order (multigpu.DepositExchange)
     sync_svo = multigpu.DepositExchange(tree) if world > 1 else None
-    off, npx = multigpu.band(args.width * args.height * world, rank, world)
+    total_pix = args.width * image_height(args, world)
+    off, npx = multigpu.band(total_pix, rank, world)
     pt = wavefront.PassRunner(sc, tree, pt_cfg, pixel_offset=off, n_pixels=npx,
                               deposit_sink=sync_svo)
     gr = wavefront.PassRunner(sc, tree, g_cfg, pixel_offset=off, n_pixels=npx,
@@ -276,9 +286,9 @@ def run_b200(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
-    n_paths = args.width * args.height
+    n_paths = npx  # this rank's paths per pass
     ms_step = ms / args.steps
-    value = n_paths * world * args.steps / (ms / 1e3)
+    value = total_pix * args.steps / (ms / 1e3)  # whole job
 
     # roofline of the dominant kernel (depth-1 field generation, n = N0)
     bpc = algorithmic_bytes_per_cone(tree.depth)
@@ -336,7 +346,7 @@ def run_b200(args):
         e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64,
                              device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
-        e2e = {"value": n_paths * world * args.steps / float(e2e_s.item()),
+        e2e = {"value": total_pix * args.steps / float(e2e_s.item()),
                "unit": "path samples/s",
                "h2d_bytes_per_step": C.sizeof(_lib.PassConfig) + C.sizeof(_lib.Camera),
                "d2h_bytes_per_step": npx * 3 * 8 + 4,
@@ -347,13 +357,17 @@ def run_b200(args):
         "metric": "path samples/sec (guided wavefront pass)",
         "value": value, "unit": "path samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic: "
+        "scaling": "strong" if args.tiled else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: "
         f"scenes/{SCENES[args.scene][0]}, path samples from the counter RNG",
-        "config": {"workload": f"{SCENES[args.scene][2]} {args.width}x{args.height} per GPU, "
+        "config": {"workload": f"{SCENES[args.scene][2]} {args.width}x{args.height} "
+                               + ("image tiled over the GPUs, " if args.tiled else "per GPU, ")
+                               + 
                                f"1 spp guided pass, SVO depth {tree.depth}, D={D}, G={D}, N0={args.field_res}, "
                                f"l_min {g_cfg.l_min}, c_ray 512, "
                                f"{'product' if args.product else 'plain'} guiding",
-                   "image": [args.width, args.height * world], "svo_nodes": tree.node_count,
+                   "image": [args.width, image_height(args, world)],
+                   "svo_nodes": tree.node_count,
                    "l2": "inputs larger than L2 (path state + guide tables > 126 MB)",
                    "parallelism": f"image bands x{world}" + (
                        f", per-pass deposit all-gather ({backend})" if world > 1 else "")},
