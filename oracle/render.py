@@ -367,7 +367,8 @@ def render_pass(sc, svo, cfg, sample, stats=None):
                     setattr(g, k, _p(tb.get(k)))
                 g.upper_dirs = _p(UPPER_DIRS)
         lib().ov_shade(C.byref(sc.c), C.byref(g), C.byref(ps), depth, _p(act), len(act),
-                       _p(hit_t), _p(hit_tri), _p(slots), 0, 3)
+                       _p(hit_t), _p(hit_tri), _p(slots), int(bool(cfg.get("russian_roulette", False))),
+                       int(cfg.get("rr_depth", 3)))
         del keep
     if svo is not None:
         update_exitance(st, svo)
