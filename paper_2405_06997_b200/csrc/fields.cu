@@ -33,6 +33,10 @@ __device__ __forceinline__ int fold_once(int raw, int n, bool* flip) {
   return lo ? -1 - raw : (hi ? 2 * n - 1 - raw : raw);
 }
 
+#ifndef WFPG_LANE_TEST_MAX_N
+#define WFPG_LANE_TEST_MAX_N 64
+#endif
+
 template <int N>
 struct FieldCfg {
   static constexpr int kStride = N + 1;  // padded rows: conflict-free column walks
@@ -303,7 +307,8 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
       double bt;
       int32_t bid;
       if (s.brute)
-        warp_nearest_bin(tb, s.n_tris, dx, dy, dz, s.ray_eps, &bt, &bid);
+        warp_nearest_bin<(N <= WFPG_LANE_TEST_MAX_N)>(tb, s.n_tris, dx, dy, dz, s.ray_eps, &bt,
+                                                       &bid);
       else
         bvh_nearest(s, ox, oy, oz, dx, dy, dz, s.ray_eps, &bt, &bid);
       if (bid >= 0) cone_shade_hit(v, ox, oy, oz, dx, dy, dz, bt, omega, rgb);

@@ -375,6 +375,7 @@ __device__ __forceinline__ double warp_min_d(double x) {
 // triangle order with the strict '<' of the brute-force kernel, so the result
 // (minimum t, lowest id on ties) is brute force over all triangles (the 1e-6
 // slack dwarfs the rounding of both the cull and the hit test).
+template <bool LANE_TEST = false>
 __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, int n, double dx,
                                                  double dy, double dz, double tmin, double* bt,
                                                  int32_t* bid) {
@@ -425,6 +426,16 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
       const int k = g + __ffs(m) - 1;
       m &= m - 1;
       const TriBin& B = tb[k];
+      if (LANE_TEST && (B.plane_ok[0] & B.plane_ok[1] & B.plane_ok[2])) {
+        // each lane's own direction against the three edge planes (fp32,
+        // 1e-5 slack): a ray outside the triangle's solid angle cannot hit
+        // it, so the warp skips the exact test when no lane is inside
+        const float fx = (float)dx, fy = (float)dy, fz = (float)dz;
+        const bool in = (fx * B.n0x + fy * B.n0y + fz * B.n0z >= -1e-5f) &
+                        (fx * B.n1x + fy * B.n1y + fz * B.n1z >= -1e-5f) &
+                        (fx * B.n2x + fy * B.n2y + fz * B.n2z >= -1e-5f);
+        if (!__any_sync(0xffffffffu, in)) continue;
+      }
       double det = dx * B.nx + dy * B.ny + dz * B.nz;
       double sg = det > 0.0 ? 1.0 : -1.0;
       double ad = det * sg;
