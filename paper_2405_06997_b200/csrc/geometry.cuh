@@ -57,10 +57,47 @@ inline SceneView make_scene_view(const wfpg_scene* s) {
   return v;
 }
 
-// Triangle record in shared memory (9 doubles).
+// Triangle record in shared memory: the fp64 vertex / edges plus an fp32
+// bounding box padded by 1e-5 of the scene diagonal and 4e-7 of the largest
+// coordinate (far above the fp32 rounding of ray origins, directions and slab
+// distances), used to skip the exact test for rays that miss the box within
+// the current [tmin, best] range.  Skipped triangles provably cannot be hit
+// there, so results equal brute force over all triangles.
 struct TriRec {
   double v0x, v0y, v0z, e1x, e1y, e1z, e2x, e2y, e2z;
+  float blo[3], bhi[3];
 };
+
+// Per-ray fp32 slab setup for the box prefilter.
+struct RaySlab {
+  float ox, oy, oz, ix, iy, iz;
+};
+
+__device__ __forceinline__ RaySlab make_ray_slab(double ox, double oy, double oz, double dx,
+                                                 double dy, double dz) {
+  auto inv = [](double d) {
+    float f = (float)d;
+    if (fabsf(f) < 1e-30f) f = copysignf(1e-30f, f);
+    return 1.0f / f;
+  };
+  return RaySlab{(float)ox, (float)oy, (float)oz, inv(dx), inv(dy), inv(dz)};
+}
+
+// may the ray meet the (padded) box at a parameter in [lo, hi]?
+__device__ __forceinline__ bool slab_maybe(const RaySlab& r, const float* blo, const float* bhi,
+                                           float lo, float hi) {
+  float t0 = (blo[0] - r.ox) * r.ix, t1 = (bhi[0] - r.ox) * r.ix;
+  float tn = fminf(t0, t1), tf = fmaxf(t0, t1);
+  t0 = (blo[1] - r.oy) * r.iy;
+  t1 = (bhi[1] - r.oy) * r.iy;
+  tn = fmaxf(tn, fminf(t0, t1));
+  tf = fminf(tf, fmaxf(t0, t1));
+  t0 = (blo[2] - r.oz) * r.iz;
+  t1 = (bhi[2] - r.oz) * r.iz;
+  tn = fmaxf(tn, fminf(t0, t1));
+  tf = fminf(tf, fmaxf(t0, t1));
+  return (tn <= tf) & (tn <= hi) & (tf >= lo);
+}
 
 constexpr int kMaxBruteTris = 512;
 
@@ -77,6 +114,15 @@ __device__ __forceinline__ void load_tris_smem(const SceneView& s, TriRec* sm) {
     r.e2x = s.e2[3 * t];
     r.e2y = s.e2[3 * t + 1];
     r.e2z = s.e2[3 * t + 2];
+    const double v[3] = {r.v0x, r.v0y, r.v0z}, a[3] = {r.e1x, r.e1y, r.e1z},
+                 b[3] = {r.e2x, r.e2y, r.e2z};
+    for (int c = 0; c < 3; ++c) {
+      const double lo = fmin(v[c], fmin(v[c] + a[c], v[c] + b[c]));
+      const double hi = fmax(v[c], fmax(v[c] + a[c], v[c] + b[c]));
+      const double pad = 0.1 * s.ray_eps + 4e-7 * fmax(fabs(lo), fabs(hi));
+      r.blo[c] = __double2float_rd(lo - pad);
+      r.bhi[c] = __double2float_ru(hi + pad);
+    }
     sm[t] = r;
   }
 }
@@ -106,8 +152,13 @@ __device__ __forceinline__ void brute_nearest(const TriRec* __restrict__ tris, i
                                               double dz, double tmin, double* bt, int32_t* bid) {
   double best = 1e300;
   int32_t id = -1;
+  const RaySlab rs = make_ray_slab(ox, oy, oz, dx, dy, dz);
+  const float lo = (float)tmin * 0.99999f;
+  float hi = 3.0e38f;
   for (int t = 0; t < n; ++t) {
+    if (!slab_maybe(rs, tris[t].blo, tris[t].bhi, lo, hi)) continue;
     double h = mt_brute(tris[t], ox, oy, oz, dx, dy, dz, tmin);
+    if (h > 0.0 && h < best) hi = __double2float_ru(h) * 1.00001f;
     if (h > 0.0 && h < best) {  // accepted hits have ts/ad > tmin > 0
       best = h;
       id = t;
@@ -460,8 +511,11 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
 __device__ __forceinline__ bool brute_occluded(const TriRec* __restrict__ tris, int n, double ox,
                                                double oy, double oz, double dx, double dy,
                                                double dz, double tmin, double tmax) {
+  const RaySlab rs = make_ray_slab(ox, oy, oz, dx, dy, dz);
+  const float lo = (float)tmin * 0.99999f, hi = __double2float_ru(tmax) * 1.00001f;
   for (int t = 0; t < n; ++t) {
     const TriRec& T = tris[t];
+    if (!slab_maybe(rs, T.blo, T.bhi, lo, hi)) continue;
     double px = dy * T.e2z - dz * T.e2y;
     double py = dz * T.e2x - dx * T.e2z;
     double pz = dx * T.e2y - dy * T.e2x;
