@@ -75,6 +75,12 @@ typedef struct wfpg_scene {
   const int32_t* bvh_order;  /* (T,) */
   int32_t brute;             /* 1 when T <= 512: nearest-hit queries use the brute
                                 force path (_kernelshim.py:13-21) */
+  /* Optional (N,8) float BVH node boxes {lo.xyz, 0, hi.xyz, 0} widened by
+   * 1e-5 of the scene diagonal + 4e-7 of the coordinate and rounded outward:
+   * the traversals then run their slab tests in fp32 (triangle tests stay
+   * fp64; the padding dwarfs every fp32 rounding, so no hit is culled).
+   * NULL: fp64 boxes. */
+  const float* bvh_box_f32;
 } wfpg_scene;
 
 /* Pinhole camera: scene.py:29-61 (Camera). Host values. */

@@ -32,7 +32,7 @@ class Scene(C.Structure):
         ("bvh_nodes", c_i32),
         ("bvh_lo", c_vp), ("bvh_hi", c_vp), ("bvh_left", c_vp), ("bvh_right", c_vp),
         ("bvh_count", c_vp), ("bvh_order", c_vp),
-        ("brute", c_i32),
+        ("brute", c_i32), ("bvh_box_f32", c_vp),
     ]
 
 

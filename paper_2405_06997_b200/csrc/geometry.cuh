@@ -30,6 +30,7 @@ struct SceneView {
   const int32_t* bright;
   const int32_t* bcount;
   const int32_t* border;
+  const float4* bbox32;  // optional (N,2) padded fp32 node boxes
 };
 
 inline SceneView make_scene_view(const wfpg_scene* s) {
@@ -54,6 +55,7 @@ inline SceneView make_scene_view(const wfpg_scene* s) {
   v.bright = s->bvh_right;
   v.bcount = s->bvh_count;
   v.border = s->bvh_order;
+  v.bbox32 = reinterpret_cast<const float4*>(s->bvh_box_f32);
   return v;
 }
 
@@ -209,6 +211,25 @@ __device__ __forceinline__ void slab(const double* lo, const double* hi, double 
   *tf = f;
 }
 
+// fp32 slab against a padded node box: (near, far) with the far side
+// rounded up by 1e-6 so it stays conservative
+__device__ __forceinline__ void slab32(const float4* box, const RaySlab& r, float* tn,
+                                       float* tf) {
+  const float4 lo = __ldg(box), hi = __ldg(box + 1);
+  float t0 = (lo.x - r.ox) * r.ix, t1 = (hi.x - r.ox) * r.ix;
+  float n = fminf(t0, t1), f = fmaxf(t0, t1);
+  t0 = (lo.y - r.oy) * r.iy;
+  t1 = (hi.y - r.oy) * r.iy;
+  n = fmaxf(n, fminf(t0, t1));
+  f = fminf(f, fmaxf(t0, t1));
+  t0 = (lo.z - r.oz) * r.iz;
+  t1 = (hi.z - r.oz) * r.iz;
+  n = fmaxf(n, fminf(t0, t1));
+  f = fminf(f, fmaxf(t0, t1));
+  *tn = n;
+  *tf = f;
+}
+
 // _kernels.pyx:398-445
 __device__ __forceinline__ void bvh_nearest(const SceneView& b, double ox, double oy, double oz,
                                             double dx, double dy, double dz, double tmin,
@@ -216,6 +237,7 @@ __device__ __forceinline__ void bvh_nearest(const SceneView& b, double ox, doubl
   int32_t stack[64];
   double dstack[64];
   double ix = 1.0 / dx, iy = 1.0 / dy, iz = 1.0 / dz;
+  const RaySlab rs = make_ray_slab(ox, oy, oz, dx, dy, dz);
   double bt = 1e300;
   int32_t bid = -1;
   stack[0] = 0;
@@ -240,8 +262,18 @@ __device__ __forceinline__ void bvh_nearest(const SceneView& b, double ox, doubl
     } else {
       int32_t c0 = b.bleft[node], c1 = b.bright[node];
       double n0, f0, n1, f1;
-      slab(b.blo + 3 * c0, b.bhi + 3 * c0, ox, oy, oz, ix, iy, iz, &n0, &f0);
-      slab(b.blo + 3 * c1, b.bhi + 3 * c1, ox, oy, oz, ix, iy, iz, &n1, &f1);
+      if (b.bbox32) {  // padded fp32 boxes: conservative entry / exit distances
+        float a0, a1, e0, e1;
+        slab32(b.bbox32 + 2 * c0, rs, &a0, &e0);
+        slab32(b.bbox32 + 2 * c1, rs, &a1, &e1);
+        n0 = a0;
+        n1 = a1;
+        f0 = (double)e0 * (1.0 + 1e-6);
+        f1 = (double)e1 * (1.0 + 1e-6);
+      } else {
+        slab(b.blo + 3 * c0, b.bhi + 3 * c0, ox, oy, oz, ix, iy, iz, &n0, &f0);
+        slab(b.blo + 3 * c1, b.bhi + 3 * c1, ox, oy, oz, ix, iy, iz, &n1, &f1);
+      }
       double d0 = (f0 >= n0 && n0 <= bt && f0 >= tmin) ? n0 : 1e301;
       double d1 = (f1 >= n1 && n1 <= bt && f1 >= tmin) ? n1 : 1e301;
       if (d0 > d1) {
@@ -274,14 +306,22 @@ __device__ __forceinline__ bool bvh_occluded(const SceneView& b, double ox, doub
                                              double tmax) {
   int32_t stack[64];
   double ix = 1.0 / dx, iy = 1.0 / dy, iz = 1.0 / dz;
+  const RaySlab rs = make_ray_slab(ox, oy, oz, dx, dy, dz);
+  const float tmax32 = (float)tmax * (1.0f + 1e-6f), tmin32 = (float)tmin * (1.0f - 1e-6f);
   stack[0] = 0;
   int sp = 1;
   while (sp > 0) {
     --sp;
     int32_t node = stack[sp];
-    double n, f;
-    slab(b.blo + 3 * node, b.bhi + 3 * node, ox, oy, oz, ix, iy, iz, &n, &f);
-    if (!(f >= n && n <= tmax && f >= tmin)) continue;
+    if (b.bbox32) {
+      float n, f;
+      slab32(b.bbox32 + 2 * node, rs, &n, &f);
+      if (!(f * (1.0f + 1e-6f) >= n && n <= tmax32 && f * (1.0f + 1e-6f) >= tmin32)) continue;
+    } else {
+      double n, f;
+      slab(b.blo + 3 * node, b.bhi + 3 * node, ox, oy, oz, ix, iy, iz, &n, &f);
+      if (!(f >= n && n <= tmax && f >= tmin)) continue;
+    }
     int32_t cnt = b.bcount[node];
     if (cnt > 0) {
       int32_t first = b.bleft[node];
