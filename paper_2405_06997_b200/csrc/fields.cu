@@ -393,6 +393,7 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
       out.total[b] = tot;
       tot_sh = tot;
       double run = rs[0];
+#pragma unroll 8
       for (int j = 1; j < N; ++j) {
         run = __dadd_rn(run, rs[j]);
         rs[j] = run;
