@@ -391,47 +391,45 @@ __device__ __forceinline__ void make_tri_bin_part(const SceneView& s, int t, int
     B.qz = tx * e1[1] - ty * e1[0];
     B.ts0 = e2[0] * B.qx + e2[1] * B.qy + e2[2] * B.qz;
     // |ts0| = |tvec . (e1 x e2)| = plane distance * |n|
-    const double nl = sqrt(B.nx * B.nx + B.ny * B.ny + B.nz * B.nz);
-    B.pnx = (float)(B.nx / nl);
-    B.pny = (float)(B.ny / nl);
-    B.pnz = (float)(B.nz / nl);
-    B.flat = fabs(B.ts0) < 1e-5 * s.ray_eps * nl ? 1 : 0;
+    const double n2 = B.nx * B.nx + B.ny * B.ny + B.nz * B.nz;
+    const double inl = rsqrt(n2);
+    B.pnx = (float)(B.nx * inl);
+    B.pny = (float)(B.ny * inl);
+    B.pnz = (float)(B.nz * inl);
+    const double fl = 1e-5 * s.ray_eps;
+    B.flat = B.ts0 * B.ts0 < fl * fl * n2 ? 1 : 0;
   }
-  // unit directions from o to the three vertices
-  double w[3][3];
+  // directions from o to the three vertices (unnormalised: the thresholds
+  // below are the unit-vector tests |a^ x b^| > 1e-9 and |n^ . c^| >= 1e-9
+  // restated on squared lengths, so no square roots or divisions)
+  double w[3][3], l2[3];
   bool degenerate = false;
+  const double dl = 1e-9 * s.ray_eps;
   for (int k = 0; k < 3; ++k) {
-    double px = v0[0] + (k == 1 ? e1[0] : (k == 2 ? e2[0] : 0.0)) - ox;
-    double py = v0[1] + (k == 1 ? e1[1] : (k == 2 ? e2[1] : 0.0)) - oy;
-    double pz = v0[2] + (k == 1 ? e1[2] : (k == 2 ? e2[2] : 0.0)) - oz;
-    double len = sqrt(px * px + py * py + pz * pz);
-    if (!(len > 1e-9 * s.ray_eps)) degenerate = true;
-    double inv = 1.0 / len;
-    w[k][0] = px * inv;
-    w[k][1] = py * inv;
-    w[k][2] = pz * inv;
+    w[k][0] = v0[0] + (k == 1 ? e1[0] : (k == 2 ? e2[0] : 0.0)) - ox;
+    w[k][1] = v0[1] + (k == 1 ? e1[1] : (k == 2 ? e2[1] : 0.0)) - oy;
+    w[k][2] = v0[2] + (k == 1 ? e1[2] : (k == 2 ? e2[2] : 0.0)) - oz;
+    l2[k] = w[k][0] * w[k][0] + w[k][1] * w[k][1] + w[k][2] * w[k][2];
+    if (!(l2[k] > dl * dl)) degenerate = true;
   }
   B.plane_ok[e] = 0;
   if (degenerate) return;
   // the plane through o and edge e, oriented toward the opposite vertex
+  const int e1i = (e + 1) % 3, e2i = (e + 2) % 3;
   const double* a = w[e];
-  const double* b = w[(e + 1) % 3];
-  const double* c = w[(e + 2) % 3];
+  const double* b = w[e1i];
+  const double* c = w[e2i];
   double nx = a[1] * b[2] - a[2] * b[1];
   double ny = a[2] * b[0] - a[0] * b[2];
   double nz = a[0] * b[1] - a[1] * b[0];
-  double len = sqrt(nx * nx + ny * ny + nz * nz);
-  if (!(len > 1e-9)) return;
-  nx /= len;
-  ny /= len;
-  nz /= len;
-  double side = nx * c[0] + ny * c[1] + nz * c[2];
-  if (fabs(side) < 1e-9) return;  // origin (nearly) in the triangle's plane
-  if (side < 0.0) {
-    nx = -nx;
-    ny = -ny;
-    nz = -nz;
-  }
+  const double m2 = nx * nx + ny * ny + nz * nz;
+  if (!(m2 > 1e-18 * l2[e] * l2[e1i])) return;
+  const double side = nx * c[0] + ny * c[1] + nz * c[2];
+  if (!(side * side >= 1e-18 * m2 * l2[e2i])) return;  // o (nearly) in the triangle's plane
+  const double inv = side < 0.0 ? -rsqrt(m2) : rsqrt(m2);
+  nx *= inv;
+  ny *= inv;
+  nz *= inv;
   float* nb = &B.n0x + 3 * e;
   nb[0] = (float)nx;
   nb[1] = (float)ny;
