@@ -59,6 +59,8 @@ def parse():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--cpu-seconds", type=float, default=20.0,
                    help="budget of the CPU-baseline sample")
+    p.add_argument("--ref-seconds", type=float, default=None,
+                   help="--impl reference: CPU sample per step (default min(10, 150 / (W + K)) s)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     a = p.parse_args()
@@ -424,7 +426,7 @@ def run_reference(args):
                           seed=args.seed, blur_sigma=1.0, epsilon=1e-2)
     wl = OR.CpuWorkload(sc, args.svo_res, cfg, seed=args.seed)
     n_paths = args.width * args.height
-    budget = min(10.0, 150.0 / max(1, args.warmup + args.steps))
+    budget = args.ref_seconds or min(10.0, 150.0 / max(1, args.warmup + args.steps))
     vals, ms = [], []
     for step in range(args.warmup + args.steps):
         r = wl.time_pass(n_paths, budget, seed=step)
