@@ -157,7 +157,10 @@ __global__ void __launch_bounds__(kSortBlock) k_sort_scatter(
     int64_t nblocks, const uint32_t* __restrict__ offs, const uint32_t* __restrict__ dbase) {
   __shared__ uint32_t whist[kSortWarps][256];
   __shared__ uint32_t goff[256];
+  __shared__ uint32_t dstart[256];
   __shared__ uint32_t sw[kSortBlock / 32 + 1];
+  __shared__ uint64_t sk[kSortTile];
+  __shared__ uint32_t sv[kSortTile];
   const int64_t n = dev_count(n_max, n_dev);
   if ((int64_t)blockIdx.x * kSortTile >= n) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -188,24 +191,40 @@ __global__ void __launch_bounds__(kSortBlock) k_sort_scatter(
     r[c] = pre + __popc(peers & lt);
   }
   __syncthreads();
-  {
-    uint32_t run = 0;
-    for (int w = 0; w < kSortWarps; ++w) {
-      uint32_t t = whist[w][threadIdx.x];
-      whist[w][threadIdx.x] = run;
-      run += t;
-    }
+  // per digit (thread t = digit t): warp-exclusive offsets within the digit,
+  // then the block-local start of each digit
+  uint32_t run = 0;
+  for (int w = 0; w < kSortWarps; ++w) {
+    uint32_t t = whist[w][threadIdx.x];
+    whist[w][threadIdx.x] = run;
+    run += t;
   }
+  __syncthreads();  // sw is reused by the scan below
+  const uint32_t lstart = block_exclusive_scan<kSortBlock>(run, sw, nullptr);
+  dstart[threadIdx.x] = lstart;
+  goff[threadIdx.x] -= lstart;  // global position = goff[d] + block-local position
   __syncthreads();
+  // reorder the tile in shared memory by digit (stable), then write each
+  // digit's run with consecutive threads: coalesced stores instead of 256-way
+  // scattered ones
 #pragma unroll
   for (int c = 0; c < kSortIpt; ++c) {
     int64_t i = wbase + c * 32 + lane;
     if (i < n) {
       uint32_t dig = (uint32_t)((k[c] >> shift) & 255u);
-      uint32_t pos = goff[dig] + whist[warp][dig] + r[c];
-      kout[pos] = k[c];
-      vout[pos] = v[c];
+      uint32_t lp = dstart[dig] + whist[warp][dig] + r[c];
+      sk[lp] = k[c];
+      sv[lp] = v[c];
     }
+  }
+  __syncthreads();
+  const int64_t tbase = (int64_t)blockIdx.x * kSortTile;
+  const int valid = (int)(n - tbase < kSortTile ? n - tbase : kSortTile);
+  for (int e = threadIdx.x; e < valid; e += kSortBlock) {
+    const uint64_t key = sk[e];
+    const uint32_t pos = goff[(uint32_t)((key >> shift) & 255u)] + (uint32_t)e;
+    kout[pos] = key;
+    vout[pos] = sv[e];
   }
 }
 
