@@ -14,17 +14,24 @@ namespace wfpg {
 // commutes with rounding), so the per-level squares come from one product and
 // exact multiplications by 4 — same bits as the reference's divisions.
 __device__ __forceinline__ int best_cone_level(double size, int depth, double area) {
-  double s2 = ldexp(size * size, -2 * depth);
-  double bd = fabs(s2 - area);
-  int best = depth;
-  for (int lv = depth - 1; lv >= 0; --lv) {
-    s2 *= 4.0;
-    double diff = fabs(s2 - area);
+  // The error |s0 * 4^-lv - area| falls while s0 * 4^-lv >= area and rises
+  // after, so the integer optimum is floor or ceil of x = log4(s0 / area).
+  // An fp32 estimate of x (error far below 1) brackets it; the candidates
+  // are then compared exactly, deepest first with strict '<' (deeper wins
+  // ties), which is what the level-by-level scan from the leaf level returns.
+  const double s0 = size * size;
+  const float x = 0.5f * (__log2f((float)s0) - __log2f((float)area));
+  const int c = (int)floorf(fminf(fmaxf(x, -4.0f), 64.0f));
+  const int lo = min(max(c - 1, 0), depth), hi = min(max(c + 2, 0), depth);
+  // exact power-of-two scaling: s0 * 2^(-2 lv)
+  int best = hi;
+  double bd = fabs(__dmul_rn(s0, __longlong_as_double((long long)(1023 - 2 * hi) << 52)) - area);
+  for (int lv = hi - 1; lv >= lo; --lv) {
+    const double diff =
+        fabs(__dmul_rn(s0, __longlong_as_double((long long)(1023 - 2 * lv) << 52)) - area);
     if (diff < bd) {
       bd = diff;
       best = lv;
-    } else if (diff > bd) {
-      break;  // past the minimum: shallower levels only grow (unimodal)
     }
   }
   return best;
