@@ -439,11 +439,13 @@ def run_reference(args):
     cb.pop("pass_seconds", None)
     print(json.dumps({
         "impl": "reference", "metric": "path samples/sec (guided wavefront pass)", "value": v,
-        "unit": "path samples/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "unit": "path samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": n_paths / v * 1e3 if v else None, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{SCENES[args.scene][2]} {args.width}x{args.height}, 1 spp guided pass, "
-                               f"SVO depth {depth}, D={args.depth}"},
+                               f"SVO depth {depth}, D={args.depth}",
+                   "host": "CPU only, rank 0's host cores; n_gpus mirrors the B200 arm "
+                           "this line is paired with"},
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "path samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0}}), flush=True)
