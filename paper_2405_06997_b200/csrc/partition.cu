@@ -73,7 +73,7 @@ __global__ void k_part_ascend(const int32_t* __restrict__ counter,
                               const int32_t* __restrict__ parent, const int32_t* __restrict__ start,
                               const int8_t* __restrict__ start_lev, int64_t n_max,
                               const int32_t* __restrict__ n_dev, int l_min, int c_ray,
-                              uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+                              uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
   const int64_t n = dev_count(n_max, n_dev);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -84,7 +84,7 @@ __global__ void k_part_ascend(const int32_t* __restrict__ counter,
       a = parent[a];
       --lev;
     }
-    keys[i] = (uint64_t)a;
+    keys[i] = (uint32_t)a;
     vals[i] = (uint32_t)i;
   }
 }
@@ -103,7 +103,7 @@ __global__ void k_part_clear(int32_t* __restrict__ counter, const int32_t* __res
   }
 }
 
-__global__ void k_part_flags(const uint64_t* __restrict__ keys, int64_t n_max,
+__global__ void k_part_flags(const uint32_t* __restrict__ keys, int64_t n_max,
                              const int32_t* __restrict__ n_dev, uint32_t* __restrict__ flags) {
   const int64_t n = dev_count(n_max, n_dev);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -111,7 +111,7 @@ __global__ void k_part_flags(const uint64_t* __restrict__ keys, int64_t n_max,
     flags[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1u : 0u;
 }
 
-__global__ void k_part_bins(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+__global__ void k_part_bins(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
                             const uint32_t* __restrict__ flags, const uint32_t* __restrict__ scan,
                             const int32_t* __restrict__ path_idx, int64_t n_max,
                             const int32_t* __restrict__ n_dev, int64_t cap,
@@ -172,7 +172,7 @@ int partition_spatial(const SvoView& v, int32_t* counter, const int32_t* parent,
   }
   int32_t* start = ws.take<int32_t>(n_max);
   int8_t* lev = ws.take<int8_t>(n_max);
-  uint64_t* keys = ws.take<uint64_t>(n_max);
+  uint32_t* keys = ws.take<uint32_t>(n_max);  // node ids < 2^31
   uint32_t* vals = ws.take<uint32_t>(n_max);
   uint32_t* flags = ws.take<uint32_t>(n_max + 1);
   uint32_t* scan = ws.take<uint32_t>(n_max + 1);

@@ -104,7 +104,8 @@ constexpr int kSortBlock = kSortWarps * 32;
 constexpr int kSortIpt = 8;  // 32-item chunks per warp
 constexpr int kSortTile = kSortBlock * kSortIpt;
 
-__global__ void __launch_bounds__(kSortBlock) k_sort_hist(const uint64_t* __restrict__ keys,
+template <typename KT>
+__global__ void __launch_bounds__(kSortBlock) k_sort_hist(const KT* __restrict__ keys,
                                                           int64_t n_max,
                                                           const int32_t* __restrict__ n_dev,
                                                           int shift, int64_t nblocks,
@@ -151,15 +152,16 @@ __global__ void __launch_bounds__(kOffThreads) k_sort_offsets(uint32_t* __restri
   if (threadIdx.x == 0) dtot[blockIdx.x] = total;
 }
 
+template <typename KT>
 __global__ void __launch_bounds__(kSortBlock) k_sort_scatter(
-    const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint64_t* __restrict__ kout,
+    const KT* __restrict__ kin, const uint32_t* __restrict__ vin, KT* __restrict__ kout,
     uint32_t* __restrict__ vout, int64_t n_max, const int32_t* __restrict__ n_dev, int shift,
     int64_t nblocks, const uint32_t* __restrict__ offs, const uint32_t* __restrict__ dbase) {
   __shared__ uint32_t whist[kSortWarps][256];
   __shared__ uint32_t goff[256];
   __shared__ uint32_t dstart[256];
   __shared__ uint32_t sw[kSortBlock / 32 + 1];
-  __shared__ uint64_t sk[kSortTile];
+  __shared__ KT sk[kSortTile];
   __shared__ uint32_t sv[kSortTile];
   const int64_t n = dev_count(n_max, n_dev);
   if ((int64_t)blockIdx.x * kSortTile >= n) return;
@@ -171,7 +173,7 @@ __global__ void __launch_bounds__(kSortBlock) k_sort_scatter(
   __syncthreads();
 
   const int64_t wbase = (int64_t)blockIdx.x * kSortTile + (int64_t)warp * 32 * kSortIpt;
-  uint64_t k[kSortIpt];
+  KT k[kSortIpt];
   uint32_t v[kSortIpt];
   uint32_t r[kSortIpt];
   const uint32_t lt = lanemask_lt();
@@ -221,15 +223,16 @@ __global__ void __launch_bounds__(kSortBlock) k_sort_scatter(
   const int64_t tbase = (int64_t)blockIdx.x * kSortTile;
   const int valid = (int)(n - tbase < kSortTile ? n - tbase : kSortTile);
   for (int e = threadIdx.x; e < valid; e += kSortBlock) {
-    const uint64_t key = sk[e];
+    const KT key = sk[e];
     const uint32_t pos = goff[(uint32_t)((key >> shift) & 255u)] + (uint32_t)e;
     kout[pos] = key;
     vout[pos] = sv[e];
   }
 }
 
-__global__ void k_copy_pairs(const uint64_t* __restrict__ ks, const uint32_t* __restrict__ vs,
-                             uint64_t* __restrict__ kd, uint32_t* __restrict__ vd, int64_t n_max,
+template <typename KT>
+__global__ void k_copy_pairs(const KT* __restrict__ ks, const uint32_t* __restrict__ vs,
+                             KT* __restrict__ kd, uint32_t* __restrict__ vd, int64_t n_max,
                              const int32_t* __restrict__ n_dev) {
   const int64_t n = dev_count(n_max, n_dev);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -246,11 +249,12 @@ size_t sort_ws_bytes(int64_t n_max) {
          align_up(sizeof(uint32_t) * 256 * nb) + align_up(sizeof(uint32_t) * 256) + 1024;
 }
 
-int sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n_max, const int32_t* n_dev, int key_bits,
-               Arena& ws, cudaStream_t st) {
+template <typename KT>
+static int sort_pairs_t(KT* keys, uint32_t* vals, int64_t n_max, const int32_t* n_dev, int key_bits,
+                        Arena& ws, cudaStream_t st) {
   if (n_max <= 1) return WFPG_OK;
   int64_t nb = ceil_div(n_max, kSortTile);
-  uint64_t* k2 = ws.take<uint64_t>(n_max);
+  KT* k2 = ws.take<KT>(n_max);
   uint32_t* v2 = ws.take<uint32_t>(n_max);
   uint32_t* hist = ws.take<uint32_t>(256 * nb);
   uint32_t* dbase = ws.take<uint32_t>(256);
@@ -259,20 +263,20 @@ int sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n_max, const int32_t* n_d
     return WFPG_ERR_WORKSPACE;
   }
   int passes = (key_bits + 7) / 8;
-  uint64_t* ka = keys;
+  KT* ka = keys;
   uint32_t* va = vals;
-  uint64_t* kb = k2;
+  KT* kb = k2;
   uint32_t* vb = v2;
   for (int p = 0; p < passes; ++p) {
     int shift = 8 * p;
-    k_sort_hist<<<(unsigned)nb, kSortBlock, 0, st>>>(ka, n_max, n_dev, shift, nb, hist);
+    k_sort_hist<KT><<<(unsigned)nb, kSortBlock, 0, st>>>(ka, n_max, n_dev, shift, nb, hist);
     WFPG_CHECK_LAUNCH("k_sort_hist");
     k_sort_offsets<<<256, kOffThreads, 0, st>>>(hist, n_max, n_dev, nb, dbase);
     WFPG_CHECK_LAUNCH("k_sort_offsets");
-    k_sort_scatter<<<(unsigned)nb, kSortBlock, 0, st>>>(ka, va, kb, vb, n_max, n_dev, shift, nb,
+    k_sort_scatter<KT><<<(unsigned)nb, kSortBlock, 0, st>>>(ka, va, kb, vb, n_max, n_dev, shift, nb,
                                                          hist, dbase);
     WFPG_CHECK_LAUNCH("k_sort_scatter");
-    uint64_t* tk = ka;
+    KT* tk = ka;
     ka = kb;
     kb = tk;
     uint32_t* tv = va;
@@ -282,10 +286,20 @@ int sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n_max, const int32_t* n_d
   if (ka != keys) {
     // odd number of passes: copy the live prefix back
     int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_max, 256), kNumSMs * 8));
-    k_copy_pairs<<<grid, 256, 0, st>>>(ka, va, keys, vals, n_max, n_dev);
+    k_copy_pairs<KT><<<grid, 256, 0, st>>>(ka, va, keys, vals, n_max, n_dev);
     WFPG_CHECK_LAUNCH("k_copy_pairs");
   }
   return WFPG_OK;
+}
+
+
+int sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n_max, const int32_t* n_dev, int key_bits,
+               Arena& ws, cudaStream_t st) {
+  return sort_pairs_t(keys, vals, n_max, n_dev, key_bits, ws, st);
+}
+int sort_pairs(uint32_t* keys, uint32_t* vals, int64_t n_max, const int32_t* n_dev, int key_bits,
+               Arena& ws, cudaStream_t st) {
+  return sort_pairs_t(keys, vals, n_max, n_dev, key_bits < 32 ? key_bits : 32, ws, st);
 }
 
 }  // namespace wfpg

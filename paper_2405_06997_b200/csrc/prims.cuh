@@ -14,6 +14,8 @@ size_t sort_ws_bytes(int64_t n_max);
 // Stable LSD radix sort of (key, value) pairs on the low key_bits bits, in place.
 int sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n_max, const int32_t* n_dev,
                int key_bits, Arena& ws, cudaStream_t st);
+int sort_pairs(uint32_t* keys, uint32_t* vals, int64_t n_max, const int32_t* n_dev,
+               int key_bits, Arena& ws, cudaStream_t st);
 
 inline int bits_for(uint64_t max_value) {
   int b = 0;
