@@ -378,14 +378,24 @@ __device__ __forceinline__ int32_t descend_coords(const uint2* __restrict__ desc
 __device__ __forceinline__ int32_t descend_view(const SvoView& v, int32_t qx, int32_t qy,
                                                 int32_t qz, int32_t max_level, bool* present,
                                                 int32_t* reached_level) {
-  if (v.top && max_level >= v.top_level) {
+  if (v.top && max_level >= v.top_level - 2) {
     const int T = v.top_level, sh = v.depth - T;
     const uint32_t cell = ((uint32_t)(qx >> sh) << (2 * T)) | ((uint32_t)(qy >> sh) << T) |
                           (uint32_t)(qz >> sh);
     const uint2 e = __ldg(&v.top[cell]);
+    const int32_t lv = (int32_t)(e.y & 0xFFu);  // deepest materialised level <= T
+    if (max_level <= lv) {
+      // shallower target: its node is an ancestor of the indexed one (one
+      // or two parent links instead of a descent from the root)
+      int32_t node = (int32_t)e.x;
+      for (int l = lv; l > max_level; --l) node = __ldg(&v.parent[node]);
+      *present = true;
+      *reached_level = max_level;
+      return node;
+    }
     if (!(e.y >> 31)) {
       *present = false;
-      *reached_level = (int32_t)(e.y & 0xFFu);
+      *reached_level = lv;
       return (int32_t)e.x;
     }
     return descend_coords(v.desc, v.depth, qx, qy, qz, max_level, present, reached_level,
