@@ -142,6 +142,11 @@ typedef struct wfpg_paths {
   double* rec_T;             /* (P,D+1,3) */
   double* emit_le;           /* (P,3) */
   int32_t* emit_depth;       /* (P,) */
+  /* Optional (P,) deepest record slot written (0 = camera only).  When set,
+   * the pass does not zero rec_pos / rec_T (2 x 24 (D+1) bytes per path):
+   * slots above n_rec hold stale values, which readers mask (the exitance
+   * update only reads slots <= emit_depth <= n_rec).  NULL: zeroed slots. */
+  uint8_t* n_rec;
 } wfpg_paths;
 
 /* Per-depth guide tables: guiding.py:254-309 (GuideTables).  The B200 layout

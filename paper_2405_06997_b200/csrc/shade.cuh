@@ -245,6 +245,7 @@ struct PathsView {
   double* rec_T;
   double* emit_le;
   int32_t* emit_depth;
+  uint8_t* n_rec;  // optional: deepest record slot written
   int32_t rec_depths;
 };
 

@@ -58,7 +58,8 @@ __global__ void k_init_paths(CameraView c, PathsView P, int64_t n_paths, int64_t
     P.alive[p] = 1;
     P.prev_pdf[p] = -1.0;
     P.emit_depth[p] = 0;
-    double* rp = P.rec_pos + (int64_t)p * P.rec_depths * 3;  // zeroed by the launcher
+    if (P.n_rec) P.n_rec[p] = 0;
+    double* rp = P.rec_pos + (int64_t)p * P.rec_depths * 3;  // zeroed by the launcher unless n_rec
     rp[0] = c.pos[0];
     rp[1] = c.pos[1];
     rp[2] = c.pos[2];
@@ -135,6 +136,7 @@ __device__ void shade_path(int64_t p, int depth, const SceneView& sa, const Guid
     P.rec_T[rb] = beta[0];
     P.rec_T[rb + 1] = beta[1];
     P.rec_T[rb + 2] = beta[2];
+    if (P.n_rec && P.n_rec[p] < depth) P.n_rec[p] = (uint8_t)depth;
   }
   const int mid = sa.tri_mat[tri];
   const int kind = sa.mat_kind[mid];
@@ -410,8 +412,10 @@ int launch_camera_init(const CameraView& c, const PathsView& P, int64_t n_paths,
                        cudaStream_t st) {
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_paths, 256), kNumSMs * 8));
   size_t rec_bytes = sizeof(double) * 3 * (size_t)P.rec_depths * (size_t)n_paths;
-  WFPG_CUDA(cudaMemsetAsync(P.rec_pos, 0, rec_bytes, st));
-  WFPG_CUDA(cudaMemsetAsync(P.rec_T, 0, rec_bytes, st));
+  if (!P.n_rec) {  // with n_rec, slots above it are masked by the readers
+    WFPG_CUDA(cudaMemsetAsync(P.rec_pos, 0, rec_bytes, st));
+    WFPG_CUDA(cudaMemsetAsync(P.rec_T, 0, rec_bytes, st));
+  }
   k_init_paths<<<grid, 256, 0, st>>>(c, P, n_paths, n_pix, n_img, pix0, sample0, seed);
   WFPG_CHECK_LAUNCH("k_init_paths");
   return WFPG_OK;
@@ -468,6 +472,7 @@ PathsView make_paths_view(const wfpg_paths* p) {
   v.alive = p->alive;
   v.prev_pdf = p->prev_pdf;
   v.rec_pos = p->rec_pos;
+  v.n_rec = p->n_rec;
   v.rec_T = p->rec_T;
   v.emit_le = p->emit_le;
   v.emit_depth = p->emit_depth;

@@ -59,6 +59,9 @@ _STATE = {
     "alive": (np.uint8, lambda d: ()), "prev_pdf": (np.float64, lambda d: ()),
     "rec_pos": (np.float64, lambda d: (d + 1, 3)), "rec_T": (np.float64, lambda d: (d + 1, 3)),
     "emit_le": (np.float64, lambda d: (3,)), "emit_depth": (np.int32, lambda d: ()),
+    # deepest record slot written this pass: slots above it are stale on the
+    # device (the pass does not re-zero them) and read back as zeros
+    "n_rec": (np.uint8, lambda d: ()),
 }
 
 
@@ -90,6 +93,9 @@ class PathState:
     def __getattr__(self, name):
         if name in _STATE and "dev" in self.__dict__:
             a = _dev.download(self.dev[name])
+            if name in ("rec_pos", "rec_T"):
+                n_rec = _dev.download(self.dev["n_rec"]).astype(np.int64)
+                a[np.arange(a.shape[1])[None, :] > n_rec[:, None]] = 0.0
             return a.astype(bool) if name == "alive" else a
         raise AttributeError(name)
 
