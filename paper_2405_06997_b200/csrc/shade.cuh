@@ -156,12 +156,20 @@ __device__ __forceinline__ void cell_of(int n, double dx, double dy, double dz, 
 }
 
 // pdf_plain_dir (_kernels.pyx:876-885): pdftab = vals * (n^2/4pi) / total
+__device__ __forceinline__ double pdf_plain_cell(const GuideView& g, int slot, int i, int j) {
+  double v = g.vals[((int64_t)slot * g.n + j) * g.n + i];
+  return __ddiv_rn(__dmul_rn(v, g.pdf_scale), g.total[slot]);
+}
 __device__ __forceinline__ double pdf_plain(const GuideView& g, int slot, double dx, double dy,
                                             double dz) {
   int i, j;
   cell_of(g.n, dx, dy, dz, &i, &j);
-  double v = g.vals[((int64_t)slot * g.n + j) * g.n + i];
-  return __ddiv_rn(__dmul_rn(v, g.pdf_scale), g.total[slot]);
+  return pdf_plain_cell(g, slot, i, j);
+}
+
+// L2 prefetch of a guide-table entry a later lookup will read
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
 // pdf_product_dir (_kernels.pyx:888-902)

@@ -247,6 +247,13 @@ __device__ void shade_path(int64_t p, int depth, const SceneView& sa, const Guid
       double cos_s = nsx * lx + nsy * ly + nsz * lz;
       if (cos_l > 1e-9 && cos_s > 0.0 && !grazing && le[0] + le[1] + le[2] > 0.0) {
         double pl = dist * dist / (sa.em_area * cos_l);
+        // the guide-table entry of the light direction (plain guiding) is
+        // requested before the shadow ray so its DRAM latency overlaps it
+        int nci = 0, ncj = 0;
+        if (guided && g.mode == 1) {
+          cell_of(g.n, lx, ly, lz, &nci, &ncj);
+          prefetch_l2(g.vals + ((int64_t)slot * g.n + ncj) * g.n + nci);
+        }
         // any-hit: brute force over the triangles in shared memory for small
         // scenes (the hit / no-hit answer does not depend on the traversal)
         bool blocked = smt ? brute_occluded(smt, sa.n_tris, px, py, pz, lx, ly, lz, sa.ray_eps,
@@ -256,7 +263,7 @@ __device__ void shade_path(int64_t p, int depth, const SceneView& sa, const Guid
         if (!blocked) {
           double p_cont;
           if (guided) {
-            double pg = g.mode == 1 ? pdf_plain(g, slot, lx, ly, lz)
+            double pg = g.mode == 1 ? pdf_plain_cell(g, slot, nci, ncj)
                                     : pdf_product(g, slot, upper, upsum, lx, ly, lz);
             p_cont = 0.5 * pg + 0.5 * (cos_s / WFPG_PI);
           } else {
