@@ -235,17 +235,17 @@ __device__ __forceinline__ void bvh_nearest(const SceneView& b, double ox, doubl
                                             double dx, double dy, double dz, double tmin,
                                             double* best_t, int32_t* best_tri) {
   int32_t stack[64];
-  double dstack[64];
+  float dstack[64];  // entry distances rounded down: the skip test stays conservative
   double ix = 1.0 / dx, iy = 1.0 / dy, iz = 1.0 / dz;
   const RaySlab rs = make_ray_slab(ox, oy, oz, dx, dy, dz);
   double bt = 1e300;
   int32_t bid = -1;
   stack[0] = 0;
-  dstack[0] = 0.0;
+  dstack[0] = 0.0f;
   int sp = 1;
   while (sp > 0) {
     --sp;
-    if (dstack[sp] >= bt) continue;
+    if ((double)dstack[sp] >= bt) continue;
     int32_t node = stack[sp];
     int32_t cnt = b.bcount[node];
     if (cnt > 0) {
@@ -286,12 +286,12 @@ __device__ __forceinline__ void bvh_nearest(const SceneView& b, double ox, doubl
       }
       if (d1 < 1e301 && sp < 64) {
         stack[sp] = c1;
-        dstack[sp] = d1;
+        dstack[sp] = __double2float_rd(d1);
         ++sp;
       }
       if (d0 < 1e301 && sp < 64) {
         stack[sp] = c0;
-        dstack[sp] = d0;
+        dstack[sp] = __double2float_rd(d0);
         ++sp;
       }
     }
