@@ -38,6 +38,7 @@ def main():
     ap.add_argument("--scene", default="c2", choices=list(SCENES))
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--height", type=int, default=1080)
+    ap.add_argument("--product", action="store_true", help="product guiding in the guided pass")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     from oracle import render as OR
@@ -54,10 +55,11 @@ def main():
     osc = OR.Scene(sc)
     osvo = OR.Svo.from_scene(sc, res, 0)
     t_build = time.perf_counter() - t0
-    out = {"bench": "parity_full", "scene": a.scene, "image": [a.width, a.height],
+    out = {"bench": "parity_full", "scene": a.scene, "product": a.product,
+           "image": [a.width, a.height],
            "svo_resolution": res, "oracle_build_s": t_build}
     for tag, sample, g in (("pt_first", 0, 0), ("guided", 1, 4)):
-        kw = dict(base, guided_depths=g)
+        kw = dict(base, guided_depths=g, product=bool(a.product and g))
         cfg = wavefront.GuidingConfig(**kw)
         frame, st = wavefront.render_pass(sc, tree, cfg, [sample])
         state = wavefront._RUNNERS[next(iter(wavefront._RUNNERS))].state
