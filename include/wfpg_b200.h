@@ -315,6 +315,18 @@ int wfpg_svo_refresh_leaves(wfpg_svo* svo, const int32_t* leaf, int64_t n, uint8
 
 /* Fill svo->top_index (see wfpg_svo) from the node arrays; top_level in
  * [1, min(depth, 7)]; bytes = wfpg_svo_top_index_bytes(top_level). */
+/* Device BVH build for scenes too large for the host
+ * build (bvh.py:33-119): linear BVH over 63-bit Morton codes of the triangle
+ * box centres (Karras 2012), one triangle per leaf, written in the host
+ * BVH's flattened layout (2T-1 nodes, root 0; lo / hi (N,3), left / right /
+ * count (N,), order (T,), padded fp32 boxes (N,8) as wfpg_scene.bvh_box_f32).
+ * Reads scene->v0/v1/v2, n_tris and the host bbox.  Nearest hits equal the
+ * host BVH's except for exact ties. */
+size_t wfpg_bvh_build_workspace_bytes(int64_t n_tris);
+int wfpg_bvh_build_device(const wfpg_scene* scene, double* lo, double* hi, int32_t* left,
+                          int32_t* right, int32_t* count, int32_t* order, float* box_f32,
+                          void* workspace, size_t ws_bytes, void* stream);
+
 size_t wfpg_svo_top_index_bytes(int32_t top_level);
 int wfpg_svo_build_top_index(wfpg_svo* svo, void* stream);
 
