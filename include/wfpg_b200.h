@@ -321,7 +321,8 @@ int wfpg_svo_refresh_leaves(wfpg_svo* svo, const int32_t* leaf, int64_t n, uint8
  * BVH's flattened layout (2T-1 nodes, root 0; lo / hi (N,3), left / right /
  * count (N,), order (T,), padded fp32 boxes (N,8) as wfpg_scene.bvh_box_f32).
  * Reads scene->v0/v1/v2, n_tris and the host bbox.  Nearest hits equal the
- * host BVH's except for exact ties. */
+ * host BVH's except for exact ties.  Synchronises the stream; fails with
+ * WFPG_ERR_ARG when the tree is deeper than the traversal stacks allow (62). */
 size_t wfpg_bvh_build_workspace_bytes(int64_t n_tris);
 int wfpg_bvh_build_device(const wfpg_scene* scene, double* lo, double* hi, int32_t* left,
                           int32_t* right, int32_t* count, int32_t* order, float* box_f32,

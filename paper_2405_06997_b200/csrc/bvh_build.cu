@@ -131,6 +131,20 @@ __global__ void k_lbvh_boxes(const double* __restrict__ v0, const double* __rest
   }
 }
 
+// tree depth (longest leaf-to-root walk): the traversals keep 64-entry stacks
+__global__ void k_lbvh_depth(const int32_t* __restrict__ parent, int n, int32_t* __restrict__ out) {
+  int deepest = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int node = n - 1 + i, d = 0;
+    while (node != 0) {
+      node = parent[node];
+      ++d;
+    }
+    deepest = max(deepest, d);
+  }
+  atomicMax(out, deepest);
+}
+
 }  // namespace wfpg
 
 using namespace wfpg;
@@ -142,6 +156,7 @@ extern "C" size_t wfpg_bvh_build_workspace_bytes(int64_t n_tris) {
   a.take<uint32_t>(n);
   a.take<int32_t>(2 * n);
   a.take<uint32_t>(n);
+  a.take<int32_t>(1);
   return a.off + sort_ws_bytes(n) + 1024;
 }
 
@@ -161,6 +176,7 @@ extern "C" int wfpg_bvh_build_device(const wfpg_scene* scene, double* lo, double
   uint32_t* idx = a.take<uint32_t>(n);
   int32_t* parent = a.take<int32_t>(2 * (int64_t)n);
   uint32_t* ticket = a.take<uint32_t>(n);
+  int32_t* depth_dev = a.take<int32_t>(1);
   if (!a.ok()) {
     set_error("bvh build: workspace too small");
     return WFPG_ERR_WORKSPACE;
@@ -186,5 +202,15 @@ extern "C" int wfpg_bvh_build_device(const wfpg_scene* scene, double* lo, double
   k_lbvh_boxes<<<grid, 256, 0, st>>>(scene->v0, scene->v1, scene->v2, idx, n, left, right, parent,
                                      ticket, lo, hi, box_f32, order, pad0);
   WFPG_CHECK_LAUNCH("k_lbvh_boxes");
+  WFPG_CUDA(cudaMemsetAsync(depth_dev, 0, sizeof(int32_t), st));
+  k_lbvh_depth<<<grid, 256, 0, st>>>(parent, n, depth_dev);
+  WFPG_CHECK_LAUNCH("k_lbvh_depth");
+  int32_t depth = 0;
+  WFPG_CUDA(cudaMemcpyAsync(&depth, depth_dev, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  WFPG_CUDA(cudaStreamSynchronize(st));
+  if (depth > 62) {  // a DFS stack holds at most depth + 1 entries
+    set_error("device BVH depth %d exceeds the 64-entry traversal stacks", depth);
+    return WFPG_ERR_ARG;
+  }
   return WFPG_OK;
 }
