@@ -317,7 +317,8 @@ int wfpg_svo_refresh_leaves(wfpg_svo* svo, const int32_t* leaf, int64_t n, uint8
  * [1, min(depth, 7)]; bytes = wfpg_svo_top_index_bytes(top_level). */
 /* Device BVH build for scenes too large for the host
  * build (bvh.py:33-119): linear BVH over 63-bit Morton codes of the triangle
- * box centres (Karras 2012), one triangle per leaf, written in the host
+ * box centres (Karras 2012), subtrees of <= 4 triangles collapsed into
+ * leaves (unreachable nodes stay in the arrays), written in the host
  * BVH's flattened layout (2T-1 nodes, root 0; lo / hi (N,3), left / right /
  * count (N,), order (T,), padded fp32 boxes (N,8) as wfpg_scene.bvh_box_f32).
  * Reads scene->v0/v1/v2, n_tris and the host bbox.  Nearest hits equal the

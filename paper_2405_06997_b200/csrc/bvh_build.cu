@@ -10,7 +10,9 @@
 //
 // Output layout = the host BVH's flattened arrays: node 0 is the root,
 // internal nodes 0 .. n-2 (count 0, left / right children), leaves
-// n-1 .. 2n-2 with one triangle each (count 1, left = slot in `order`).
+// n-1 .. 2n-2 with one triangle each (count 1, left = slot in `order`);
+// internal nodes over at most 4 triangles are then turned into leaves
+// (count = size, left = first slot), leaving their subtrees unreachable.
 #include "prims.cuh"
 
 namespace wfpg {
@@ -46,7 +48,8 @@ __global__ void k_lbvh_codes(const double* __restrict__ v0, const double* __rest
 
 __global__ void k_lbvh_hierarchy(const uint64_t* __restrict__ k, int n,
                                  int32_t* __restrict__ left, int32_t* __restrict__ right,
-                                 int32_t* __restrict__ count, int32_t* __restrict__ parent) {
+                                 int32_t* __restrict__ count, int32_t* __restrict__ parent,
+                                 int32_t* __restrict__ span) {
   const int leaf0 = n - 1;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     // leaf i
@@ -77,6 +80,23 @@ __global__ void k_lbvh_hierarchy(const uint64_t* __restrict__ k, int n,
     count[i] = 0;
     parent[cl] = i;
     parent[cr] = i;
+    span[2 * i] = min(i, j);  // the node covers sorted primitives [first, last]
+    span[2 * i + 1] = max(i, j);
+  }
+}
+
+// Subtrees of at most kLeafTris triangles become one leaf over their
+// contiguous slice of `order` (the host build's leaf size, bvh.py:14); the
+// nodes below stay in the arrays but are no longer reachable.
+constexpr int kLeafTris = 4;
+__global__ void k_lbvh_collapse(int n, const int32_t* __restrict__ span,
+                                int32_t* __restrict__ left, int32_t* __restrict__ count) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n - 1; i += gridDim.x * blockDim.x) {
+    const int first = span[2 * i], size = span[2 * i + 1] - first + 1;
+    if (size <= kLeafTris) {
+      left[i] = first;
+      count[i] = size;
+    }
   }
 }
 
@@ -157,6 +177,7 @@ extern "C" size_t wfpg_bvh_build_workspace_bytes(int64_t n_tris) {
   a.take<int32_t>(2 * n);
   a.take<uint32_t>(n);
   a.take<int32_t>(1);
+  a.take<int32_t>(2 * n);
   return a.off + sort_ws_bytes(n) + 1024;
 }
 
@@ -177,6 +198,7 @@ extern "C" int wfpg_bvh_build_device(const wfpg_scene* scene, double* lo, double
   int32_t* parent = a.take<int32_t>(2 * (int64_t)n);
   uint32_t* ticket = a.take<uint32_t>(n);
   int32_t* depth_dev = a.take<int32_t>(1);
+  int32_t* span = a.take<int32_t>(2 * (int64_t)n);
   if (!a.ok()) {
     set_error("bvh build: workspace too small");
     return WFPG_ERR_WORKSPACE;
@@ -197,7 +219,7 @@ extern "C" int wfpg_bvh_build_device(const wfpg_scene* scene, double* lo, double
   WFPG_TRY(sort_pairs(keys, idx, n, nullptr, 63, a, st));
   WFPG_CUDA(cudaMemsetAsync(ticket, 0, sizeof(uint32_t) * (size_t)n, st));
   WFPG_CUDA(cudaMemsetAsync(parent, 0xff, sizeof(int32_t) * 2 * (size_t)n, st));
-  k_lbvh_hierarchy<<<grid, 256, 0, st>>>(keys, n, left, right, count, parent);
+  k_lbvh_hierarchy<<<grid, 256, 0, st>>>(keys, n, left, right, count, parent, span);
   WFPG_CHECK_LAUNCH("k_lbvh_hierarchy");
   k_lbvh_boxes<<<grid, 256, 0, st>>>(scene->v0, scene->v1, scene->v2, idx, n, left, right, parent,
                                      ticket, lo, hi, box_f32, order, pad0);
@@ -205,6 +227,8 @@ extern "C" int wfpg_bvh_build_device(const wfpg_scene* scene, double* lo, double
   WFPG_CUDA(cudaMemsetAsync(depth_dev, 0, sizeof(int32_t), st));
   k_lbvh_depth<<<grid, 256, 0, st>>>(parent, n, depth_dev);
   WFPG_CHECK_LAUNCH("k_lbvh_depth");
+  k_lbvh_collapse<<<grid, 256, 0, st>>>(n, span, left, count);
+  WFPG_CHECK_LAUNCH("k_lbvh_collapse");
   int32_t depth = 0;
   WFPG_CUDA(cudaMemcpyAsync(&depth, depth_dev, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   WFPG_CUDA(cudaStreamSynchronize(st));

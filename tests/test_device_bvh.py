@@ -35,17 +35,24 @@ def test_structure(scene_path, monkeypatch):
     count, order = d["bvh_count"].cpu().numpy(), d["bvh_order"].cpu().numpy()
     box = d["bvh_box_f32"].cpu().numpy()
     assert np.array_equal(np.sort(order), np.arange(t))
-    inner = count == 0
-    assert inner.sum() == t - 1 and np.all(count[~inner] == 1)
-    kids = np.concatenate([left[inner], right[inner]])
-    assert np.array_equal(np.sort(kids), np.arange(1, n))  # a tree rooted at 0
-    for c in (left[inner], right[inner]):
-        assert np.all(lo[inner] <= lo[c]) and np.all(hi[inner] >= hi[c])
-    leaves = np.nonzero(~inner)[0]
-    tri = order[left[leaves]]
-    tlo = np.minimum(np.minimum(sc.v0, sc.v1), sc.v2)[tri]
-    thi = np.maximum(np.maximum(sc.v0, sc.v1), sc.v2)[tri]
-    assert np.array_equal(lo[leaves], tlo) and np.array_equal(hi[leaves], thi)
+    # walk the reachable tree: every triangle in exactly one leaf, leaves of
+    # at most 4 triangles, children inside their parent's box
+    seen = np.zeros(t, dtype=np.int64)
+    todo = [0]
+    while todo:
+        k = todo.pop()
+        if count[k] > 0:
+            assert count[k] <= 4
+            tri = order[left[k]:left[k] + count[k]]
+            seen[tri] += 1
+            tlo = np.minimum(np.minimum(sc.v0, sc.v1), sc.v2)[tri].min(axis=0)
+            thi = np.maximum(np.maximum(sc.v0, sc.v1), sc.v2)[tri].max(axis=0)
+            assert np.array_equal(lo[k], tlo) and np.array_equal(hi[k], thi)
+        else:
+            for c in (left[k], right[k]):
+                assert np.all(lo[k] <= lo[c]) and np.all(hi[k] >= hi[c])
+                todo.append(int(c))
+    assert np.all(seen == 1)
     assert np.all(box[:, 0:3] <= lo) and np.all(box[:, 4:7] >= hi)
 
 
