@@ -87,3 +87,46 @@ def test_render_pass_matches_host_bvh(scene_path, monkeypatch):
     (p0, e0), (p1, e1) = states
     same = (e0 == e1) & (np.abs(p0 - p1).max(axis=(1, 2)) <= 1e-5 * host.diagonal)
     assert same.mean() >= 0.99, same.mean()
+
+
+@pytest.mark.parametrize("n_quads,flat", [(0, False), (1, True), (40, True), (40, False)])
+def test_small_and_flat_scenes(monkeypatch, n_quads, flat):
+    """Edge cases of the device build: a single triangle (the root is a
+    leaf), scenes flat in z (one zero extent) and equal centroids; every
+    query equals the brute-force answer of the host-BVH scene."""
+    from paper_2405_06997_b200 import scene as S
+
+    rng = np.random.default_rng(n_quads)
+    tris = [np.array([[0.0, 0.0, 0.0], [1.0, 0.0, 0.0], [0.0, 1.0, 0.0]])]  # the emitter
+    for k in range(n_quads):
+        o = rng.random(3) * 4.0
+        if flat:
+            o[2] = 0.0
+        a, b = np.array([0.7, 0.1, 0.0]), np.array([0.1, 0.6, 0.0])
+        tris += [np.stack([o, o + a, o + b]), np.stack([o + a, o + a + b, o + b])]
+    if n_quads == 40:
+        tris += [tris[1].copy() for _ in range(5)]  # duplicate centroids
+    v = np.stack(tris)
+    mats = [S.Material("light", 2, [1.0, 1.0, 1.0]), S.Material("white", 0, [0.5, 0.5, 0.5])]
+    mid = np.ones(len(v), dtype=np.int32)
+    mid[0] = 0
+    cam = S.Camera([2.0, 2.0, 5.0], [2.0, 2.0, 0.0], [0.0, 1.0, 0.0], 40.0, 8, 8)
+    o = np.column_stack([rng.random(512) * 5.0, rng.random(512) * 5.0, np.full(512, 3.0)])
+    d = np.tile([0.0, 0.0, -1.0], (512, 1)) + rng.normal(0.0, 0.05, (512, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    res = []
+    for lbvh in (False, True):
+        monkeypatch.setattr(S, "DEVICE_BVH_MIN_TRIS", 1 if lbvh else 10 ** 9)
+        monkeypatch.setattr(S, "SIMD_BRUTE_MAX_TRIS", 0)  # force the BVH traversal
+        sc = S.Scene(v[:, 0], v[:, 1], v[:, 2], mid, mats, cam)
+        res.append(sc.intersect_batch(o, d))
+        assert sc.abi().brute == 0 and sc.device_bvh == lbvh
+    (t0, i0), (t1, i1) = res
+    # the nearest distance never depends on the tree; which of several
+    # triangles at exactly that distance wins does (overlapping coplanar
+    # quads in the flat scenes tie everywhere)
+    assert np.array_equal(i0 >= 0, i1 >= 0)
+    hit = i0 >= 0
+    np.testing.assert_allclose(t1[hit], t0[hit], rtol=1e-12)
+    if not flat:
+        assert np.mean(i0 == i1) >= 0.995
