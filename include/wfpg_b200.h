@@ -315,6 +315,14 @@ int wfpg_svo_refresh_leaves(wfpg_svo* svo, const int32_t* leaf, int64_t n, uint8
 
 /* Fill svo->top_index (see wfpg_svo) from the node arrays; top_level in
  * [1, min(depth, 7)]; bytes = wfpg_svo_top_index_bytes(top_level). */
+/* Host BVH build with the reference's decisions (bvh.py:33-119): the C++
+ * port of paper_2405_06997_b200/bvh.py (binned SAH, 16 bins, <= 4 triangles
+ * per leaf, stable partitions, depth-first numbering), bitwise the same
+ * arrays.  Host pointers; node arrays of capacity 2T-1; *n_nodes = count. */
+int wfpg_bvh_build_host(const double* v0, const double* v1, const double* v2, int64_t n,
+                        double* lo, double* hi, int32_t* left, int32_t* right, int32_t* count,
+                        int32_t* order, int64_t* n_nodes);
+
 /* Device BVH build for scenes too large for the host
  * build (bvh.py:33-119): linear BVH over 63-bit Morton codes of the triangle
  * box centres (Karras 2012), subtrees of <= 4 triangles collapsed into

@@ -121,6 +121,8 @@ _SIGS = {
     "wfpg_svo_build_fill": (c_i32, [P(Svo), c_vp, c_vp, c_i64, c_u64, c_vp, c_size, c_vp]),
     "wfpg_svo_build_sorted": (c_i32, [c_vp, c_i64, P(c_vp), P(c_vp)]),
     "wfpg_descend": (c_i32, [P(Svo), c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "wfpg_bvh_build_host": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                    c_vp]),
     "wfpg_bvh_build_workspace_bytes": (c_size, [c_i64]),
     "wfpg_bvh_build_device": (c_i32, [P(Scene), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                       c_size, c_vp]),

@@ -73,6 +73,30 @@ def _choose_split(tri_lo, tri_hi, cen, ids):
 
 
 def build(v0, v1, v2):
+    """The reference's BVH (see the module doc), built by the C++ port in
+    libwfpg_b200.so (csrc/bvh_host.cu); bitwise the arrays of build_py."""
+    import ctypes as C
+
+    from . import _lib
+
+    v0, v1, v2 = (np.ascontiguousarray(a, dtype=np.float64) for a in (v0, v1, v2))
+    n = len(v0)
+    cap = max(2 * n - 1, 1)
+    lo, hi = np.empty((cap, 3)), np.empty((cap, 3))
+    left, right, count = (np.empty(cap, dtype=np.int32) for _ in range(3))
+    order = np.empty(n, dtype=np.int32)
+    nn = C.c_int64(0)
+    p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    _lib.call("wfpg_bvh_build_host", p(v0), p(v1), p(v2), n, p(lo), p(hi), p(left), p(right),
+              p(count), p(order), C.byref(nn))
+    k = nn.value
+    return Bvh(lo[:k].copy(), hi[:k].copy(), left[:k].astype(np.int64),
+               right[:k].astype(np.int64), count[:k].astype(np.int64), order.astype(np.int64))
+
+
+def build_py(v0, v1, v2):
+    """numpy restatement of the reference's build (kept as the checker of
+    the C++ port, tests/test_host_api.py)."""
     n = len(v0)
     tri_lo = np.minimum(np.minimum(v0, v1), v2)
     tri_hi = np.maximum(np.maximum(v0, v1), v2)
