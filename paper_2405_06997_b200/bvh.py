@@ -1,7 +1,9 @@
 """Host-side binned-SAH BVH, flattened for the device traversal kernels.
 
-Built once at scene load (the reference builds it the same way, bvh.py:33-119),
-then uploaded; traversal runs in the CUDA kernels (geometry.cuh).  The build
+Built on first use by the C++ port in libwfpg_b200.so (csrc/bvh_host.cu) with
+the reference's decisions (bvh.py:33-119; ``build_py`` is the numpy
+restatement it is checked against), then uploaded; traversal runs in the
+CUDA kernels (geometry.cuh).  The build
 makes the same split decisions as the reference so that the device traversal
 visits the same boxes: 16 centroid bins on the widest centroid axis, at most
 4 triangles per leaf, surface-area cost with strict improvement, stable
