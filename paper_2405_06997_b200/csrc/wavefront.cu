@@ -38,31 +38,48 @@ __global__ void k_camera(CameraView c, const uint64_t* __restrict__ keys,
 
 // Pass initialisation (wavefront.py:211-219): keys, camera rays, ctr = 2,
 // beta = 1, radiance = 0, alive, prev_pdf = -1, records, emitter slots.
-__global__ void k_init_paths(CameraView c, PathsView P, int64_t n_paths, int64_t n_pix,
-                             int64_t n_img, int64_t pix0, const int64_t* __restrict__ sample_dev,
-                             uint64_t seed) {
+// Tiles of 256 paths per block: the (P,3) arrays are written as contiguous
+// runs of 768 doubles (directions staged in shared memory) instead of
+// 24-byte-strided per-thread stores.
+constexpr int kInitTile = 256;
+__global__ void __launch_bounds__(kInitTile) k_init_paths(CameraView c, PathsView P,
+                                                          int64_t n_paths, int64_t n_pix,
+                                                          int64_t n_img, int64_t pix0,
+                                                          const int64_t* __restrict__ sample_dev,
+                                                          uint64_t seed) {
+  __shared__ double sdir[3 * kInitTile];
   const int64_t sample0 = *sample_dev;
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_paths;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    int64_t pix = pix0 + p % n_pix;  // global pixel index
-    int64_t sample = sample0 + p / n_pix;
-    uint64_t key = stream_key(seed, (uint64_t)(sample * n_img + pix) * 4u);
-    const_cast<uint64_t*>(P.key)[p] = key;
-    camera_ray(c, key, pix, P.ray_o + 3 * p, P.ray_d + 3 * p);
-    P.ctr[p] = 2;
-    for (int k = 0; k < 3; ++k) {
-      P.beta[3 * p + k] = 1.0;
-      P.radiance[3 * p + k] = 0.0;
-      P.emit_le[3 * p + k] = 0.0;
+  for (int64_t base = (int64_t)blockIdx.x * kInitTile; base < n_paths;
+       base += (int64_t)gridDim.x * kInitTile) {
+    const int64_t p = base + threadIdx.x;
+    const int m = (int)(n_paths - base < kInitTile ? n_paths - base : kInitTile);
+    if (p < n_paths) {
+      int64_t pix = pix0 + p % n_pix;  // global pixel index
+      int64_t sample = sample0 + p / n_pix;
+      uint64_t key = stream_key(seed, (uint64_t)(sample * n_img + pix) * 4u);
+      const_cast<uint64_t*>(P.key)[p] = key;
+      double o[3];
+      camera_ray(c, key, pix, o, sdir + 3 * threadIdx.x);
+      P.ctr[p] = 2;
+      P.alive[p] = 1;
+      P.prev_pdf[p] = -1.0;
+      P.emit_depth[p] = 0;
+      if (P.n_rec) P.n_rec[p] = 0;
+      double* rp = P.rec_pos + (int64_t)p * P.rec_depths * 3;  // zeroed by the launcher unless n_rec
+      rp[0] = c.pos[0];
+      rp[1] = c.pos[1];
+      rp[2] = c.pos[2];
     }
-    P.alive[p] = 1;
-    P.prev_pdf[p] = -1.0;
-    P.emit_depth[p] = 0;
-    if (P.n_rec) P.n_rec[p] = 0;
-    double* rp = P.rec_pos + (int64_t)p * P.rec_depths * 3;  // zeroed by the launcher unless n_rec
-    rp[0] = c.pos[0];
-    rp[1] = c.pos[1];
-    rp[2] = c.pos[2];
+    __syncthreads();
+    for (int e = threadIdx.x; e < 3 * m; e += kInitTile) {
+      const int64_t g = 3 * base + e;
+      P.ray_d[g] = sdir[e];
+      P.ray_o[g] = c.pos[e % 3];
+      P.beta[g] = 1.0;
+      P.radiance[g] = 0.0;
+      P.emit_le[g] = 0.0;
+    }
+    __syncthreads();
   }
 }
 
@@ -423,7 +440,9 @@ int launch_camera_init(const CameraView& c, const PathsView& P, int64_t n_paths,
     WFPG_CUDA(cudaMemsetAsync(P.rec_pos, 0, rec_bytes, st));
     WFPG_CUDA(cudaMemsetAsync(P.rec_T, 0, rec_bytes, st));
   }
-  k_init_paths<<<grid, 256, 0, st>>>(c, P, n_paths, n_pix, n_img, pix0, sample0, seed);
+  const int igrid =
+      (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_paths, kInitTile), kNumSMs * 8));
+  k_init_paths<<<igrid, kInitTile, 0, st>>>(c, P, n_paths, n_pix, n_img, pix0, sample0, seed);
   WFPG_CHECK_LAUNCH("k_init_paths");
   return WFPG_OK;
 }
