@@ -4,6 +4,9 @@
 // _kernels.pyx:319-478).  Same acceptance tests and tie rules as the
 // reference: brute force keeps the minimum t with the lowest triangle id on
 // ties; BVH traversal visits children nearest-first with the same stacks.
+// Box tests run in fp32 on padded boxes (triangle boxes for the brute-force
+// prefilter, bvh_box_f32 node boxes when present) — the padding dwarfs fp32
+// rounding, so they only skip work; every accepted hit is the fp64 test's.
 #pragma once
 #include "common.cuh"
 
