@@ -51,3 +51,22 @@ def test_b200_arm_line():
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     cb = d["cpu_baseline"]
     assert cb["value"] > 0 and cb["kind"] in ("port", "reference")
+
+
+@pytest.mark.gpu
+def test_b200_arm_two_ranks_gloo():
+    """The N>1 launch path (torchrun, one process per rank, per-pass deposit
+    exchange, max-over-ranks timing) on the one visible GPU over gloo."""
+    env = dict(os.environ, PYTHONPATH=REPO, WFPG_DIST_BACKEND="gloo")
+    out = subprocess.run(
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+         "--master-addr", "127.0.0.1", "--master-port", "29561", os.path.join(REPO, "bench.py"),
+         "--gpus", "2", "--width", "96", "--height", "64", "--svo-res", "64", "--steps", "3",
+         "--warmup", "3", "--no-cpu-baseline"],
+        cwd=REPO, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]  # rank 0 only
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
+    assert d["e2e"]["value"] > 0
