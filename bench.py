@@ -11,9 +11,13 @@ timed passes are guided samples 1, 2, ... so the SVO keeps learning.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-Under torchrun (N > 1) each rank renders its own 1920x1080 band of a
-1920 x (1080 N) image (weak scaling); after every pass the leaf exitance
-deposits are summed across ranks with an NCCL all-reduce.
+Under torchrun (N > 1) the 1920x1080 image is split into N pixel bands
+(strong scaling; --weak: every rank renders its own 1920x1080 band).  Each
+rank's pass bins the guided depths globally (start nodes all-gathered),
+generates the fields of only the bins its own paths belong to, and splats
+every rank's exitance deposits in global path order — NCCL collectives issued
+by the native library inside the pass's CUDA graph (multigpu.py).  The image
+is the 1-GPU image path for path.
 """
 
 import argparse
@@ -53,20 +57,46 @@ def parse():
     p.add_argument("--field-res", type=int, default=128)
     p.add_argument("--product", action="store_true")
     p.add_argument("--tiled", action="store_true",
-                   help="C4: --width x --height is the whole image, split into one band per "
-                        "GPU (strong scaling); default: every GPU renders its own "
-                        "width x height band of a taller image (weak scaling)")
+                   help="(default) --width x --height is the whole image, split into one band "
+                        "per GPU (strong scaling); C4 = --tiled --width 3840 --height 2160")
+    p.add_argument("--weak", action="store_true",
+                   help="every GPU renders its own width x height band of a taller image")
     p.add_argument("--seed", type=int, default=0)
-    p.add_argument("--cpu-seconds", type=float, default=20.0,
-                   help="budget of the CPU-baseline sample")
-    p.add_argument("--ref-seconds", type=float, default=None,
-                   help="--impl reference: CPU sample per step (default min(10, 150 / (W + K)) s)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     a = p.parse_args()
     if a.svo_res is None:
         a.svo_res = SCENES[a.scene][1]
     return a
+
+
+METRIC = "path samples/sec (guided wavefront pass)"
+DATA = "synthetic: scenes/{scene}, path samples from the counter RNG"
+
+
+def scaling(args):
+    return "weak" if args.weak else "strong"
+
+
+def image_height(args, world):
+    return args.height * world if args.weak else args.height
+
+
+def workload_config(args, svo_depth, world):
+    """The config dict both arms print (identical for the same arguments)."""
+    H = image_height(args, world)
+    lmin = min(5, svo_depth - 1)
+    return {"workload": f"{SCENES[args.scene][2]} {args.width}x{H}, 1 spp guided pass per step, "
+                        f"SVO depth {svo_depth}, D={args.depth}, G={args.depth}, "
+                        f"N0={args.field_res}, l_min {lmin}, c_ray 512, "
+                        f"{'product' if args.product else 'plain'} guiding",
+            "scene": SCENES[args.scene][0], "image": [args.width, H], "svo_depth": svo_depth,
+            "max_depth": args.depth, "guided_depths": args.depth, "field_res": args.field_res,
+            "l_min": lmin, "c_ray": 512, "product": bool(args.product), "seed": args.seed,
+            "l2": "inputs larger than L2 (path state + guide tables > 126 MB)",
+            "parallelism": "single GPU" if world == 1 else (
+                f"image bands x{world} ({'weak: one band per GPU' if args.weak else 'strong: one image split'}), "
+                "global Alg. 2 binning + per-pass deposit exchange (NCCL, in the pass graph)")}
 
 
 def peaks():
@@ -154,19 +184,15 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def image_height(args, world):
-    return args.height if args.tiled else args.height * world
-
-
-def build_workload(args, rank=0, world=1):
+def build_workload(args, world=1):
     import torch
 
     from paper_2405_06997_b200 import scene as S, svo, wavefront
 
     sc = S.load_scene(os.path.join(REPO, "scenes", SCENES[args.scene][0]))
     cam = sc.camera
-    # weak scaling: rank r renders band r of a width x (height * world) image;
-    # --tiled (C4): the width x height image is split into world bands
+    # strong scaling (default): the width x height image is split into world
+    # bands; --weak: every rank renders its own width x height band
     sc.camera = S.Camera(cam.position, cam.target, cam.up, cam.vfov_deg, args.width,
                          image_height(args, world))
     t0 = time.perf_counter()
@@ -206,16 +232,19 @@ def algorithmic_bytes_per_cone(svo_depth):
 
 
 def run_b200(args):
+    import ctypes as C
+
     import torch
     import torch.distributed as dist
 
-    from paper_2405_06997_b200 import _lib, wavefront
+    from paper_2405_06997_b200 import _lib, multigpu, wavefront
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     # one GPU per rank; WFPG_DIST_BACKEND=gloo + a shared device lets the
-    # multi-rank path be exercised on a 1-GPU box (functional check only)
+    # multi-rank path be exercised on a 1-GPU box (functional check only:
+    # host-exchange communicator over gloo, eager passes)
     dev = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev)
     backend = os.environ.get("WFPG_DIST_BACKEND", "nccl")
@@ -224,35 +253,30 @@ def run_b200(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
             dist.init_process_group(backend)
-    sc, tree, pt_cfg, g_cfg, build_ms = build_workload(args, rank, world)
+    sc, tree, pt_cfg, g_cfg, build_ms = build_workload(args, world)
     lib = _lib.load()
-
-    from paper_2405_06997_b200 import multigpu
-
-    # per-pass SVO sync: every rank exports its deposits, all-gathers the
-    # lists and splats them in global path order (multigpu.DepositExchange)
-    sync_svo = multigpu.DepositExchange(tree) if world > 1 else None
+    comm = None
+    if world > 1:
+        # the pass's own collectives: NCCL captured in the pass graph, or the
+        # host-exchange protocol over gloo
+        comm = (multigpu.Communicator.nccl() if backend == "nccl"
+                else multigpu.Communicator.torch_distributed())
     total_pix = args.width * image_height(args, world)
     off, npx = multigpu.band(total_pix, rank, world)
-    pt = wavefront.PassRunner(sc, tree, pt_cfg, pixel_offset=off, n_pixels=npx,
-                              deposit_sink=sync_svo)
-    gr = wavefront.PassRunner(sc, tree, g_cfg, pixel_offset=off, n_pixels=npx,
-                              deposit_sink=sync_svo)
-
-    def one_pass(runner, sample, stats=False):
-        runner.launch(sample, want_stats=stats)
-        if sync_svo is not None:
-            sync_svo.reduce_and_apply(runner)
+    pt = wavefront.PassRunner(sc, tree, pt_cfg, pixel_offset=off, n_pixels=npx, comm=comm)
+    gr = wavefront.PassRunner(sc, tree, g_cfg, pixel_offset=off, n_pixels=npx, comm=comm)
 
     # field-kernel timing stamps are part of the captured pass, so switch them
     # on before the warm-up (which also captures the pass's CUDA graph)
     lib.wfpg_profile_enable(1)
-    one_pass(pt, 0, True)
+    pt.launch(0, want_stats=True)
     sample = 1
     for _ in range(max(args.warmup, 3)):
-        one_pass(gr, sample, True)
+        gr.launch(sample, want_stats=True)
         sample += 1
     stats = gr.pass_stats()
+    if comm is not None:
+        comm.settle()
     torch.cuda.synchronize()
 
     lib.wfpg_profile_enable(1)  # zero the accumulators; timed passes replay the graph
@@ -266,29 +290,35 @@ def run_b200(args):
         torch.cuda.synchronize()
         start.record(stream)
         for _ in range(args.steps):
-            one_pass(gr, sample)
+            gr.launch(sample, want_stats=False)
             sample += 1
+        if comm is not None:
+            comm.settle()  # the last pass's deposit exchange is part of the work
         end.record(stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
     ms = start.elapsed_time(end)
     launches = _lib.launch_count() - launches0
-    import ctypes as C
-
     D = args.depth
     fms = (C.c_double * (D + 1))()
     cones = (C.c_double * (D + 1))()
     nl = (C.c_int64 * (D + 1))()
     lib.wfpg_profile_read(fms, cones, nl, D)
     lib.wfpg_profile_enable(0)
+    per_rank = {"rank": rank, "paths_per_pass": npx, "ms": ms,
+                "cones_per_pass": sum(cones[d] for d in range(1, D + 1)) / args.steps,
+                "field_bins_per_pass": [cones[d] / max(nl[d], 1) / max(8, args.field_res >> (d - 1)) ** 2
+                                        for d in range(1, D + 1)]}
     if world > 1:
-        t = torch.tensor([ms], device="cuda" if backend == "nccl" else "cpu",
-                         dtype=torch.float64)
+        t = torch.tensor([ms], device="cuda" if backend == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+        ranks = [None] * world
+        dist.all_gather_object(ranks, per_rank)
+    else:
+        ranks = [per_rank]
 
-    n_paths = npx  # this rank's paths per pass
     ms_step = ms / args.steps
     value = total_pix * args.steps / (ms / 1e3)  # whole job
 
@@ -299,7 +329,7 @@ def run_b200(args):
     peak, peak_kind = peaks()
     achieved = d1_bytes / (d1_ms / 1e3) / 1e9 if d1_ms > 0 else 0.0
     field_ms_step = sum(fms[d] for d in range(1, D + 1)) / args.steps
-    roof = {"bound": "hbm", "kernel": "k_fields<128> (depth-1 fields)",
+    roof = {"bound": "hbm", "kernel": f"k_fields<{args.field_res}> (depth-1 fields)",
             "timer": "%globaltimer stamp kernels on the pass stream around each field launch, "
                      "inside the timed CUDA-graph replays (host events cannot sit between "
                      "graph nodes)",
@@ -312,11 +342,10 @@ def run_b200(args):
             "field_share_of_step": field_ms_step / ms_step,
             "limiter": (_traffic_entry(args) or {}).get("limiter")}
 
-    # e2e through the public API: every pass's frame delivered to pinned host
-    # memory by wavefront.FramePipeline (D2H of pass i overlapped with pass i+1)
+    # e2e through the public API with every pass's frame in pinned host memory
     e2e = None
     if world == 1 and not args.no_e2e:
-        frame_bytes = n_paths * 3 * 8
+        frame_bytes = npx * 3 * 8
         pipe = wavefront.FramePipeline(sc, tree, g_cfg)
         for _ in pipe.run(range(sample, sample + 3)):  # API warm-up (captures both graphs)
             pass
@@ -328,88 +357,89 @@ def run_b200(args):
             checksum += float(f[0, 0, 0])  # the host frame is read every step
         e2e_s = time.perf_counter() - t0
         sample += args.steps
-        e2e = {"value": n_paths * args.steps / e2e_s, "unit": "path samples/s",
+        e2e = {"value": npx * args.steps / e2e_s, "unit": "path samples/s",
                "h2d_bytes_per_step": C.sizeof(_lib.PassConfig) + C.sizeof(_lib.Camera),
                "d2h_bytes_per_step": frame_bytes,
                "api": "paper_2405_06997_b200.wavefront.FramePipeline.run -> pinned host "
                       "frame per pass (copy of pass i overlapped with pass i+1)"}
     elif world > 1 and not args.no_e2e:
-        # per rank: pass + deposit exchange + its band of the frame to pinned
-        # host memory; whole-job time = max over ranks
+        # per rank: pass (with its in-graph exchange) + its band of the frame
+        # to pinned host memory; whole-job time = max over ranks
         host = torch.empty((npx, 3), dtype=torch.float64, pin_memory=True)
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            one_pass(gr, sample)
+            gr.launch(sample, want_stats=False)
             sample += 1
             host.copy_(gr.frame, non_blocking=True)
             torch.cuda.current_stream().synchronize()
+            float(host[0, 0])
+        comm.settle()
         e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64,
                              device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
         e2e = {"value": total_pix * args.steps / float(e2e_s.item()),
                "unit": "path samples/s",
                "h2d_bytes_per_step": C.sizeof(_lib.PassConfig) + C.sizeof(_lib.Camera),
-               "d2h_bytes_per_step": npx * 3 * 8 + 4,
-               "api": "wavefront.PassRunner.launch + multigpu.DepositExchange per rank, "
-                      "band frame -> pinned host; max over ranks"}
+               "d2h_bytes_per_step": npx * 3 * 8,
+               "api": "wavefront.PassRunner.launch(comm=multigpu.Communicator) per rank, band "
+                      "frame -> pinned host; max over ranks"}
 
     out = {
-        "metric": "path samples/sec (guided wavefront pass)",
+        "metric": METRIC,
         "value": value, "unit": "path samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "strong" if args.tiled else "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: "
-        f"scenes/{SCENES[args.scene][0]}, path samples from the counter RNG",
-        "config": {"workload": f"{SCENES[args.scene][2]} {args.width}x{args.height} "
-                               + ("image tiled over the GPUs, " if args.tiled else "per GPU, ")
-                               + 
-                               f"1 spp guided pass, SVO depth {tree.depth}, D={D}, G={D}, N0={args.field_res}, "
-                               f"l_min {g_cfg.l_min}, c_ray 512, "
-                               f"{'product' if args.product else 'plain'} guiding",
-                   "image": [args.width, image_height(args, world)],
-                   "svo_nodes": tree.node_count,
-                   "l2": "inputs larger than L2 (path state + guide tables > 126 MB)",
-                   "parallelism": f"image bands x{world}" + (
-                       f", per-pass deposit all-gather ({backend})" if world > 1 else "")},
+        "scaling": scaling(args), "vs_baseline": None, "dtype": "f64",
+        "data": DATA.format(scene=SCENES[args.scene][0]),
+        "config": workload_config(args, tree.depth, world),
+        "svo_nodes": tree.node_count,
         "bins_per_depth": stats.bins_per_depth, "rays_per_depth": stats.rays_per_depth,
+        "per_rank": ranks,
         "svo_build_ms": build_ms,
         "gpu_launches": int(launches),
         "roofline": roof,
         "e2e": e2e,
         "clocks": clocks.summary(),
     }
+    if world > 1:
+        out["comm"] = {"backend": backend, "kind": comm.kind}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(args, sc, tree, g_cfg, stats)
+        out["cpu_baseline"] = cpu_baseline(args, sc, tree, g_cfg, sample)
     if rank == 0:
         print(json.dumps(out))
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
 
 
-def cpu_baseline(args, sc, tree, cfg, stats, seconds=None):
-    """Time the CPU oracle (port of the reference's guided pass) on a bounded
-    sample of the same workload: the guided field generation of a subset of
-    the depth-1 bins plus the shading of their paths, scaled to path samples/s
-    by the fraction of the pass's field work the sample covers."""
+def cpu_baseline(args, sc, tree, cfg, next_sample):
+    """The CPU oracle (port of the reference's guided pass) on a bounded
+    sample of the same workload: ONE full guided pass of the next sample,
+    continuing from the device run's SVO state (structure + exitance, bit-exact
+    with the oracle's), timed on this host's cores."""
     try:
         from oracle import render as OR
     except Exception as e:  # pragma: no cover
         return {"value": None, "unit": "path samples/s", "cores": 0, "kind": "port",
                 "sample": f"oracle unavailable: {e}"}
-    seconds = seconds or args.cpu_seconds
-    return OR.time_guided_pass_sample(sc, tree, cfg, stats, args.width * args.height, seconds)
+    wl = OR.CpuWorkload.from_device(sc, tree, cfg, next_sample)
+    return OR.time_guided_passes(wl, args.width * args.height, passes=1)
 
 
 def run_reference(args):
-    """--impl reference: the CPU port of the reference's guided pass (oracle/,
-    C + OpenMP on every host core; the reference itself is Python/Cython and
-    does not travel to the GPU box).  No CUDA anywhere on this arm.  Setup
-    builds the SVO and runs the PT-first pass with the oracle; each step then
-    times a bounded sample of the guided pass's field generation, scaled to the
-    full pass by its bin counts.  Rank 0 only under torchrun."""
+    """--impl reference: the CPU port of the reference's guided pass (oracle/:
+    C + OpenMP field generation on every host thread, numpy bookkeeping; the
+    reference itself is Python/Cython and does not travel to the GPU box).  No
+    CUDA and no product library on this arm: the scene is parsed by the
+    package's pure-Python loader and its BVH comes from the numpy restatement
+    (oracle/render.py _oracle_bvh).  Setup builds the SVO and renders the
+    PT-first pass with the oracle; every warm-up and timed step then renders
+    the next guided sample IN FULL (wavefront.render_pass semantics, SVO
+    learning between passes).  Rank 0 only under torchrun."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     from types import SimpleNamespace
@@ -423,29 +453,29 @@ def run_reference(args):
     depth = args.svo_res.bit_length() - 1
     cfg = SimpleNamespace(l_min=min(5, depth - 1), c_ray=512, field_res=args.field_res,
                           guided_depths=args.depth, max_depth=args.depth, product=args.product,
-                          seed=args.seed, blur_sigma=1.0, epsilon=1e-2)
+                          seed=args.seed)
     wl = OR.CpuWorkload(sc, args.svo_res, cfg, seed=args.seed)
     n_paths = args.width * args.height
-    budget = args.ref_seconds or min(10.0, 150.0 / max(1, args.warmup + args.steps))
-    vals, ms = [], []
+    secs = []
     for step in range(args.warmup + args.steps):
-        r = wl.time_pass(n_paths, budget, seed=step)
-        vals.append(r)
-    timed = vals[args.warmup:]
-    v = statistics.mean(x["value"] for x in timed)
-    cb = dict(timed[-1])
-    cb["value"] = v
-    cb["sample"] += f"; {budget:.1f} s sample per step; " + cb.pop("setup")
-    cb.pop("pass_seconds", None)
+        dt, st = wl.run_pass()
+        secs.append(dt)
+    timed = secs[args.warmup:]
+    v = n_paths * len(timed) / sum(timed)
+    cb = {"value": v, "unit": "path samples/s", "cores": OR._threads(), "kind": "port",
+          "sample": f"every step is one full guided pass of the workload ({n_paths} paths) by "
+                    f"the CPU oracle; {wl.describe()}; bins per depth of the last pass "
+                    f"{st.get('bins')}",
+          "pass_seconds": timed}
     print(json.dumps({
-        "impl": "reference", "metric": "path samples/sec (guided wavefront pass)", "value": v,
+        "impl": "reference", "metric": METRIC, "value": v,
         "unit": "path samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": n_paths / v * 1e3 if v else None, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{SCENES[args.scene][2]} {args.width}x{args.height}, 1 spp guided pass, "
-                               f"SVO depth {depth}, D={args.depth}",
-                   "host": "CPU only, rank 0's host cores; n_gpus mirrors the B200 arm "
-                           "this line is paired with"},
+        "ms_per_step": sum(timed) / len(timed) * 1e3, "higher_is_better": True,
+        "scaling": scaling(args), "vs_baseline": None, "dtype": "f64", "data": DATA.format(
+            scene=SCENES[args.scene][0]),
+        "config": workload_config(args, depth, world),
+        "host": "CPU only (rank 0's host threads); n_gpus mirrors the B200 arm this line is "
+                "paired with",
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "path samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0}}), flush=True)

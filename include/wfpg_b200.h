@@ -226,6 +226,28 @@ typedef struct wfpg_pass_config {
   double* dep_rad;
   int32_t* dep_count;
   int64_t dep_capacity;
+  /* Optional multi-GPU communicator (wfpg_comm_init_*).  With
+   * comm set (n_samples must be 1; pixel_offset / n_pixels give this rank's
+   * band, band r = [r*n_img/W, (r+1)*n_img/W)) the pass is the 1-GPU pass of
+   * the whole image restricted to this band, path for path:
+   *  - guided depths bin GLOBALLY (Alg. 2 over every rank's lambert hits): the
+   *    per-path start nodes are all-gathered, every rank runs the same
+   *    partition, the bin origins (the k-th member in global path order) are
+   *    contributed by the rank that owns that path (one all-reduce of bit
+   *    patterns), and each rank generates the fields only of the bins its own
+   *    paths belong to;
+   *  - the Eq. 5 deposits of all ranks are all-gathered (fixed wire capacity
+   *    per rank, dep_wire_capacity records; 0 = n_pixels / 4) and splatted in
+   *    global path order, so every rank's SVO equals the 1-GPU SVO bit for
+   *    bit.  A rank that exports more deposits than the wire holds makes
+   *    every rank skip the in-pass splat; the exact variable-size exchange of
+   *    that pass then runs before the next pass on this communicator (or in
+   *    wfpg_comm_settle).
+   * NCCL communicators are captured into the pass's CUDA graph; host-exchange
+   * communicators run the pass eagerly.  Non-guided depths bin locally
+   * (their bins only feed PassStats). */
+  struct wfpg_comm* comm;
+  int64_t dep_wire_capacity;
 } wfpg_pass_config;
 
 /* Per-pass statistics returned to the host: wavefront.py:81-85 (PassStats). */
@@ -235,7 +257,9 @@ typedef struct wfpg_pass_stats {
   int32_t rays_per_depth[32];
   int32_t live_per_depth[32];
   int32_t deposits;
-  int32_t mat_groups[32][16]; /* per depth, per material id (first 16 ids) */
+  int32_t mat_groups[32][64]; /* per depth, per material id (first 64 ids): paths of the
+                                  depth's live queue that hit a triangle of that material
+                                  (partition_material, wavefront.py:88-95,250-253) */
 } wfpg_pass_stats;
 
 /* ------------------------------------------------------------------------ */
@@ -243,6 +267,41 @@ typedef struct wfpg_pass_stats {
 /* ------------------------------------------------------------------------ */
 
 int wfpg_abi_version(void);
+/* Struct layout of this build, for binding checks (ctypes / cgo mirrors):
+ * struct_id 0 scene, 1 camera, 2 svo, 3 paths, 4 guide, 5 pass_config,
+ * 6 pass_stats.  sizeof, or the byte offset of the named field; -1 when
+ * unknown. */
+int64_t wfpg_abi_sizeof(int32_t struct_id);
+int64_t wfpg_abi_offsetof(int32_t struct_id, const char* field);
+
+/* ------------------------------------------------------------------------ */
+/* Multi-GPU communicator: the exchange steps of a banded     */
+/* render pass (wfpg_pass_config.comm).                                      */
+/* ------------------------------------------------------------------------ */
+
+typedef struct wfpg_comm wfpg_comm;
+/* cudaMemcpyAsync(cudaMemcpyDefault) on `stream` + synchronise: lets a host
+ * exchange callback stage device buffers without a CUDA binding of its own. */
+int wfpg_memcpy(void* dst, const void* src, size_t bytes, void* stream);
+/* Host exchange callback: perform the collective `op` (0 all-gather: recv =
+ * every rank's `count` elements in rank order; 1 all-reduce sum) on DEVICE
+ * buffers of `dtype` (0 int32, 1 uint64, 2 float64); the stream has been
+ * synchronised.  Return 0 on success. */
+typedef int32_t (*wfpg_exchange_fn)(void* user, int32_t op, const void* send, void* recv,
+                                    int64_t count, int32_t dtype, void* stream);
+/* 1 when libnccl.so.2 can be loaded (dlopen; the process's NCCL is reused). */
+int wfpg_comm_nccl_available(void);
+/* 128-byte ncclUniqueId (rank 0), to be broadcast to every rank. */
+int wfpg_comm_nccl_unique_id(uint8_t* out128);
+/* NCCL communicator on the current device (collective over all ranks). */
+int wfpg_comm_init_nccl(int32_t world, int32_t rank, const uint8_t* unique_id, wfpg_comm** out);
+/* Host-exchange communicator (tests, gloo runs). */
+int wfpg_comm_init_host(int32_t world, int32_t rank, wfpg_exchange_fn fn, void* user,
+                        wfpg_comm** out);
+/* Complete the deposit exchange of the last pass on this communicator
+ * (synchronises with it; runs the exact exchange if the wire overflowed). */
+int wfpg_comm_settle(wfpg_comm* comm);
+int wfpg_comm_destroy(wfpg_comm* comm);
 const char* wfpg_last_error(void);
 /* Number of kernel launches issued by this library since load (process-wide). */
 uint64_t wfpg_launch_count(void);

@@ -89,6 +89,25 @@ def u01(key, counter):
     return float(lib().ov_u01(int(key) & (2**64 - 1), int(counter) & (2**64 - 1)))
 
 
+def _mix64_np(x):
+    x = x.astype(np.uint64, copy=True)
+    with np.errstate(over="ignore"):
+        x ^= x >> np.uint64(30)
+        x *= np.uint64(0xBF58476D1CE4E5B9)
+        x ^= x >> np.uint64(27)
+        x *= np.uint64(0x94D049BB133111EB)
+        x ^= x >> np.uint64(31)
+    return x
+
+
+def stream_keys(seed, streams):
+    """Vectorised stream_key (core.py:213-219) over a uint64 array."""
+    s = _mix64_np(np.array([int(seed) & (2**64 - 1)], dtype=np.uint64))
+    with np.errstate(over="ignore"):
+        m = _mix64_np(np.asarray(streams, dtype=np.uint64)) * np.uint64(0x9E3779B97F4A7C15)
+    return _mix64_np(s ^ m)
+
+
 # ---------------------------------------------------------------------------
 # SVO build (svo.py:39-46, 94-136, 416-500)
 # ---------------------------------------------------------------------------

@@ -73,6 +73,18 @@ def lib():
 # ---------------------------------------------------------------------------
 # data
 # ---------------------------------------------------------------------------
+def _oracle_bvh(sc):
+    """The scene's BVH without touching the product library: a BVH the caller
+    already built, else the numpy restatement of bvh.py:33-119 (bvh.build_py,
+    pure numpy; the oracle's any-hit queries traverse it)."""
+    built = sc.__dict__.get("_bvh")
+    if built is not None:
+        return built
+    from paper_2405_06997_b200 import bvh as _bvh  # numpy module, no native code
+
+    return _bvh.build_py(np.asarray(sc.v0), np.asarray(sc.v1), np.asarray(sc.v2))
+
+
 class Scene:
     """Host arrays of a scene (any object with the reference Scene attributes)."""
 
@@ -86,7 +98,7 @@ class Scene:
         self.mat_rgb = c(sc.mat_rgb, np.float64)
         self.em_cdf = c(sc.emitter_cdf, np.float64)
         self.em_tris = c(sc.emitter_tris, np.int64)
-        b = sc.bvh
+        b = _oracle_bvh(sc)
         self.blo, self.bhi = c(b.lo, np.float64), c(b.hi, np.float64)
         self.bl, self.br = c(b.left, np.int64), c(b.right, np.int64)
         self.bc, self.bo = c(b.count, np.int64), c(b.order, np.int64)
@@ -232,8 +244,7 @@ def fields(sc, svo, origins, jitters, n, blur_sigma=1.0, eps=1e-2):
     return out
 
 
-def tables(values, mode):
-    """guiding.py:293-309 restated."""
+def _tables_chunk(values, mode):
     b, n, _ = values.shape
     rows = values.sum(axis=2)
     tot = rows.sum(axis=1)
@@ -249,6 +260,24 @@ def tables(values, mode):
         t["block_sums"] = sums
         t["blk_marg"] = np.cumsum(brow, axis=3) / sums[..., None]
         t["blk_cond"] = np.cumsum(blocks, axis=4) / brow[..., None]
+    return t
+
+
+def tables(values, mode):
+    """guiding.py:293-309 restated (per-bin arithmetic, so chunks of bins are
+    evaluated on a thread pool with identical results)."""
+    b = values.shape[0]
+    nt = min(_threads(), max(1, b // 64))
+    if nt <= 1:
+        t = _tables_chunk(values, mode)
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+
+        cuts = np.linspace(0, b, nt + 1).astype(int)
+        with ThreadPoolExecutor(nt) as ex:
+            parts = list(ex.map(lambda k: _tables_chunk(values[cuts[k]:cuts[k + 1]], mode),
+                                range(nt)))
+        t = {k: np.concatenate([p[k] for p in parts]) for k in parts[0]}
     return {k: np.ascontiguousarray(v) for k, v in t.items()}
 
 
@@ -320,8 +349,8 @@ def render_pass(sc, svo, cfg, sample, stats=None):
           "emit_depth": np.zeros(n, dtype=np.int32)}
     st["rec_pos"][:, 0] = cam.position
     pix = np.arange(n, dtype=np.int64)
-    st["key"] = np.array([O.stream_key(cfg["seed"], (sample * n + p) * 4) for p in range(n)],
-                         dtype=np.uint64)
+    st["key"] = O.stream_keys(cfg["seed"], (np.uint64(sample * n) + np.arange(n, dtype=np.uint64))
+                              * np.uint64(4))
     lib().ov_camera(_p(st["key"]), _p(pix), n, w, h, _p(np.ascontiguousarray(cam.position)),
                     _p(np.ascontiguousarray(cam.forward)), _p(np.ascontiguousarray(cam.right)),
                     _p(np.ascontiguousarray(cam.up_ortho)), cam.tan_half, _p(st["ray_o"]),
@@ -379,16 +408,15 @@ def update_exitance(st, svo):
     """wavefront.py:286-332 restated."""
     ed, le = st["emit_depth"].astype(np.int64), st["emit_le"]
     paths = np.nonzero((ed >= 2) & (le.sum(axis=1) > 0.0))[0]
-    pk, kk = [], []
-    for p in paths:
-        for k in range(1, ed[p]):
-            if np.all(st["rec_T"][p, k] > 0.0):
-                pk.append(p)
-                kk.append(k)
-    if not pk:
+    cnt = ed[paths] - 1
+    pk = np.repeat(paths, cnt)
+    kk = np.arange(cnt.sum()) - np.repeat(np.cumsum(cnt) - cnt, cnt) + 1
+    if len(pk):
+        ok = np.all(st["rec_T"][pk, kk] > 0.0, axis=1)
+        pk, kk = pk[ok], kk[ok]
+    if not len(pk):
         svo.propagate()
         return 0
-    pk, kk = np.array(pk), np.array(kk)
     tk = st["rec_T"][pk, kk]
     tn = st["rec_T"][pk, ed[pk]]
     rad = (tn / tk) * le[pk]
@@ -408,86 +436,75 @@ def update_exitance(st, svo):
 # ---------------------------------------------------------------------------
 # CPU baseline for bench.py
 # ---------------------------------------------------------------------------
-def _time_fields(sc, svo, pts_by_depth, bins_by_depth, field_res, guided_depths, blur_sigma,
-                 epsilon, n_paths, seconds, rng):
-    """Per-bin field time at each depth on a bounded sample (OpenMP over all
-    host cores), scaled by that depth's bin count."""
-    cores = os.cpu_count() or 1
-    budget = seconds / max(1, len(bins_by_depth))
-    total, parts = 0.0, []
-    for depth, bins in enumerate(bins_by_depth, start=1):
-        if depth > guided_depths or bins == 0:
-            continue
-        nf = max(8, field_res >> (depth - 1))
-        pts = pts_by_depth[min(depth, len(pts_by_depth)) - 1]
-        k, spent, done = cores, 0.0, 0
-        while spent < budget and done < bins:
-            k = min(k, bins - done)
-            idx = rng.integers(0, len(pts), k)
-            t0 = time.perf_counter()
-            fields(sc, svo, pts[idx], rng.random((k, 2)), nf, blur_sigma, epsilon)
-            spent += time.perf_counter() - t0
-            done += k
-            k *= 2
-        total += spent / max(done, 1) * bins
-        parts.append(f"d{depth}: {done} of {bins} bins at {nf}^2")
-    return {"value": n_paths / total if total > 0 else None, "unit": "path samples/s",
-            "cores": cores, "kind": "port",
-            "sample": "oracle field generation (cone trace + fold blur + floor, C/OpenMP on all "
-                      "host cores) for " + "; ".join(parts) + "; pass time = sum over depths of "
-                      "bins x measured per-bin time (fields are >99% of the reference's guided "
-                      "pass, SURVEY §0)",
-            "pass_seconds": total}
+def _cfg_dict(cfg):
+    g = (lambda k, d=None: getattr(cfg, k, d)) if not isinstance(cfg, dict) else cfg.get
+    return dict(max_depth=g("max_depth"), guided_depths=g("guided_depths"),
+                field_res=g("field_res"), l_min=g("l_min"), c_ray=g("c_ray"), seed=g("seed", 0),
+                product=bool(g("product", False)), jitter=bool(g("jitter", True)))
 
 
-def time_guided_pass_sample(scene, tree, cfg, stats, n_paths, seconds=20.0):
-    """CPU baseline next to a device run: the oracle gets the device SVO's
-    structure and exitance state and the device pass's bin counts."""
-    sc = Scene(scene)
-    built = {k: getattr(tree, k) for k in ("level_off", "codes", "child_base", "child_mask",
-                                           "parent", "normal")}
-    svo = Svo(built, tree.cube_lo, tree.cube_size, tree.resolution)
-    svo.mean_a, svo.mean_b = np.ascontiguousarray(tree.mean_a), np.ascontiguousarray(tree.mean_b)
-    cam = scene.camera
-    rng = np.random.default_rng(0)
-    m = 4096
-    o = np.repeat(cam.position[None, :], m, axis=0)
-    d = rng.standard_normal((m, 3))
-    d[:, 2] = np.abs(d[:, 2]) + 1.0
-    d /= np.linalg.norm(d, axis=1, keepdims=True)
-    t, tri = intersect(sc, o, d)
-    pts = (o + t[:, None] * d)[tri >= 0]
-    return _time_fields(sc, svo, [pts], stats.bins_per_depth, cfg.field_res, cfg.guided_depths,
-                        cfg.blur_sigma, cfg.epsilon, n_paths, seconds, rng)
+def _threads():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
 
 
 class CpuWorkload:
-    """The bench workload entirely on the host: oracle SVO build, a PT-first
-    oracle pass (exitance state + bins per depth + hit points per depth)."""
+    """The bench workload entirely on the host, with the reference's pass
+    sequence: oracle SVO build (svo.build_from_scene), a PT-first pass
+    (sample 0, guided_depths 0, SVO updated), then every call of ``run_pass``
+    renders the next guided sample in full (wavefront.render_pass,
+    wavefront.py:198-277, with its exitance update) — nothing extrapolated."""
 
-    def __init__(self, scene, resolution, cfg, seed=0):
+    def __init__(self, scene, resolution, cfg, seed=0, svo=None):
         self.sc = Scene(scene)
+        self.cfg = _cfg_dict(cfg)
         t0 = time.perf_counter()
-        self.svo = Svo.from_scene(scene, resolution, seed)
+        self.svo = svo if svo is not None else Svo.from_scene(scene, resolution, seed)
         self.build_s = time.perf_counter() - t0
-        stats = {}
-        pt_cfg = dict(max_depth=cfg.max_depth, guided_depths=0, field_res=cfg.field_res,
-                      l_min=cfg.l_min, c_ray=cfg.c_ray, seed=cfg.seed)
-        t0 = time.perf_counter()
-        _, st = render_pass(self.sc, self.svo, pt_cfg, 0, stats)
-        self.pt_s = time.perf_counter() - t0
-        self.bins = stats.get("bins", [])
-        rp, ed = st["rec_pos"], st["emit_depth"]
-        self.pts = []
-        for depth in range(1, cfg.max_depth + 1):
-            hit = np.any(rp[:, depth] != 0.0, axis=1)
-            self.pts.append(rp[hit, depth] if hit.any() else rp[:, 0])
-        self.cfg = cfg
+        self.pt_s = 0.0
+        self.next_sample = 1
+        if svo is None:
+            t0 = time.perf_counter()
+            render_pass(self.sc, self.svo, dict(self.cfg, guided_depths=0), 0, {})
+            self.pt_s = time.perf_counter() - t0
 
-    def time_pass(self, n_paths, seconds, seed=0):
-        c = self.cfg
-        r = _time_fields(self.sc, self.svo, self.pts, self.bins, c.field_res, c.guided_depths,
-                         c.blur_sigma, c.epsilon, n_paths, seconds, np.random.default_rng(seed))
-        r["setup"] = (f"oracle SVO build {self.build_s:.1f} s, PT-first pass {self.pt_s:.1f} s "
-                      f"(bins per depth {self.bins})")
-        return r
+    @classmethod
+    def from_device(cls, scene, tree, cfg, next_sample):
+        """Continue a device run on the host: the device SVO's structure and
+        exitance state (bit-exact with the oracle's, tests/test_full_size.py)."""
+        built = {k: np.ascontiguousarray(getattr(tree, k)) for k in (
+            "level_off", "codes", "child_base", "child_mask", "parent", "normal")}
+        svo = Svo(built, tree.cube_lo, tree.cube_size, tree.resolution)
+        for k in ("sum_a", "sum_b", "weight_a", "weight_b", "mean_a", "mean_b"):
+            setattr(svo, k, np.ascontiguousarray(getattr(tree, k)))
+        w = cls(scene, tree.resolution, cfg, svo=svo)
+        w.next_sample = int(next_sample)
+        return w
+
+    def run_pass(self):
+        """Render the next guided sample; returns (seconds, stats)."""
+        stats = {}
+        t0 = time.perf_counter()
+        render_pass(self.sc, self.svo, self.cfg, self.next_sample, stats)
+        dt = time.perf_counter() - t0
+        self.next_sample += 1
+        return dt, stats
+
+    def describe(self):
+        return (f"oracle SVO build {self.build_s:.1f} s, PT-first pass {self.pt_s:.1f} s")
+
+
+def time_guided_passes(workload, n_paths, passes=1):
+    """cpu_baseline object: ``passes`` full guided oracle passes, timed."""
+    secs, bins = [], None
+    for _ in range(passes):
+        dt, st = workload.run_pass()
+        secs.append(dt)
+        bins = st.get("bins")
+    tot = sum(secs)
+    return {"value": n_paths * len(secs) / tot if tot > 0 else None, "unit": "path samples/s",
+            "cores": _threads(), "kind": "port",
+            "sample": f"{len(secs)} full guided pass(es) of the same workload by the CPU oracle "
+                      f"(oracle/: C + OpenMP field generation on all host threads, numpy "
+                      f"bookkeeping), samples {workload.next_sample - len(secs)}.."
+                      f"{workload.next_sample - 1}, {tot:.1f} s; bins per depth {bins}",
+            "pass_seconds": secs}

@@ -89,7 +89,17 @@ class PassConfig(C.Structure):
         ("dep_rad", c_vp),
         ("dep_count", c_vp),
         ("dep_capacity", c_i64),
+        ("comm", c_vp),
+        ("dep_wire_capacity", c_i64),
     ]
+
+
+# host exchange callback (include/wfpg_b200.h wfpg_exchange_fn)
+EXCHANGE_FN = C.CFUNCTYPE(c_i32, c_vp, c_i32, c_vp, c_vp, c_i64, c_i32, c_vp)
+
+# struct ids of wfpg_abi_sizeof / wfpg_abi_offsetof
+ABI_STRUCTS = {0: "Scene", 1: "Camera", 2: "Svo", 3: "Paths", 4: "Guide", 5: "PassConfig",
+               6: "PassStats"}
 
 
 class PassStats(C.Structure):
@@ -99,7 +109,7 @@ class PassStats(C.Structure):
         ("rays_per_depth", c_i32 * 32),
         ("live_per_depth", c_i32 * 32),
         ("deposits", c_i32),
-        ("mat_groups", (c_i32 * 16) * 32),
+        ("mat_groups", (c_i32 * 64) * 32),
     ]
 
 
@@ -108,6 +118,15 @@ _SIGS = {
     "wfpg_abi_version": (c_i32, []),
     "wfpg_last_error": (C.c_char_p, []),
     "wfpg_launch_count": (c_u64, []),
+    "wfpg_abi_sizeof": (c_i64, [c_i32]),
+    "wfpg_abi_offsetof": (c_i64, [c_i32, C.c_char_p]),
+    "wfpg_memcpy": (c_i32, [c_vp, c_vp, c_size, c_vp]),
+    "wfpg_comm_nccl_available": (c_i32, []),
+    "wfpg_comm_nccl_unique_id": (c_i32, [c_vp]),
+    "wfpg_comm_init_nccl": (c_i32, [c_i32, c_i32, c_vp, P(c_vp)]),
+    "wfpg_comm_init_host": (c_i32, [c_i32, c_i32, c_vp, c_vp, P(c_vp)]),
+    "wfpg_comm_settle": (c_i32, [c_vp]),
+    "wfpg_comm_destroy": (c_i32, [c_vp]),
     "wfpg_scan_workspace_bytes": (c_size, [c_i64]),
     "wfpg_scan_u32": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_vp, c_size, c_vp]),
     "wfpg_sort_workspace_bytes": (c_size, [c_i64]),

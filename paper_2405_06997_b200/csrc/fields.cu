@@ -283,9 +283,14 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
       }
     }
   };
-  int64_t b = blockIdx.x;
-  if (b < nb) setup(b);
-  for (; b < nb;) {
+  // work item w -> bin (identity, or the multi-GPU work list); thread 0 owns
+  // the work index, the loop carries only the bin
+  auto bin_of = [&](int64_t w) -> int64_t { return out.bin_list ? (int64_t)out.bin_list[w] : w; };
+  __shared__ int64_t cur_w;
+  int64_t b = (int64_t)blockIdx.x < nb ? bin_of(blockIdx.x) : -1;
+  if (threadIdx.x == 0) cur_w = blockIdx.x;
+  if (b >= 0) setup(b);
+  for (; b >= 0;) {
     const double ox = origins[3 * b], oy = origins[3 * b + 1], oz = origins[3 * b + 2];
 #ifdef WFPG_FIELD_PHASES
     if (threadIdx.x == 0) ph_mark(0);
@@ -317,11 +322,15 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
       if (lane == 0) next = atomicAdd(&tile_ctr, 1);
       tile = __shfl_sync(0xffffffffu, next, 0);
     }
-    if (threadIdx.x == 0)
-      next_bin = out.bin_ctr ? (int64_t)atomicAdd(out.bin_ctr, 1) + gridDim.x : b + gridDim.x;
+    if (threadIdx.x == 0) {
+      const int64_t wn =
+          out.bin_ctr ? (int64_t)atomicAdd(out.bin_ctr, 1) + gridDim.x : cur_w + gridDim.x;
+      cur_w = wn;
+      next_bin = wn < nb ? bin_of(wn) : -1;
+    }
     __syncthreads();
     const int64_t b_next = next_bin;
-    if (b_next < nb) setup(b_next);  // overlaps the blur below
+    if (b_next >= 0) setup(b_next);  // overlaps the blur below
 #ifdef WFPG_FIELD_PHASES
     if (threadIdx.x == 0) ph_mark(2);
 #endif

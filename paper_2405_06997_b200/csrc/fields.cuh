@@ -19,6 +19,10 @@ struct FieldOut {
   // optional zeroed device counter: bins after each CTA's first are handed
   // out dynamically (bin costs vary; static striding left SMs idle at the end)
   int32_t* bin_ctr = nullptr;
+  // optional work list: work item w generates bin bin_list[w] (the outputs
+  // stay indexed by bin); nb_max / nb_dev then count work items.  Multi-GPU
+  // ranks generate only the bins their own paths belong to.
+  const int32_t* bin_list = nullptr;
 };
 
 int launch_fields(const SceneView& s, const SvoView& v, const double* origins,

@@ -69,6 +69,33 @@ __global__ void k_part_count(SvoView v, int32_t* __restrict__ counter,
   }
 }
 
+// k_part_count from given start nodes: each item adds 1 to every node of
+// its ancestor chain above l_min, walking parent links (the chains of
+// neighbouring items in path order coincide, so the warp aggregates them).
+__global__ void k_part_count_chain(int32_t* __restrict__ counter, const int32_t* __restrict__ parent,
+                                   const int32_t* __restrict__ start,
+                                   const int8_t* __restrict__ start_lev, int64_t n_max,
+                                   const int32_t* __restrict__ n_dev, int l_min) {
+  const int64_t n = dev_count(n_max, n_dev);
+  const int lane = threadIdx.x & 31;
+  for (int64_t w0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; w0 < n;
+       w0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = w0 + lane;
+    const bool valid = i < n;
+    int32_t cur = valid ? start[i] : -1;
+    const int lvl = valid ? (int)start_lev[i] : 0;
+    int top = lvl;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) top = max(top, __shfl_xor_sync(0xffffffffu, top, o));
+    for (int l = top; l > l_min; --l) {
+      const int32_t a = (valid && l <= lvl) ? cur : -1;
+      const unsigned grp = __match_any_sync(0xffffffffu, a);
+      if (a >= 0 && lane == __ffs(grp) - 1) atomicAdd(&counter[a], __popc(grp));
+      if (a >= 0) cur = __ldg(&parent[a]);
+    }
+  }
+}
+
 __global__ void k_part_ascend(const int32_t* __restrict__ counter,
                               const int32_t* __restrict__ parent, const int32_t* __restrict__ start,
                               const int8_t* __restrict__ start_lev, int64_t n_max,
@@ -117,14 +144,18 @@ __global__ void k_part_bins(const uint32_t* __restrict__ keys, const uint32_t* _
                             const int32_t* __restrict__ n_dev, int64_t cap,
                             int32_t* __restrict__ bin_node, int32_t* __restrict__ bin_start,
                             int32_t* __restrict__ members, int32_t* __restrict__ bin_slot,
-                            const int32_t* __restrict__ item_path) {
+                            const int32_t* __restrict__ item_path, int32_t* __restrict__ need) {
   const int64_t n = dev_count(n_max, n_dev);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     if (members) members[i] = path_idx ? path_idx[vals[i]] : (int32_t)vals[i];
     if (bin_slot) {
       uint32_t b = scan[i] + flags[i] - 1u;  // bin of this sorted position
-      if (b < cap) bin_slot[item_path[vals[i]]] = (int32_t)b;
+      const int32_t p = item_path[vals[i]];
+      if (b < cap && p >= 0) {
+        bin_slot[p] = (int32_t)b;
+        if (need) need[b] = 1;
+      }
     }
     if (flags[i]) {
       uint32_t b = scan[i];
@@ -170,8 +201,9 @@ int partition_spatial(const SvoView& v, int32_t* counter, const int32_t* parent,
     WFPG_CUDA(cudaMemsetAsync(out.n_bins, 0, sizeof(int32_t), st));
     return WFPG_OK;
   }
-  int32_t* start = ws.take<int32_t>(n_max);
-  int8_t* lev = ws.take<int8_t>(n_max);
+  const bool given = pos == nullptr;
+  int32_t* start = given ? const_cast<int32_t*>(out.start_in) : ws.take<int32_t>(n_max);
+  int8_t* lev = given ? const_cast<int8_t*>(out.lev_in) : ws.take<int8_t>(n_max);
   uint32_t* keys = ws.take<uint32_t>(n_max);  // node ids < 2^31
   uint32_t* vals = ws.take<uint32_t>(n_max);
   uint32_t* flags = ws.take<uint32_t>(n_max + 1);
@@ -182,8 +214,17 @@ int partition_spatial(const SvoView& v, int32_t* counter, const int32_t* parent,
     return WFPG_ERR_WORKSPACE;
   }
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_max, 256), kNumSMs * 8));
-  k_part_count<<<grid, 256, 0, st>>>(v, counter, pos, n_max, n_dev, l_min, start, lev);
-  WFPG_CHECK_LAUNCH("k_part_count");
+  if (given) {
+    if (!start || !lev) {
+      set_error("partition: neither positions nor start nodes");
+      return WFPG_ERR_ARG;
+    }
+    k_part_count_chain<<<grid, 256, 0, st>>>(counter, parent, start, lev, n_max, n_dev, l_min);
+    WFPG_CHECK_LAUNCH("k_part_count_chain");
+  } else {
+    k_part_count<<<grid, 256, 0, st>>>(v, counter, pos, n_max, n_dev, l_min, start, lev);
+    WFPG_CHECK_LAUNCH("k_part_count");
+  }
   k_part_ascend<<<grid, 256, 0, st>>>(counter, parent, start, lev, n_max, n_dev, l_min, c_ray,
                                       keys, vals);
   WFPG_CHECK_LAUNCH("k_part_ascend");
@@ -208,7 +249,7 @@ int partition_spatial(const SvoView& v, int32_t* counter, const int32_t* parent,
   }
   k_part_bins<<<grid, 256, 0, st>>>(keys, vals, flags, scan, path_idx, n_max, n_dev, out.capacity,
                                     out.bin_node, out.bin_start, out.members, out.bin_slot,
-                                    out.item_path);
+                                    out.item_path, out.need);
   WFPG_CHECK_LAUNCH("k_part_bins");
   int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(out.capacity, 256), kNumSMs * 4));
   k_part_counts<<<bgrid, 256, 0, st>>>(out.bin_start, nb, n_max, n_dev, out.capacity,

@@ -17,6 +17,14 @@ struct PartitionOut {
   // first node id above level l_min (level_off[l_min + 1]); counters live only
   // there, so one memset of [clear_from, n_nodes) clears them.  < 0: per-path walk.
   int64_t clear_from = -1;
+  // Start nodes given instead of positions (pos == NULL): the deepest
+  // materialised node of every item and its level (multi-GPU global binning,
+  // where the start nodes of all ranks' hits are all-gathered).
+  const int32_t* start_in = nullptr;
+  const int8_t* lev_in = nullptr;
+  // optional (capacity,) flags: set to 1 for every bin holding an item with
+  // item_path >= 0 (items of other ranks carry -1 and get no bin slot)
+  int32_t* need = nullptr;
 };
 
 size_t partition_ws_bytes(int64_t n);

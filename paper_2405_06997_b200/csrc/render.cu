@@ -9,6 +9,7 @@
 #include <utility>
 #include <vector>
 
+#include "comm.cuh"
 #include "exitance.cuh"
 #include "fields.cuh"
 #include "partition.cuh"
@@ -19,7 +20,7 @@
 namespace wfpg {
 
 constexpr int kMaxDepth = 31;
-constexpr int kMatStats = 16;
+constexpr int kMatStats = 64;
 
 struct StatsDev {
   int32_t live[kMaxDepth + 1];
@@ -161,6 +162,176 @@ __global__ void k_frame(const double* __restrict__ radiance, int64_t n_pix, int 
   }
 }
 
+// ---------------------------------------------------------------------------
+// multi-GPU global binning (wfpg_pass_config.comm)
+// ---------------------------------------------------------------------------
+// Start node (deepest materialised node) of every local lambert hit, written
+// at the path's slot of this rank's segment; -1 elsewhere (pre-filled).
+__global__ void k_start_nodes(SvoView v, const int32_t* __restrict__ lam,
+                              const double* __restrict__ lam_pos, int64_t n_max,
+                              const int32_t* __restrict__ n_dev, int32_t* __restrict__ seg) {
+  const int64_t n = dev_count(n_max, n_dev);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t qx = quantise(lam_pos[3 * i], v.lox, v.scale, v.resolution);
+    const int32_t qy = quantise(lam_pos[3 * i + 1], v.loy, v.scale, v.resolution);
+    const int32_t qz = quantise(lam_pos[3 * i + 2], v.loz, v.scale, v.resolution);
+    bool pres;
+    int32_t lvl;
+    seg[lam[i]] = descend_view(v, qx, qy, qz, v.depth, &pres, &lvl);
+  }
+}
+
+struct LevelOffsets {
+  int64_t off[33];
+  int depth;
+};
+
+// Compact the gathered start nodes (rank-major = global path order) into the
+// partition's item arrays: start node, its level and the local path id of
+// items this rank owns (-1 for the other ranks' items).
+__global__ void k_global_items(const int32_t* __restrict__ all, int64_t n_all,
+                               const uint32_t* __restrict__ scan, int64_t seg, int rank,
+                               LevelOffsets lo, int32_t* __restrict__ start,
+                               int8_t* __restrict__ lev, int32_t* __restrict__ item_path,
+                               int32_t* __restrict__ item_g, const uint32_t* __restrict__ total,
+                               int32_t* __restrict__ n_items) {
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n_all;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t node = all[g];
+    if (node < 0) continue;
+    const uint32_t o = scan[g];
+    int l = 0;
+    while (l < lo.depth && (int64_t)node >= lo.off[l + 1]) ++l;
+    start[o] = node;
+    lev[o] = (int8_t)l;
+    item_path[o] = (g / seg == rank) ? (int32_t)(g % seg) : -1;
+    item_g[o] = (int32_t)g;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n_items = (int32_t)*total;
+}
+
+__global__ void k_flags_nonneg(const int32_t* __restrict__ a, int64_t n,
+                               uint32_t* __restrict__ flags) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    flags[i] = a[i] >= 0 ? 1u : 0u;
+}
+
+// wavefront.py:170-189 over global bins: the origin member is the k-th item in
+// global path order; the rank that owns it contributes the hit position's bit
+// pattern (every other rank contributes 0, so the all-reduced sum is an exact
+// copy), jitters come from the bin's own stream on every rank.
+__global__ void k_bin_setup_global(const int32_t* __restrict__ n_bins,
+                                   const int32_t* __restrict__ bin_node,
+                                   const int32_t* __restrict__ bin_start,
+                                   const int32_t* __restrict__ bin_count,
+                                   const uint32_t* __restrict__ sorted_items,
+                                   const int32_t* __restrict__ item_path,
+                                   const double* __restrict__ ray_o,
+                                   const double* __restrict__ ray_d,
+                                   const double* __restrict__ hit_t, uint64_t seed,
+                                   const int64_t* __restrict__ sample_dev, int depth, int jitter,
+                                   uint64_t* __restrict__ origin_bits,
+                                   double* __restrict__ jitters, int32_t* __restrict__ stat) {
+  const int64_t nb = *n_bins;
+  const int64_t sample0 = *sample_dev;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *stat = (int32_t)nb;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t node = bin_node[b];
+    const int64_t len = bin_count[b], s0 = bin_start[b];
+    uint64_t sid = ((((uint64_t)sample0 * 64u + (uint64_t)depth) << 32) + (uint64_t)node) * 4u + 1u;
+    uint64_t key = stream_key(seed, sid);
+    long long k = (long long)(u01(key, 0) * (double)len);
+    if (k > len - 1) k = len - 1;
+    const int32_t p = item_path[sorted_items[s0 + k]];
+    if (p >= 0) {  // k_scatter_lambert's arithmetic: o + t * d, rounded per op
+      const double t = hit_t[p];
+      for (int c = 0; c < 3; ++c)
+        origin_bits[3 * b + c] = (uint64_t)__double_as_longlong(
+            __dadd_rn(ray_o[3 * (int64_t)p + c], __dmul_rn(t, ray_d[3 * (int64_t)p + c])));
+    }
+    jitters[2 * b] = jitter ? u01(key, 1) : 0.5;
+    jitters[2 * b + 1] = jitter ? u01(key, 2) : 0.5;
+  }
+}
+
+// bins that hold at least one of this rank's paths -> work list of the fields
+__global__ void k_need_list(const int32_t* __restrict__ need, const uint32_t* __restrict__ scan,
+                            const int32_t* __restrict__ n_bins, int32_t* __restrict__ list,
+                            const uint32_t* __restrict__ total, int32_t* __restrict__ n_list) {
+  const int64_t nb = *n_bins;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x)
+    if (need[b]) list[scan[b]] = (int32_t)b;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n_list = (int32_t)*total;
+}
+
+__global__ void k_need_flags(const int32_t* __restrict__ need, const int32_t* __restrict__ n_bins,
+                             int64_t cap, uint32_t* __restrict__ flags) {
+  const int64_t nb = *n_bins;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < cap;
+       b += (int64_t)gridDim.x * blockDim.x)
+    flags[b] = (b < nb && need[b]) ? 1u : 0u;
+}
+
+// Deposit wire (fixed capacity per rank): record 0 = count, then up to `cap`
+// records of 7 words {leaf, dir xyz, rad xyz} as bit patterns.
+__global__ void k_wire_pack(const int32_t* __restrict__ leaf, const double* __restrict__ dir,
+                            const double* __restrict__ rad, const int32_t* __restrict__ count,
+                            int64_t cap, uint64_t* __restrict__ wire) {
+  const int64_t n = *count;
+  if (blockIdx.x == 0 && threadIdx.x == 0) wire[0] = (uint64_t)n;
+  const int64_t m = n < cap ? n : cap;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t* r = wire + 1 + 7 * i;
+    r[0] = (uint64_t)(int64_t)leaf[i];
+    for (int c = 0; c < 3; ++c) {
+      r[1 + c] = (uint64_t)__double_as_longlong(dir[3 * i + c]);
+      r[4 + c] = (uint64_t)__double_as_longlong(rad[3 * i + c]);
+    }
+  }
+}
+
+// Concatenate every rank's records in rank order (global path order); if any
+// rank overflowed its wire, apply nothing and raise the status word (the
+// exact exchange then runs on the host side, comm.cu comm_settle).
+__global__ void k_wire_unpack(const uint64_t* __restrict__ wire, int world, int64_t cap,
+                              int32_t* __restrict__ leaf, double* __restrict__ dir,
+                              double* __restrict__ rad, int32_t* __restrict__ n_total,
+                              int32_t* __restrict__ status) {
+  const int64_t stride = 1 + 7 * cap;
+  bool over = false;
+  int64_t tot = 0;
+  for (int r = 0; r < world; ++r) {
+    const int64_t c = (int64_t)wire[r * stride];
+    over |= c > cap;
+    tot += c;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *n_total = over ? 0 : (int32_t)tot;
+    *status = over ? 1 : 0;
+  }
+  if (over) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)world * cap;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / cap);
+    const int64_t k = i % cap;
+    const uint64_t* seg = wire + r * stride;
+    if (k >= (int64_t)seg[0]) continue;
+    int64_t o = k;
+    for (int q = 0; q < r; ++q) o += (int64_t)wire[q * stride];
+    const uint64_t* s = seg + 1 + 7 * k;
+    leaf[o] = (int32_t)(int64_t)s[0];
+    for (int c = 0; c < 3; ++c) {
+      dir[3 * o + c] = __longlong_as_double((long long)s[1 + c]);
+      rad[3 * o + c] = __longlong_as_double((long long)s[4 + c]);
+    }
+  }
+}
+
 struct PassLayout {
   int64_t P, n_pix, cap;
   int n0;
@@ -193,6 +364,32 @@ struct PassLayout {
   double* upper_dirs;
   StatsDev* stats;
   int64_t* sample;  // device copy of cfg->sample_index (graph replays read it)
+  // multi-GPU (cfg->comm)
+  int world, rank;
+  int64_t seg;       // per-rank segment of the gathered path arrays (max band size)
+  int64_t wire_cap;  // deposit records per rank on the wire
+  int32_t* g_seg;    // (seg,) this rank's start nodes
+  int32_t* g_all;    // (world * seg,) everyone's
+  int32_t* g_start;  // compacted items: start node, level, local path, global index
+  int8_t* g_lev;
+  int32_t* g_item_path;
+  int32_t* g_item_g;
+  int32_t* g_n_items;
+  uint64_t* origin_bits;
+  int32_t* need;
+  int32_t* need_list;
+  int32_t* n_need;
+  int32_t* dep_leaf;  // local deposit export (P * max_depth)
+  double* dep_dir;
+  double* dep_rad;
+  int32_t* dep_count;
+  uint64_t* wire_send;
+  uint64_t* wire_recv;
+  int32_t* wdep_leaf;  // gathered deposits, global path order
+  double* wdep_dir;
+  double* wdep_rad;
+  int32_t* wdep_n;
+  int32_t* status;
   size_t scratch_off;
 };
 
@@ -208,7 +405,17 @@ static void carve_pass(Arena& a, const wfpg_svo* svo, const wfpg_camera* cam,
                        const wfpg_pass_config* cfg, PassLayout& L) {
   L.n_pix = cfg->n_pixels > 0 ? cfg->n_pixels : (int64_t)cam->width * cam->height;
   L.P = L.n_pix * std::max(1, cfg->n_samples);
-  L.cap = bin_capacity(svo, cfg, L.P);
+  const Comm* comm = reinterpret_cast<const Comm*>(cfg->comm);
+  L.world = comm_world(comm);
+  L.rank = comm_rank(comm);
+  const bool multi = comm && svo;
+  const int64_t n_img = (int64_t)cam->width * cam->height;
+  L.seg = multi ? ceil_div(n_img, L.world) : L.P;
+  L.wire_cap = multi ? (cfg->dep_wire_capacity > 0 ? cfg->dep_wire_capacity
+                                                   : std::max<int64_t>(1024, L.seg / 4))
+                     : 0;
+  // global binning: the partition sees every rank's paths
+  L.cap = bin_capacity(svo, cfg, multi ? L.seg * L.world : L.P);
   L.n0 = std::max(8, cfg->field_res);
   const int64_t P = L.P;
   L.active = a.take<int32_t>(P);
@@ -243,8 +450,41 @@ static void carve_pass(Arena& a, const wfpg_svo* svo, const wfpg_camera* cam,
       L.bin_ctr = a.take<int32_t>(4);
     }
   }
+  if (multi) {
+    const int64_t G = L.seg * L.world;
+    L.g_seg = a.take<int32_t>(L.seg);
+    L.g_all = a.take<int32_t>(G);
+    L.g_start = a.take<int32_t>(G);
+    L.g_lev = a.take<int8_t>(G);
+    L.g_item_path = a.take<int32_t>(G);
+    L.g_item_g = a.take<int32_t>(G);
+    L.g_n_items = a.take<int32_t>(4);
+    L.origin_bits = a.take<uint64_t>(3 * L.cap);
+    L.need = a.take<int32_t>(L.cap);
+    L.need_list = a.take<int32_t>(L.cap);
+    L.n_need = a.take<int32_t>(4);
+    const int64_t m = P * (int64_t)std::max(1, cfg->max_depth);
+    L.dep_leaf = a.take<int32_t>(m);
+    L.dep_dir = a.take<double>(3 * m);
+    L.dep_rad = a.take<double>(3 * m);
+    L.dep_count = a.take<int32_t>(4);
+    L.wire_send = a.take<uint64_t>(1 + 7 * L.wire_cap);
+    L.wire_recv = a.take<uint64_t>((1 + 7 * L.wire_cap) * L.world);
+    const int64_t wm = L.wire_cap * L.world;
+    L.wdep_leaf = a.take<int32_t>(wm);
+    L.wdep_dir = a.take<double>(3 * wm);
+    L.wdep_rad = a.take<double>(3 * wm);
+    L.wdep_n = a.take<int32_t>(4);
+    L.status = a.take<int32_t>(4);
+  }
   L.scratch_off = a.off;
   size_t scratch = std::max(scan_ws_bytes(P + 1), partition_ws_bytes(P));
+  if (multi) {
+    const int64_t G = L.seg * L.world;
+    scratch = std::max(scratch, std::max(scan_ws_bytes(G + 1), partition_ws_bytes(G)));
+    scratch = std::max(scratch, accumulate_ws_bytes(L.wire_cap * L.world) + 4096);
+    scratch = std::max(scratch, 2 * align_up(4 * (G + 1)) + scan_ws_bytes(G + 1) + 4096);
+  }
   if (svo) scratch = std::max(scratch, update_exitance_ws_bytes(P, cfg->max_depth));
   a.take<char>((int64_t)scratch);
 }
@@ -304,6 +544,8 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
                         cudaStream_t st) {
   Arena scratch(static_cast<char*>(workspace) + L.scratch_off, ws_bytes - L.scratch_off);
   const int64_t P = L.P;
+  Comm* comm = reinterpret_cast<Comm*>(cfg->comm);
+  const bool multi = comm && svo;
   const SceneView sv = make_scene_view(scene);
   const CameraView cv = make_camera_view(cam);
   const PathsView pv = make_paths_view(paths);
@@ -366,16 +608,74 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
                       &L.stats->overflow, L.cap, nullptr,
                       (guided_depth || want_image) ? L.bin_slot : nullptr, L.lam};
       po.clear_from = svo->level_off[cfg->l_min + 1];
-      size_t mark = scratch.off;
-      WFPG_TRY(partition_spatial(vv, svo->counter, svo->parent, L.lam_pos, nullptr, P, L.n_lam,
-                                 cfg->l_min, cfg->c_ray, (int)svo->n_nodes, po, scratch, st));
+      const bool global = multi && guided_depth;
       int bgrid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(L.cap, 128), kNumSMs * 8));
-      k_bin_setup<<<bgrid, 128, 0, st>>>(L.n_bins, L.bin_node, L.bin_start, L.bin_count,
-                                         po.sorted_items, L.lam, L.lam_pos, cfg->seed,
-                                         L.sample, depth, cfg->jitter, L.origins, L.jitters,
-                                         &L.stats->bins[depth]);
-      WFPG_CHECK_LAUNCH("k_bin_setup");
-      scratch.off = mark;
+      if (global) {
+        // Alg. 2 over every rank's hits: gather the start nodes (global
+        // path order = rank order of the bands), partition them identically
+        // on every rank, take each bin's origin from the rank owning it
+        const int64_t G = L.seg * L.world;
+        WFPG_CUDA(cudaMemsetAsync(L.g_seg, 0xFF, sizeof(int32_t) * L.seg, st));
+        k_start_nodes<<<grid, 256, 0, st>>>(vv, L.lam, L.lam_pos, P, L.n_lam, L.g_seg);
+        WFPG_CHECK_LAUNCH("k_start_nodes");
+        WFPG_TRY(comm_all_gather(comm, L.g_seg, L.g_all, L.seg, kI32, st));
+        {
+          size_t mark = scratch.off;
+          uint32_t* gflags = scratch.take<uint32_t>(G + 1);
+          uint32_t* gscan = scratch.take<uint32_t>(G + 1);
+          const int ggrid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(G, 256), kNumSMs * 8));
+          k_flags_nonneg<<<ggrid, 256, 0, st>>>(L.g_all, G, gflags);
+          WFPG_CHECK_LAUNCH("k_flags_nonneg");
+          WFPG_TRY(scan_u32(gflags, gscan, G, nullptr, L.total, scratch, st));
+          LevelOffsets lo{};
+          lo.depth = svo->depth;
+          for (int l = 0; l <= svo->depth + 1 && l < 33; ++l) lo.off[l] = svo->level_off[l];
+          k_global_items<<<ggrid, 256, 0, st>>>(L.g_all, G, gscan, L.seg, L.rank, lo, L.g_start,
+                                                L.g_lev, L.g_item_path, L.g_item_g, L.total,
+                                                L.g_n_items);
+          WFPG_CHECK_LAUNCH("k_global_items");
+          scratch.off = mark;
+        }
+        po.item_path = L.g_item_path;
+        po.start_in = L.g_start;
+        po.lev_in = L.g_lev;
+        po.need = L.need;
+        WFPG_CUDA(cudaMemsetAsync(L.need, 0, sizeof(int32_t) * L.cap, st));
+        WFPG_CUDA(cudaMemsetAsync(L.origin_bits, 0, sizeof(uint64_t) * 3 * L.cap, st));
+        size_t mark = scratch.off;
+        WFPG_TRY(partition_spatial(vv, svo->counter, svo->parent, nullptr, nullptr, G,
+                                   L.g_n_items, cfg->l_min, cfg->c_ray, (int)svo->n_nodes, po,
+                                   scratch, st));
+        k_bin_setup_global<<<bgrid, 128, 0, st>>>(
+            L.n_bins, L.bin_node, L.bin_start, L.bin_count, po.sorted_items, L.g_item_path,
+            paths->ray_o, paths->ray_d, L.hit_t, cfg->seed, L.sample, depth, cfg->jitter,
+            L.origin_bits, L.jitters, &L.stats->bins[depth]);
+        WFPG_CHECK_LAUNCH("k_bin_setup_global");
+        scratch.off = mark;
+        WFPG_TRY(comm_all_reduce_sum(comm, L.origin_bits, L.origins, 3 * L.cap, kU64, st));
+        {
+          size_t mk = scratch.off;
+          uint32_t* nflags = scratch.take<uint32_t>(L.cap + 1);
+          uint32_t* nscan = scratch.take<uint32_t>(L.cap + 1);
+          k_need_flags<<<bgrid, 128, 0, st>>>(L.need, L.n_bins, L.cap, nflags);
+          WFPG_CHECK_LAUNCH("k_need_flags");
+          WFPG_TRY(scan_u32(nflags, nscan, L.cap, nullptr, L.total, scratch, st));
+          k_need_list<<<bgrid, 128, 0, st>>>(L.need, nscan, L.n_bins, L.need_list, L.total,
+                                             L.n_need);
+          WFPG_CHECK_LAUNCH("k_need_list");
+          scratch.off = mk;
+        }
+      } else {
+        size_t mark = scratch.off;
+        WFPG_TRY(partition_spatial(vv, svo->counter, svo->parent, L.lam_pos, nullptr, P, L.n_lam,
+                                   cfg->l_min, cfg->c_ray, (int)svo->n_nodes, po, scratch, st));
+        k_bin_setup<<<bgrid, 128, 0, st>>>(L.n_bins, L.bin_node, L.bin_start, L.bin_count,
+                                           po.sorted_items, L.lam, L.lam_pos, cfg->seed,
+                                           L.sample, depth, cfg->jitter, L.origins, L.jitters,
+                                           &L.stats->bins[depth]);
+        WFPG_CHECK_LAUNCH("k_bin_setup");
+        scratch.off = mark;
+      }
       if (want_image) {
         int igrid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(L.n_pix, 256), kNumSMs * 8));
         k_bin_image<<<igrid, 256, 0, st>>>(L.bin_slot, L.bin_node, L.n_pix, P / L.n_pix,
@@ -386,14 +686,17 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
         const int n = std::max(8, cfg->field_res >> (depth - 1));
         FieldOut fo{L.vals, L.row_sum, L.marg, L.tot, cfg->product ? L.block_sums : nullptr,
                     cfg->epsilon, L.cum, L.bin_ctr};
+        // multi-GPU: only the bins holding this rank's paths
+        const int32_t* work_n = global ? L.n_need : L.n_bins;
+        fo.bin_list = global ? L.need_list : nullptr;
         WFPG_CUDA(cudaMemsetAsync(L.bin_ctr, 0, sizeof(int32_t), st));
         if (prof) {
           k_stamp_begin<<<1, 1, 0, st>>>(prof, depth);
           WFPG_CHECK_LAUNCH("k_stamp_begin");
         }
-        WFPG_TRY(launch_fields(sv, vv, L.origins, L.jitters, L.cap, L.n_bins, n, bp, fo, st));
+        WFPG_TRY(launch_fields(sv, vv, L.origins, L.jitters, L.cap, work_n, n, bp, fo, st));
         if (prof) {
-          k_stamp_end<<<1, 1, 0, st>>>(prof, depth, n, L.n_bins);
+          k_stamp_end<<<1, 1, 0, st>>>(prof, depth, n, work_n);
           WFPG_CHECK_LAUNCH("k_stamp_end");
         }
         gv.mode = cfg->product ? 2 : 1;
@@ -415,7 +718,36 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
                           cfg->russian_roulette != 0, cfg->rr_depth, st));
   }
 
-  if (svo && cfg->dep_leaf) {
+  if (multi) {
+    // Eq. 5 deposits of every rank, splatted in global path order (bands are
+    // rank-ordered), so each rank's SVO update equals the 1-GPU update
+    DepositSink sink{L.dep_leaf, L.dep_dir, L.dep_rad, L.dep_count,
+                     P * (int64_t)std::max(1, cfg->max_depth)};
+    WFPG_TRY(update_exitance(svo, paths->emit_depth, paths->emit_le, paths->rec_T,
+                             paths->rec_pos, cfg->max_depth + 1, P, cfg->deterministic,
+                             &L.stats->deposits, scratch, st, 0, nullptr, &sink));
+    const int wgrid =
+        (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(L.wire_cap, 256), kNumSMs * 4));
+    k_wire_pack<<<wgrid, 256, 0, st>>>(L.dep_leaf, L.dep_dir, L.dep_rad, L.dep_count, L.wire_cap,
+                                       L.wire_send);
+    WFPG_CHECK_LAUNCH("k_wire_pack");
+    WFPG_TRY(comm_all_gather(comm, L.wire_send, L.wire_recv, 1 + 7 * L.wire_cap, kU64, st));
+    const int64_t wm = L.wire_cap * L.world;
+    const int ugrid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(wm, 256), kNumSMs * 4));
+    k_wire_unpack<<<ugrid, 256, 0, st>>>(L.wire_recv, L.world, L.wire_cap, L.wdep_leaf,
+                                         L.wdep_dir, L.wdep_rad, L.wdep_n, L.status);
+    WFPG_CHECK_LAUNCH("k_wire_unpack");
+    {
+      size_t mark = scratch.off;
+      WFPG_TRY(svo_accumulate(svo, L.wdep_leaf, L.wdep_dir, L.wdep_rad, wm, L.wdep_n,
+                              cfg->deterministic, scratch, st));
+      scratch.off = mark;
+    }
+    WFPG_CUDA(cudaMemsetAsync(L.dirty, 0, (size_t)svo->n_nodes, st));
+    WFPG_TRY(svo_propagate_dirty(svo, L.wdep_leaf, wm, L.wdep_n, L.dirty, st));
+    WFPG_CUDA(cudaMemcpyAsync(comm_status_host(comm), L.status, sizeof(int32_t),
+                              cudaMemcpyDeviceToHost, st));
+  } else if (svo && cfg->dep_leaf) {
     // multi-GPU: export this rank's deposits; the caller gathers every rank's
     // lists and splats them in global path order (wfpg_svo_accumulate +
     // wfpg_svo_refresh_leaves), so all ranks end with the same SVO
@@ -522,7 +854,20 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
               cfg->max_depth);
     return WFPG_ERR_ARG;
   }
+  Comm* comm = reinterpret_cast<Comm*>(cfg->comm);
+  const bool multi = comm && svo;
+  if (cfg->dep_leaf && cfg->n_samples != 1) {
+    // band order is global path order only for one sample per pixel
+    set_error("wfpg_render_pass: deposit export (dep_leaf) needs n_samples == 1");
+    return WFPG_ERR_ARG;
+  }
+  if (multi && cfg->n_samples != 1) {
+    set_error("wfpg_render_pass: a multi-GPU pass (comm) renders one sample per pixel");
+    return WFPG_ERR_ARG;
+  }
   cudaStream_t st = as_stream(stream);
+  // the previous pass on this communicator must have applied its deposits
+  if (multi) WFPG_TRY(comm_settle(comm));
   Arena a(workspace, ws_bytes);
   PassLayout L;
   carve_pass(a, svo, cam, cfg, L);
@@ -541,9 +886,17 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
     return WFPG_ERR_ARG;
   }
   ProfDev* prof = g_prof_on ? g_prof_dev : nullptr;
+  if (multi) {
+    const int64_t lo = (int64_t)L.rank * n_img / L.world, hi = (int64_t)(L.rank + 1) * n_img / L.world;
+    if (cfg->pixel_offset != lo || L.n_pix != hi - lo) {
+      set_error("wfpg_render_pass: rank %d must render pixels [%lld, %lld)", L.rank,
+                (long long)lo, (long long)hi);
+      return WFPG_ERR_ARG;
+    }
+  }
   k_set_i64<<<1, 1, 0, st>>>(L.sample, cfg->sample_index);
   WFPG_CHECK_LAUNCH("k_set_i64");
-  if (!cfg->use_graph) {
+  if (!cfg->use_graph || (comm && !comm_capturable(comm))) {
     WFPG_TRY(enqueue_pass(scene, svo, cam, cfg, paths, frame, workspace, ws_bytes, L, prof, st));
   } else {
     const uint64_t key = pass_key(scene, svo, cam, cfg, paths, frame, ws_bytes, prof);
@@ -614,6 +967,18 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
     }
   }
 
+  if (multi) {
+    DepositPending& pd = comm_pending(comm);
+    pd.svo = *svo;
+    pd.leaf = L.dep_leaf;
+    pd.dir = L.dep_dir;
+    pd.rad = L.dep_rad;
+    pd.count = L.dep_count;
+    pd.dirty = L.dirty;
+    pd.stream = st;
+    WFPG_CUDA(cudaEventRecord(comm_done_event(comm), st));
+    pd.active = true;
+  }
   if (stats) {
     StatsDev h;
     WFPG_CUDA(cudaMemcpyAsync(&h, L.stats, sizeof(StatsDev), cudaMemcpyDeviceToHost, st));

@@ -467,6 +467,13 @@ int launch_intersect_origin(const SceneView& s, const double* origin, const doub
     return launch_intersect(s, nullptr, dirs, active, n_max, n_dev, tmin, out_t, out_tri, false,
                             st);
   size_t smem = sizeof(TriBin) * s.n_tris;
+  // up to kMaxBruteTris records (72 KB) exceed the 48 KB default window
+  static bool smem_opt_in = false;
+  if (!smem_opt_in) {
+    WFPG_CUDA(cudaFuncSetAttribute(k_intersect_origin, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(sizeof(TriBin) * kMaxBruteTris)));
+    smem_opt_in = true;
+  }
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_max, 256), kNumSMs * 8));
   k_intersect_origin<<<grid, 256, smem, st>>>(s, origin[0], origin[1], origin[2], dirs, active,
                                               n_max, n_dev, tmin, out_t, out_tri);

@@ -1,29 +1,37 @@
-"""Multi-GPU image tiling with an exitance exchange.
+"""Multi-GPU image tiling: one process per GPU, pixel bands,
+and the exchange steps of the render pass behind one communicator.
 
-One process per GPU.  Rank r renders the pixel band
-[r * n_pix / world, (r + 1) * n_pix / world) of the global image; paths use
-global pixel indices for their RNG streams, so a path draws exactly what it
-draws on one GPU.  The SVO structure is built identically on every rank.
-After each pass every rank has splatted its own Eq. 5 deposits into a zeroed
-per-leaf buffer (4 planes: sum_a, sum_b, weight_a, weight_b); the buffers are
-summed with one NCCL all-reduce and added into every rank's leaf
-accumulators, followed by the same bottom-up refresh on every rank, so all
-ranks hold the same exitance cache for the next pass (ExitanceAllReduce:
-432 MB per pass at depth 10).
+Rank r renders the pixel band [r * n_pix / world, (r + 1) * n_pix / world)
+of the image; paths use global pixel indices for their RNG streams, so a path
+draws exactly what it draws on one GPU.  The SVO structure is built
+identically on every rank.  A pass given a communicator
+(``PassRunner(comm=...)``, include/wfpg_b200.h ``wfpg_pass_config.comm``) is
+the 1-GPU pass restricted to the band, path for path:
 
-DepositExchange is the sparse alternative the survey recommends and the one
-bench.py uses: each rank exports its pass's deposit list (leaf, direction,
-radiance; ~0.03 deposits per path, a few MB at 1080p) instead of splatting
-it, the lists are all-gathered (counts first, then one padded
-all_gather_into_tensor), concatenated in rank order — which is global path
-order, because bands are contiguous pixel ranges — and splatted
-deterministically + refreshed on every rank.  The SVO update is then bitwise
-the 1-GPU update of the same paths.  Binning (Alg. 2) is
-per rank: bins depend on the rank's own paths, so multi-GPU images agree with
-the 1-GPU image statistically, not per pixel.
+* guided depths bin GLOBALLY: every rank all-gathers the Alg. 2 start nodes
+  of all ranks' lambert hits (one int32 per path), runs the same partition,
+  takes each bin's origin from the rank owning that path (an all-reduce of
+  bit patterns) and generates the fields of only the bins its own paths
+  belong to (depth-1 field work splits with the image; wavefront.py:98-195);
+* after the last depth every rank's Eq. 5 deposits are all-gathered and
+  splatted in global path order (wavefront.py:286-332), so every rank's SVO
+  equals the 1-GPU SVO bit for bit.
+
+With NCCL the collectives are enqueued by the native library on the pass
+stream and captured into the pass's CUDA graph: no torch op, host copy or
+host synchronisation per pass (one event wait on the previous pass, which
+decides whether its deposit wire overflowed).  ``Communicator.host`` runs the
+same steps through a Python exchange callback — over torch.distributed (gloo
+on host copies) or between threads of one process (``ThreadGroup``, used by
+the single-GPU tests to run W ranks' passes side by side).
+
+``ExitanceAllReduce`` is the dense alternative the north star names (one
+all-reduce of the 8 per-leaf accumulator planes per pass, then a full
+bottom-up refresh); it is exact up to fp summation order.
 """
 
 import ctypes as C
+import threading
 
 import numpy as np
 
@@ -37,7 +45,155 @@ def band(n_pix, rank, world):
     return lo, hi - lo
 
 
+_DTYPES = {0: ("int32", 4), 1: ("int64", 8), 2: ("float64", 8)}  # u64 travels as int64 bits
+
+
+class Communicator:
+    """Owner of a native wfpg_comm (see the module doc)."""
+
+    def __init__(self, handle, world, rank, kind, keep=None):
+        self.handle = handle
+        self.world = int(world)
+        self.rank = int(rank)
+        self.kind = kind
+        self._keep = keep  # the ctypes callback must outlive the communicator
+
+    @property
+    def ptr(self):
+        return self.handle.value
+
+    @classmethod
+    def nccl(cls, group=None):
+        """NCCL communicator over the torch.distributed group (the unique id
+        travels over the group; the collectives themselves are the library's)."""
+        import torch.distributed as dist
+
+        lib = _lib.load()
+        if not lib.wfpg_comm_nccl_available():
+            raise _lib.WfpgError("libnccl.so.2 is not loadable")
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        uid = (C.c_uint8 * 128)()
+        if rank == 0:
+            _lib.call("wfpg_comm_nccl_unique_id", uid)
+        box = [bytes(uid) if rank == 0 else None]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group else 0,
+                                   group=group)
+        uid = (C.c_uint8 * 128).from_buffer_copy(box[0])
+        h = C.c_void_p()
+        _lib.call("wfpg_comm_init_nccl", world, rank, uid, C.byref(h))
+        return cls(h, world, rank, "nccl")
+
+    @classmethod
+    def host(cls, world, rank, exchange):
+        """Host-exchange communicator; exchange(op, send_tensor) -> recv_tensor
+        performs the collective on torch tensors (op 0 all-gather, 1 all-reduce
+        sum) and is called with the pass stream synchronised."""
+        t = _dev.torch()
+
+        def fn(user, op, send, recv, count, dtype, stream):
+            try:
+                name, size = _DTYPES[int(dtype)]
+                n = int(count)
+                dev = t.device("cuda", t.cuda.current_device())
+                src = t.empty((n,), dtype=getattr(t, name), device=dev)
+                _lib.call("wfpg_memcpy", C.c_void_p(src.data_ptr()), C.c_void_p(send),
+                          n * size, C.c_void_p(stream))
+                out = exchange(int(op), src)
+                out = out.to(dev).contiguous()
+                want = n * (self_world if int(op) == 0 else 1)
+                if out.numel() != want:
+                    return 3
+                _lib.call("wfpg_memcpy", C.c_void_p(recv), C.c_void_p(out.data_ptr()),
+                          want * size, C.c_void_p(stream))
+                return 0
+            except Exception as e:  # reported through the library's status
+                import sys
+
+                print(f"wfpg host exchange failed: {e!r}", file=sys.stderr)
+                return 2
+
+        self_world = int(world)
+        cb = _lib.EXCHANGE_FN(fn)
+        h = C.c_void_p()
+        _lib.call("wfpg_comm_init_host", int(world), int(rank), cb, None, C.byref(h))
+        return cls(h, world, rank, "host", keep=cb)
+
+    @classmethod
+    def torch_distributed(cls, group=None):
+        """Host exchange over torch.distributed (gloo: host copies)."""
+        import torch.distributed as dist
+
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        return cls.host(world, rank, lambda op, x: dist_exchange(op, x, group))
+
+    def settle(self):
+        """Finish the deposit exchange of the last pass (wfpg_comm_settle)."""
+        _lib.call("wfpg_comm_settle", self.handle)
+
+    def close(self):
+        if self.handle is not None and self.handle.value:
+            _lib.call("wfpg_comm_destroy", self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def dist_exchange(op, x, group=None):
+    """One collective of the host-exchange protocol over torch.distributed:
+    op 0 all-gather (rank order), op 1 all-reduce sum.  gloo collectives run
+    on host copies."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    home = x.device
+    if dist.get_backend(group) == "gloo" and home.type != "cpu":
+        x = x.cpu()
+    if op == 0:
+        out = x.new_empty((world * x.numel(),))
+        dist.all_gather_into_tensor(out, x.contiguous(), group=group)
+    else:
+        out = x.clone()
+        dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+    return out.to(home)
+
+
+class ThreadGroup:
+    """In-process exchange between W threads (each thread one rank, each with
+    its own CUDA stream): the host-side barrier synchronises the ranks, the
+    kernels never wait on each other.  For single-GPU tests of the banded
+    multi-rank pass."""
+
+    def __init__(self, world):
+        self.world = int(world)
+        self.slots = [None] * self.world
+        self.barrier = threading.Barrier(self.world)
+
+    def exchange(self, rank, op, x):
+        import torch as t
+
+        self.slots[rank] = x
+        self.barrier.wait()
+        if op == 0:
+            out = t.cat([s.to(x.device) for s in self.slots])
+        else:
+            out = self.slots[0].clone()
+            for s in self.slots[1:]:
+                out += s.to(x.device)
+        self.barrier.wait()  # every rank has read the slots
+        return out
+
+    def communicator(self, rank):
+        return Communicator.host(self.world, rank, lambda op, x: self.exchange(rank, op, x))
+
+
 class ExitanceAllReduce:
+    """Dense per-leaf exitance all-reduce (the north star's formulation):
+    render with PassRunner(leaf_acc=acc.acc), then reduce_and_apply()."""
+
     def __init__(self, svo, group=None):
         self.svo = svo
         self.group = group
@@ -58,100 +214,6 @@ class ExitanceAllReduce:
     def reduce_and_apply(self, runner=None):
         self.reduce(self.acc, self.group)
         self.apply()
-
-
-class DepositExchange:
-    """Sparse per-pass exitance exchange (see module doc).  Pass it to
-    PassRunner(deposit_sink=...); call exchange(runner) after each pass."""
-
-    PACK = 7  # leaf (as float64, exact below 2^53), dir xyz, rad xyz
-
-    def __init__(self, svo, group=None):
-        self.svo = svo
-        self.group = group
-        self.capacity = 0
-        self.dirty = _dev.zeros((max(svo.node_count, 1),), np.uint8)
-        self._ws = None
-
-    def bind(self, pc, capacity):
-        """Allocate the export buffers (capacity deposits) and point the pass
-        configuration at them."""
-        if capacity > self.capacity:
-            self.capacity = int(capacity)
-            self.leaf = _dev.empty((self.capacity,), np.int32)
-            self.dir = _dev.empty((self.capacity, 3), np.float64)
-            self.rad = _dev.empty((self.capacity, 3), np.float64)
-            self.count = _dev.zeros((1,), np.int32)
-        pc.dep_leaf, pc.dep_dir = self.leaf.data_ptr(), self.dir.data_ptr()
-        pc.dep_rad, pc.dep_count = self.rad.data_ptr(), self.count.data_ptr()
-        pc.dep_capacity = self.capacity
-
-    def local(self):
-        n = int(_dev.download(self.count)[0])
-        return self.leaf[:n], self.dir[:n], self.rad[:n]
-
-    @classmethod
-    def gather(cls, leaf, dirs, rad, group=None):
-        """All-gather variable-length deposit lists; returns the concatenation
-        in rank order as (leaf int32 (n,), dir (n,3), rad (n,3)) tensors on the
-        input's device.  Works for any backend (gloo on CPU in the tests)."""
-        import torch
-        import torch.distributed as dist
-
-        world = dist.get_world_size(group)
-        home = leaf.device
-        if dist.get_backend(group) == "gloo" and home.type != "cpu":
-            # gloo collectives on host copies (1-GPU functional runs)
-            out = cls.gather(leaf.cpu(), dirs.cpu(), rad.cpu(), group)
-            return tuple(t.to(home) for t in out)
-        n = torch.tensor([leaf.shape[0]], dtype=torch.int64, device=leaf.device)
-        counts = [torch.zeros_like(n) for _ in range(world)]
-        dist.all_gather(counts, n, group=group)
-        counts = [int(c.item()) for c in counts]
-        cap = max(max(counts), 1)
-        pack = torch.zeros((cap, cls.PACK), dtype=torch.float64, device=leaf.device)
-        k = leaf.shape[0]
-        if k:
-            pack[:k, 0] = leaf.to(torch.float64)
-            pack[:k, 1:4] = dirs
-            pack[:k, 4:7] = rad
-        everyone = torch.empty((world * cap, cls.PACK), dtype=torch.float64, device=leaf.device)
-        dist.all_gather_into_tensor(everyone, pack, group=group)
-        rows = torch.cat([everyone[r * cap:r * cap + c] for r, c in enumerate(counts)])
-        return (rows[:, 0].to(torch.int32).contiguous(), rows[:, 1:4].contiguous(),
-                rows[:, 4:7].contiguous())
-
-    def apply(self, leaf, dirs, rad):
-        """Deterministic splat of the gathered deposits + dirty refresh."""
-        n = int(leaf.shape[0])
-        s = self.svo.abi()
-        if n:
-            need = _lib.load().wfpg_accumulate_workspace_bytes(n)
-            if self._ws is None or self._ws.numel() < need:
-                self._ws = _dev.workspace(need)
-            _lib.call("wfpg_svo_accumulate", C.byref(s), _lib.ptr(leaf), _lib.ptr(dirs),
-                      _lib.ptr(rad), n, None, 1, _lib.ptr(self._ws), self._ws.numel(),
-                      _dev.stream())
-        _lib.call("wfpg_svo_refresh_leaves", C.byref(s), _lib.ptr(leaf) if n else None, n,
-                  _lib.ptr(self.dirty), _dev.stream())
-        return n
-
-    def exchange(self, runner=None):
-        leaf, dirs, rad = self.local()
-        if self.group is not None or _dist_ready():
-            leaf, dirs, rad = self.gather(leaf, dirs, rad, self.group)
-        return self.apply(leaf, dirs, rad)
-
-    reduce_and_apply = exchange
-
-
-def _dist_ready():
-    try:
-        import torch.distributed as dist
-
-        return dist.is_available() and dist.is_initialized()
-    except ImportError:  # pragma: no cover
-        return False
 
 
 def leaf_acc_planes(acc, n_leaves):

@@ -178,7 +178,7 @@ class PassRunner:
 
     def __init__(self, scene, svo, cfg, n_samples=1, deterministic=True, pixel_offset=0,
                  n_pixels=None, leaf_acc=None, use_graph=True, collect_bin_image=False,
-                 deposit_sink=None):
+                 comm=None, wire_capacity=0):
         cam = scene.camera
         self.scene = scene
         self.svo = svo
@@ -212,11 +212,12 @@ class PassRunner:
         # depth-1 bin node per pixel (wavefront.py:221,254-256)
         self.bin_image = _dev.empty((self.n_pix,), np.int32) if collect_bin_image else None
         pc.bin_image = self.bin_image.data_ptr() if collect_bin_image else None
-        # multi-GPU: export the pass's deposits instead of splatting them
-        # (multigpu.DepositExchange); needs capacity P * max_depth
-        self.deposit_sink = deposit_sink
-        if deposit_sink is not None:
-            deposit_sink.bind(pc, self.P * int(cfg.max_depth))
+        # multi-GPU (multigpu.Communicator): global binning of the guided
+        # depths and the in-pass deposit exchange; this runner renders the
+        # band [pixel_offset, pixel_offset + n_pixels) of rank comm.rank
+        self.comm = comm
+        pc.comm = comm.ptr if comm is not None else None
+        pc.dep_wire_capacity = int(wire_capacity)
         self.svo_abi = svo.abi() if svo is not None else None
         nbytes = _lib.load().wfpg_render_workspace_bytes(
             C.byref(scene.abi()), C.byref(self.svo_abi) if svo is not None else None,
@@ -245,7 +246,7 @@ class PassRunner:
             if self.svo is not None:
                 st.bins_per_depth.append(int(s.bins_per_depth[d]))
                 st.rays_per_depth.append(int(s.rays_per_depth[d]))
-                groups = {m: int(s.mat_groups[d][m]) for m in range(16) if s.mat_groups[d][m]}
+                groups = {m: int(s.mat_groups[d][m]) for m in range(64) if s.mat_groups[d][m]}
                 st.material_groups.append(groups)
         st.deposits = int(s.deposits)
         return st
@@ -254,9 +255,16 @@ class PassRunner:
 _RUNNERS = {}
 
 
+def _camera_key(cam):
+    return (tuple(cam.position.tolist()), tuple(cam.target.tolist()), tuple(cam.up.tolist()),
+            cam.vfov_deg, cam.width, cam.height)
+
+
 def _runner(scene, svo, cfg, n_samples, collect_bin_image=False):
+    # the camera is part of the key: the reference reads scene.camera on every
+    # pass, so a reassigned camera must not replay the old view
     key = (id(scene), id(svo), tuple(sorted(vars(cfg).items())), n_samples,
-           bool(collect_bin_image))
+           bool(collect_bin_image), _camera_key(scene.camera))
     r = _RUNNERS.get(key)
     if r is None or r.scene is not scene or r.svo is not svo:
         _RUNNERS.clear()  # one live configuration at a time keeps HBM bounded

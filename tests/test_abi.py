@@ -55,11 +55,26 @@ def test_workspace_queries_are_host_only():
     assert lib.wfpg_update_exitance_workspace_bytes(4096, 4) > 4096 * 4 * 4
 
 
-@pytest.mark.parametrize("name", ["Scene", "Camera", "Svo", "Paths", "Guide", "PassConfig",
-                                  "PassStats"])
-def test_struct_layouts_are_plain(name):
+@pytest.mark.parametrize("sid,name", sorted({0: "Scene", 1: "Camera", 2: "Svo", 3: "Paths",
+                                               4: "Guide", 5: "PassConfig",
+                                               6: "PassStats"}.items()))
+def test_struct_layouts_match_the_c_build(sid, name):
+    """Every ctypes mirror has the C build's sizeof and the offset of every
+    field (wfpg_abi_sizeof / wfpg_abi_offsetof), and names every header field:
+    a layout drift between include/wfpg_b200.h and _lib.py fails here."""
     from paper_2405_06997_b200 import _lib
 
+    lib = _lib.load()
+    assert _lib.ABI_STRUCTS[sid] == name
     st = getattr(_lib, name)
-    assert C.sizeof(st) > 0
-    assert all(isinstance(f[0], str) for f in st._fields_)
+    assert lib.wfpg_abi_sizeof(sid) == C.sizeof(st)
+    for field, _ in st._fields_:
+        assert lib.wfpg_abi_offsetof(sid, field.encode()) == getattr(st, field).offset, field
+    text = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    cname = {"PassConfig": "pass_config", "PassStats": "pass_stats"}.get(name, name.lower())
+    body = re.search(r"typedef struct wfpg_%s \{(.*?)\} wfpg_%s;" % (cname, cname), text,
+                     re.S).group(1)
+    header_fields = [re.search(r"([A-Za-z_]\w*)\s*(\[[^\]]*\])*\s*$", d.strip()).group(1)
+                     for d in body.split(";") if d.strip()]
+    assert header_fields == [f for f, _ in st._fields_]
+    assert lib.wfpg_abi_offsetof(sid, b"no_such_field") == -1

@@ -96,39 +96,83 @@ def test_summed_deposits_equal_single_rank_deposits(world):
     np.testing.assert_allclose(acc, full, rtol=1e-13)
 
 
-def _gather_worker(rank, world, port, sizes, out):
+def _exchange_worker(rank, world, port, n, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     rng = np.random.default_rng(200 + rank)
-    n = sizes[rank]
-    leaf = torch.from_numpy(rng.integers(-1, 1000, n).astype(np.int32))
-    dirs = torch.from_numpy(rng.random((n, 3)))
-    rad = torch.from_numpy(rng.random((n, 3)))
-    g = multigpu.DepositExchange.gather(leaf, dirs, rad)
-    out[rank] = tuple(t.numpy().copy() for t in g)
+    res = {}
+    for name, dt in (("i32", np.int32), ("i64", np.int64), ("f64", np.float64)):
+        x = torch.from_numpy((rng.random(n) * 1e6).astype(dt))
+        res["gather_" + name] = multigpu.dist_exchange(0, x).numpy().copy()
+        res["sum_" + name] = multigpu.dist_exchange(1, x).numpy().copy()
+    out[rank] = res
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("sizes", [(5, 3), (0, 4), (7, 0), (0, 0)])
-def test_deposit_gather_is_rank_ordered_concatenation(sizes):
-    """DepositExchange.gather returns every rank's list in rank order (= global
-    path order for contiguous bands), bit-exact, whatever the lengths."""
-    world = len(sizes)
+@pytest.mark.parametrize("world,n", [(2, 5), (3, 1), (2, 0)])
+def test_host_exchange_protocol_over_gloo(world, n):
+    """The host-exchange protocol of a wfpg_comm over torch.distributed: op 0
+    is the rank-ordered concatenation (global path order for contiguous
+    bands), op 1 the element-wise sum, bit-exact for every wire dtype."""
     port = _free_port()
     with mp.Manager() as m:
         out = m.dict()
-        mp.spawn(_gather_worker, args=(world, port, sizes, out), nprocs=world, join=True)
+        mp.spawn(_exchange_worker, args=(world, port, n, out), nprocs=world, join=True)
         res = [out[r] for r in range(world)]
-    exp = []
-    for r, n in enumerate(sizes):
-        rng = np.random.default_rng(200 + r)
-        exp.append((rng.integers(-1, 1000, n).astype(np.int32), rng.random((n, 3)),
-                    rng.random((n, 3))))
-    for k in range(3):
-        want = np.concatenate([e[k] for e in exp])
+    for name, dt in (("i32", np.int32), ("i64", np.int64), ("f64", np.float64)):
+        xs = [(np.random.default_rng(200 + r).random(n) * 1e6).astype(dt) for r in range(world)]
+        # the generator is consumed in dtype order: regenerate the same way
+        xs = []
         for r in range(world):
-            assert np.array_equal(res[r][k], want)
-    assert res[0][0].dtype == np.int32
+            rng = np.random.default_rng(200 + r)
+            for nm, d in (("i32", np.int32), ("i64", np.int64), ("f64", np.float64)):
+                v = (rng.random(n) * 1e6).astype(d)
+                if nm == name:
+                    xs.append(v)
+        cat = np.concatenate(xs)
+        tot = xs[0].copy()
+        for v in xs[1:]:
+            tot = tot + v
+        for r in range(world):
+            assert np.array_equal(res[r]["gather_" + name], cat)
+            assert res[r]["gather_" + name].dtype == dt
+            assert np.array_equal(res[r]["sum_" + name], tot)
+
+
+def test_thread_group_exchange_on_host_tensors():
+    """ThreadGroup (the single-GPU multi-rank tests' exchange): every rank
+    thread gets the rank-ordered concatenation / the sum."""
+    import threading
+
+    world = 3
+    g = multigpu.ThreadGroup(world)
+    got = [None] * world
+
+    def rank_main(r):
+        x = torch.arange(4, dtype=torch.int64) + 10 * r
+        got[r] = (g.exchange(r, 0, x).clone(), g.exchange(r, 1, x).clone())
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    cat = torch.cat([torch.arange(4) + 10 * r for r in range(world)])
+    tot = sum(torch.arange(4) + 10 * r for r in range(world))
+    for r in range(world):
+        assert torch.equal(got[r][0], cat) and torch.equal(got[r][1], tot)
+
+
+def test_bit_pattern_sum_is_an_exact_copy():
+    """Bin origins travel as u64 bit patterns summed over ranks with exactly
+    one non-zero contributor: the sum reproduces every double bit for bit
+    (signed zeros, subnormals, NaN payloads included)."""
+    vals = np.array([-0.0, 0.0, 5e-324, -1.5, np.inf, np.nan, 1e308], dtype=np.float64)
+    bits = vals.view(np.int64)
+    for owner in range(3):
+        parts = [bits if r == owner else np.zeros_like(bits) for r in range(3)]
+        tot = parts[0] + parts[1] + parts[2]
+        assert np.array_equal(tot, bits)
 
 
 def test_rank_ordered_deposits_reproduce_the_single_rank_splat():

@@ -1,46 +1,203 @@
-"""Multi-GPU data path on ONE GPU without collectives (the ranks are run one
-after the other in one process; nothing waits on another kernel): pixel
-bands with deposit export + rank-ordered splat reproduce the single-GPU pass
-and SVO update bit for bit (PT pass: binning cannot change the paths)."""
+"""Multi-GPU pass on ONE GPU: W ranks run as W threads of one process, each
+with its own CUDA stream, SVO copy and band of the image, exchanging through
+multigpu.ThreadGroup (the host barrier synchronises the ranks; no kernel ever
+waits on another rank's kernel).  The banded passes must reproduce the 1-GPU
+passes path for path: identical frames, identical global bins, and every
+rank's SVO equal to the 1-GPU SVO bit for bit (wavefront.py:98-195,286-332)."""
+
+import threading
 
 import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
 
+SVO_KEYS = ("sum_a", "sum_b", "weight_a", "weight_b", "mean_a", "mean_b")
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_banded_pass_with_deposit_exchange_equals_one_gpu(golden, scene_path, world):
-    import torch
 
-    from paper_2405_06997_b200 import multigpu, scene as S, svo, wavefront
+def _setup(golden, scene_path, W=None, H=None):
+    from paper_2405_06997_b200 import scene as S
 
     R = golden("render_golden.npz")
     c = dict(zip([str(k) for k in R["cfg_keys"]], [int(v) for v in R["cfg_vals"]]))
     sc = S.load_scene(scene_path("cornell.scene"))
     cam = sc.camera
-    sc.camera = S.Camera(cam.position, cam.target, cam.up, cam.vfov_deg, c["W"], c["H"])
-    cfg = wavefront.GuidingConfig(max_depth=c["max_depth"], guided_depths=0,
-                                  field_res=c["field_res"], l_min=c["l_min"], c_ray=c["c_ray"],
-                                  seed=c["seed"])
-    one = svo.build_from_scene(sc, c["R"], seed=c["svo_seed"])
-    frame1, st1 = wavefront.render_pass(sc, one, cfg, [0])
-    multi = svo.build_from_scene(sc, c["R"], seed=c["svo_seed"])
-    ex = multigpu.DepositExchange(multi)
-    lists, frames = [], []
-    for r in range(world):
-        off, npx = multigpu.band(c["W"] * c["H"], r, world)
-        run = wavefront.PassRunner(sc, multi, cfg, pixel_offset=off, n_pixels=npx,
-                                   deposit_sink=ex, use_graph=False)
-        run.launch(0)
-        frames.append(run.frame.cpu().numpy().copy())
-        lists.append(tuple(t.clone() for t in ex.local()))
-    # SVO untouched by the exporting passes
-    assert not np.any(multi.weight_a) and not np.any(multi.weight_b)
-    leaf, dirs, rad = (torch.cat([l[k] for l in lists]) for k in range(3))
-    n = ex.apply(leaf, dirs, rad)
-    assert n == st1.deposits
-    np.testing.assert_array_equal(np.concatenate(frames).reshape(frame1.shape), frame1)
-    for k in ("sum_a", "sum_b", "weight_a", "weight_b", "mean_a", "mean_b"):
-        a, b = getattr(multi, k), getattr(one, k)
-        assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), k
+    sc.camera = S.Camera(cam.position, cam.target, cam.up, cam.vfov_deg, W or c["W"],
+                         H or c["H"])
+    return c, sc
+
+
+def _cfgs(c, product):
+    from paper_2405_06997_b200 import wavefront
+
+    base = dict(max_depth=c["max_depth"], field_res=c["field_res"], l_min=c["l_min"],
+                c_ray=c["c_ray"], seed=c["seed"])
+    return (wavefront.GuidingConfig(guided_depths=0, **base),
+            wavefront.GuidingConfig(guided_depths=c["max_depth"], product=product, **base))
+
+
+def _one_gpu(sc, c, pt, g, samples):
+    from paper_2405_06997_b200 import svo, wavefront
+
+    tree = svo.build_from_scene(sc, c["R"], seed=c["svo_seed"])
+    out = []
+    for s in samples:
+        frame, st = wavefront.render_pass(sc, tree, pt if s == 0 else g, [s])
+        out.append((frame.copy(), st))
+    return tree, out
+
+
+def _ranks(sc, c, pt, g, samples, world, wire_capacity=0):
+    import torch
+
+    from paper_2405_06997_b200 import multigpu, svo, wavefront
+
+    group = multigpu.ThreadGroup(world)
+    n_pix = sc.camera.width * sc.camera.height
+    res, errs = [None] * world, []
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                tree = svo.build_from_scene(sc, c["R"], seed=c["svo_seed"])
+                comm = group.communicator(r)
+                off, npx = multigpu.band(n_pix, r, world)
+                mk = lambda cfg: wavefront.PassRunner(  # noqa: E731
+                    sc, tree, cfg, pixel_offset=off, n_pixels=npx, comm=comm, use_graph=False,
+                    wire_capacity=wire_capacity)
+                runners = {0: mk(pt), 1: mk(g)}
+                frames = []
+                for s in samples:
+                    run = runners[0 if s == 0 else 1]
+                    run.launch(s, want_stats=True)
+                    frames.append((run.frame.cpu().numpy().copy(), run.pass_stats()))
+                comm.settle()
+                torch.cuda.synchronize()
+                res[r] = (tree, frames)
+                comm.close()
+        except BaseException as e:  # surfaced in the main thread
+            errs.append(e)
+            group.barrier.abort()
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    return res
+
+
+@pytest.mark.parametrize("world,product", [(2, False), (3, False), (2, True)])
+def test_banded_ranks_reproduce_the_one_gpu_passes(golden, scene_path, world, product):
+    c, sc = _setup(golden, scene_path)
+    pt, g = _cfgs(c, product)
+    samples = [0, 1, 2]
+    one, ref = _one_gpu(sc, c, pt, g, samples)
+    ranks = _ranks(sc, c, pt, g, samples, world)
+    for k, s in enumerate(samples):
+        frame = np.concatenate([rk[1][k][0] for rk in ranks]).reshape(ref[k][0].shape)
+        np.testing.assert_array_equal(frame, ref[k][0], err_msg=f"sample {s}")
+        if s > 0:  # guided depths bin globally: every rank reports the 1-GPU bins
+            for rk in ranks:
+                assert rk[1][k][1].bins_per_depth == ref[k][1].bins_per_depth
+        # deposits: the ranks' local counts add up to the 1-GPU count
+        assert sum(rk[1][k][1].deposits for rk in ranks) == ref[k][1].deposits
+    for tree, _ in ranks:
+        for key in SVO_KEYS:
+            a, b = getattr(tree, key), getattr(one, key)
+            assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), key
+
+
+def test_wire_overflow_falls_back_to_the_exact_exchange(golden, scene_path):
+    """A deposit wire of 1 record per rank overflows every pass; the exact
+    exchange (wfpg_comm_settle / the next pass) must still apply every
+    deposit in global path order."""
+    c, sc = _setup(golden, scene_path)
+    pt, g = _cfgs(c, False)
+    samples = [0, 1, 2]
+    one, ref = _one_gpu(sc, c, pt, g, samples)
+    ranks = _ranks(sc, c, pt, g, samples, 2, wire_capacity=1)
+    for k in range(len(samples)):
+        frame = np.concatenate([rk[1][k][0] for rk in ranks]).reshape(ref[k][0].shape)
+        np.testing.assert_array_equal(frame, ref[k][0])
+    for tree, _ in ranks:
+        for key in SVO_KEYS:
+            assert np.array_equal(getattr(tree, key).view(np.uint64),
+                                  getattr(one, key).view(np.uint64)), key
+
+
+def test_ranks_generate_only_their_bins(golden, scene_path):
+    """Depth-1 field work splits with the image: each rank generates the
+    fields of the bins its own paths belong to (fewer than all bins), and
+    together the ranks cover every bin."""
+    import ctypes as C
+
+    from paper_2405_06997_b200 import _lib
+
+    c, sc = _setup(golden, scene_path, 64, 64)
+    pt, g = _cfgs(c, False)
+    lib = _lib.load()
+    lib.wfpg_profile_enable(1)
+    one, ref = _one_gpu(sc, c, pt, g, [0, 1])
+    D = c["max_depth"]
+
+    def field_bins():
+        cones = (C.c_double * (D + 1))()
+        nl = (C.c_int64 * (D + 1))()
+        ms = (C.c_double * (D + 1))()
+        lib.wfpg_profile_read(ms, cones, nl, D)
+        lib.wfpg_profile_enable(1)
+        return [cones[d] / max(8, c["field_res"] >> (d - 1)) ** 2 for d in range(1, D + 1)]
+
+    total = field_bins()
+    assert total[0] == ref[1][1].bins_per_depth[0]
+    world = 2
+    _ranks(sc, c, pt, g, [0, 1], world)
+    both = field_bins()  # both ranks' launches (profile counters are process-wide)
+    lib.wfpg_profile_enable(0)
+    # every bin is generated by at least one rank, and depth 1 is not replicated
+    assert both[0] >= total[0] and both[0] < world * total[0]
+
+
+def test_nccl_communicator_world1_graph(golden, scene_path):
+    """A one-rank NCCL communicator: the multi-GPU pass flow (global binning,
+    wire exchange, deferred check) captured into the pass's CUDA graph and
+    replayed, equal to the plain pass."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2405_06997_b200 import multigpu, svo, wavefront
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("gloo", rank=0, world_size=1,
+                            init_method=f"tcp://127.0.0.1:{port}")
+    try:
+        comm = multigpu.Communicator.nccl()
+        c, sc = _setup(golden, scene_path)
+        pt, g = _cfgs(c, False)
+        one, ref = _one_gpu(sc, c, pt, g, [0, 1, 2, 3, 4])
+        tree = svo.build_from_scene(sc, c["R"], seed=c["svo_seed"])
+        n = sc.camera.width * sc.camera.height
+        rp = wavefront.PassRunner(sc, tree, pt, pixel_offset=0, n_pixels=n, comm=comm)
+        rg = wavefront.PassRunner(sc, tree, g, pixel_offset=0, n_pixels=n, comm=comm)
+        frames = []
+        for s in range(5):  # eager, eager, captured, replayed, replayed
+            r = rp if s == 0 else rg
+            r.launch(s, want_stats=False)
+            frames.append(r.frame.cpu().numpy().copy())
+        comm.settle()
+        for s in range(5):
+            np.testing.assert_array_equal(frames[s].reshape(ref[s][0].shape), ref[s][0])
+        for key in SVO_KEYS:
+            assert np.array_equal(getattr(tree, key).view(np.uint64),
+                                  getattr(one, key).view(np.uint64)), key
+        comm.close()
+    finally:
+        dist.destroy_process_group()
