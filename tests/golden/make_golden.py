@@ -461,6 +461,127 @@ def gen_relmse():
     save("relmse_golden.npz", **out)
 
 
+# ---------------------------------------------------------------------------
+C1_CFG = dict(W=256, H=256, R=256, svo_seed=0, max_depth=4, field_res=128, l_min=5, c_ray=512,
+              seed=0)
+
+
+def _path_record(cap, stats):
+    st = cap["state"]
+    return {"emit_depth": st["emit_depth"].astype(np.int8),
+            "rec_pos": st["rec_pos"][:, 1:].astype(np.float32),
+            "radiance": st["radiance"].astype(np.float32),
+            "bins": np.array(stats.bins_per_depth), "rays": np.array(stats.rays_per_depth),
+            "mat_groups": _mat_groups(stats)}
+
+
+def _mat_groups(stats):
+    """material_groups per depth as a dense (depths, n_mats) int64 table."""
+    n = max([max(g) + 1 for g in stats.material_groups if g] + [1])
+    out = np.zeros((len(stats.material_groups), n), dtype=np.int64)
+    for d, g in enumerate(stats.material_groups):
+        for m, k in g.items():
+            out[d, m] = k
+    return out
+
+
+def gen_c1():
+    """the primary per-path equivalence configuration:
+    Cornell 256x256, SVO R=256 (depth 8), D=4, N0=128, l_min 5, c_ray 512,
+    seed 0; pass 0 PT-first (SVO updated), then sample 1 guided plain and,
+    from the same PT-first SVO state, sample 1 guided product.  Per path:
+    emit depth, vertices 1..4 and radiance (float32), plus bins / rays /
+    material groups per depth.  ~5 min of reference time."""
+    import time
+
+    c = C1_CFG
+    sc = load_scene("cornell.scene", c["W"], c["H"])
+    tree = rsvo.build_from_scene(sc, c["R"], seed=c["svo_seed"])
+    out = {"cfg_keys": np.array(list(c)), "cfg_vals": np.array(list(c.values()))}
+    base = dict(max_depth=c["max_depth"], field_res=c["field_res"], l_min=c["l_min"],
+                c_ray=c["c_ray"], seed=c["seed"])
+    _, st0, cap0 = _capture_pass(sc, tree, wavefront.GuidingConfig(guided_depths=0, **base), 0)
+    for k, v in _path_record(cap0, st0).items():
+        out["p0_" + k] = v
+    state = _svo_state(tree)
+    for k, v in state.items():
+        out["p0_svo_" + k] = v.astype(np.float32) if k.startswith("mean") else v
+    for tag, product in (("p1", False), ("p1x", True)):
+        for k, v in state.items():
+            setattr(tree, k, v.copy())
+        t0 = time.time()
+        _, st1, cap1 = _capture_pass(
+            sc, tree, wavefront.GuidingConfig(guided_depths=c["max_depth"], product=product,
+                                              **base), 1)
+        print(tag, "pass", time.time() - t0, "s, bins", st1.bins_per_depth, flush=True)
+        for k, v in _path_record(cap1, st1).items():
+            out[f"{tag}_" + k] = v
+        out[f"{tag}_svo_weight_a"] = tree.weight_a.copy()
+        out[f"{tag}_svo_weight_b"] = tree.weight_b.copy()
+    save("c1_golden.npz", **out)
+
+
+def gen_queries():
+    """Direct parity anchors for helpers the render loop uses implicitly:
+    descend_tracked (node, present, deepest; _kernelshim.py:60-71 ->
+    _kernels.pyx:591-658), SvoCache.ancestor_chain (svo.py:326-340) and
+    PassStats.material_groups (wavefront.py:88-95,250-253)."""
+    c = RENDER_CFG
+    sc = load_scene("cornell.scene", c["W"], c["H"])
+    tree = rsvo.build_from_scene(sc, c["R"], seed=c["svo_seed"])
+    rng = np.random.default_rng(21)
+    m = 4096
+    lo, size = tree.cube_lo, tree.cube_size
+    pts = lo + size * rng.random((m, 3))
+    # plus exact voxel corners (boundary quantisation)
+    corners = lo + size * (rng.integers(0, tree.resolution, (256, 3)) / tree.resolution)
+    pts = np.concatenate([pts, corners])
+    node, present, deepest = wfpg.backend.get().descend_tracked(tree, pts)
+    out = {"desc_points": pts, "desc_node": node, "desc_present": present,
+           "desc_deepest": deepest}
+    coords = rng.integers(0, tree.resolution, (600, 3))
+    # plus the leaf coordinates of materialised leaves (full-depth chains)
+    leaf_codes = tree.codes[tree.level_off[tree.depth]:tree.level_off[tree.depth + 1]]
+    pick = rng.choice(len(leaf_codes), 200, replace=False)
+    coords = np.concatenate([coords, np.stack(core.morton_decode(leaf_codes[pick]), axis=1)])
+    chains = [tree.ancestor_chain(cc) for cc in coords]
+    out["chain_coords"] = coords
+    out["chain_len"] = np.array([len(ch) for ch in chains])
+    out["chain_flat"] = np.concatenate([np.array(ch, dtype=np.int64) for ch in chains])
+    base = dict(max_depth=c["max_depth"], field_res=c["field_res"], l_min=c["l_min"],
+                c_ray=c["c_ray"], seed=c["seed"])
+    for tag, g, sample in (("p0", 0, 0), ("p1", c["max_depth"], 1)):
+        _, st = wavefront.render_pass(sc, tree, wavefront.GuidingConfig(guided_depths=g, **base),
+                                      [sample])
+        out[tag + "_mat_groups"] = _mat_groups(st)
+    # a mirror scene: every material kind (lambert, mirror, emitter) appears
+    sc2 = load_scene("cornell.scene", 48, 40)
+    tree2 = rsvo.build_from_scene(sc2, 64, seed=0)
+    _, st = wavefront.render_pass(sc2, tree2, wavefront.GuidingConfig(guided_depths=0, **base), [0])
+    out["w48_mat_groups"] = _mat_groups(st)
+    save("queries_golden.npz", **out)
+
+
+def gen_r1024():
+    """Reference digests of the C2 SVO (cornell.scene, R=1024, seed 0), the
+    headline depth (~4-5 min in the reference)."""
+    import time
+
+    sc = load_scene("cornell.scene")
+    t0 = time.time()
+    frags = rsvo.voxelize(sc, 1024)
+    lo, side = rsvo.scene_cube(sc)
+    tree = rsvo.build_octree(frags, lo, side, 1024, seed=0)
+    print("R=1024 build", time.time() - t0, "s", flush=True)
+    out = {"frags": np.array(len(frags.tris)), "nodes": np.array(tree.node_count),
+           "level_off": np.asarray(tree.level_off)}
+    for k in ("codes", "child_base", "child_mask", "parent", "normal"):
+        out[k] = np.array(digest(getattr(tree, k)))
+    out["frag_coords"] = np.array(digest(frags.coords))
+    out["frag_tris"] = np.array(digest(frags.tris))
+    save("r1024_golden.npz", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["svo"]
     for w in which:
