@@ -248,6 +248,12 @@ typedef struct wfpg_pass_config {
    * (their bins only feed PassStats). */
   struct wfpg_comm* comm;
   int64_t dep_wire_capacity;
+  /* Optional (n_samples,) int64 device array: the sample index of each
+   * sample slot of the pass (any list, wavefront.py:207-215: path stream
+   * (sample_list[s] * n_img + pixel) * 4).  NULL: sample_index + s.  The
+   * bins' streams use sample_index, the list's first entry, as the
+   * reference does (samples[0], wavefront.py:264). */
+  const int64_t* sample_list;
 } wfpg_pass_config;
 
 /* Per-pass statistics returned to the host: wavefront.py:81-85 (PassStats). */

@@ -91,6 +91,7 @@ class PassConfig(C.Structure):
         ("dep_capacity", c_i64),
         ("comm", c_vp),
         ("dep_wire_capacity", c_i64),
+        ("sample_list", c_vp),
     ]
 
 

@@ -556,7 +556,7 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
   WFPG_CUDA(cudaMemsetAsync(L.stats, 0, sizeof(StatsDev), st));
   const int64_t n_img = (int64_t)cam->width * cam->height;
   WFPG_TRY(launch_camera_init(cv, pv, P, L.n_pix, n_img, cfg->pixel_offset, L.sample,
-                              cfg->seed, st));
+                              cfg->sample_list, cfg->seed, st));
 
   BlurParams bp{};
   bp.radius = cfg->blur_radius;

@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(kInitTile) k_init_paths(CameraView c, PathsVie
                                                           int64_t n_paths, int64_t n_pix,
                                                           int64_t n_img, int64_t pix0,
                                                           const int64_t* __restrict__ sample_dev,
+                                                          const int64_t* __restrict__ sample_list,
                                                           uint64_t seed) {
   __shared__ double sdir[3 * kInitTile];
   const int64_t sample0 = *sample_dev;
@@ -55,7 +56,7 @@ __global__ void __launch_bounds__(kInitTile) k_init_paths(CameraView c, PathsVie
     const int m = (int)(n_paths - base < kInitTile ? n_paths - base : kInitTile);
     if (p < n_paths) {
       int64_t pix = pix0 + p % n_pix;  // global pixel index
-      int64_t sample = sample0 + p / n_pix;
+      int64_t sample = sample_list ? sample_list[p / n_pix] : sample0 + p / n_pix;
       uint64_t key = stream_key(seed, (uint64_t)(sample * n_img + pix) * 4u);
       const_cast<uint64_t*>(P.key)[p] = key;
       double o[3];
@@ -432,8 +433,8 @@ __global__ void __launch_bounds__(256) k_intersect_origin(SceneView s, double ox
 // internal launchers
 // ---------------------------------------------------------------------------
 int launch_camera_init(const CameraView& c, const PathsView& P, int64_t n_paths, int64_t n_pix,
-                       int64_t n_img, int64_t pix0, const int64_t* sample0, uint64_t seed,
-                       cudaStream_t st) {
+                       int64_t n_img, int64_t pix0, const int64_t* sample0,
+                       const int64_t* sample_list, uint64_t seed, cudaStream_t st) {
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_paths, 256), kNumSMs * 8));
   size_t rec_bytes = sizeof(double) * 3 * (size_t)P.rec_depths * (size_t)n_paths;
   if (!P.n_rec) {  // with n_rec, slots above it are masked by the readers
@@ -442,7 +443,8 @@ int launch_camera_init(const CameraView& c, const PathsView& P, int64_t n_paths,
   }
   const int igrid =
       (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_paths, kInitTile), kNumSMs * 8));
-  k_init_paths<<<igrid, kInitTile, 0, st>>>(c, P, n_paths, n_pix, n_img, pix0, sample0, seed);
+  k_init_paths<<<igrid, kInitTile, 0, st>>>(c, P, n_paths, n_pix, n_img, pix0, sample0,
+                                            sample_list, seed);
   WFPG_CHECK_LAUNCH("k_init_paths");
   return WFPG_OK;
 }

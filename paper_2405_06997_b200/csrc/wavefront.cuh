@@ -15,7 +15,8 @@ CameraView make_camera_view(const wfpg_camera* c);
 GuideView make_guide_view(const wfpg_guide* g);
 
 int launch_camera_init(const CameraView& c, const PathsView& P, int64_t n_paths, int64_t n_pix,
-                       int64_t n_img, int64_t pix0, const int64_t* sample0, uint64_t seed,
+                       int64_t n_img, int64_t pix0, const int64_t* sample0,
+                       const int64_t* sample_list, uint64_t seed,
                        cudaStream_t st);
 // primary rays from one origin (host pointer to 3 doubles); brute-force scenes
 // use the warp-culled tracer, others fall back to launch_intersect (which

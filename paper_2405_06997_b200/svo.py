@@ -363,14 +363,39 @@ class SvoCache:
                 "sum_b": take("<f8", (n, 3)), "weight_a": take("<f8", (n,)),
                 "weight_b": take("<f8", (n,)),
             }
-        svo._alloc(n)
-        for k, v in host.items():
-            setattr(svo, k, v)
-        desc = np.stack([host["child_base"].astype(np.int64) & 0xFFFFFFFF,
-                         host["child_mask"].astype(np.int64)], axis=1).astype(np.uint32)
-        svo._d["node_desc"].copy_(_dev.upload(desc))
-        _lib.call("wfpg_svo_build_top_index", _lib.C.byref(svo.abi()), _dev.stream())
+        svo._fill_host(host)
         svo.propagate_up()
+        return svo
+
+    def _fill_host(self, host):
+        """Allocate and upload host node arrays (structure + accumulators),
+        then the derived descent records and top index."""
+        n = int(self.level_off[-1])
+        self._alloc(n)
+        for k, v in host.items():
+            setattr(self, k, v)
+        desc = np.stack([np.asarray(host["child_base"]).astype(np.int64) & 0xFFFFFFFF,
+                         np.asarray(host["child_mask"]).astype(np.int64)], axis=1).astype(np.uint32)
+        self._d["node_desc"].copy_(_dev.upload(desc))
+        _lib.call("wfpg_svo_build_top_index", _lib.C.byref(self.abi()), _dev.stream())
+
+    @classmethod
+    def from_arrays(cls, src):
+        """Device copy of any SvoCache-like object with the reference's host
+        arrays (svo.py:176-199): structure, normals, accumulators and means
+        uploaded as they are (backend_cuda adapts the reference's SvoCache)."""
+        svo = cls(src.resolution, np.asarray(src.cube_lo), float(src.cube_size))
+        svo.level_off = np.asarray(src.level_off, dtype=np.int64).copy()
+        n = int(svo.level_off[-1])
+        host = {}
+        for k in ("codes", "child_base", "child_mask", "parent", "normal", "sum_a", "sum_b",
+                  "weight_a", "weight_b", "mean_a", "mean_b"):
+            v = getattr(src, k, None)
+            if v is None:
+                v = np.zeros((n, 3) if k in ("normal", "sum_a", "sum_b", "mean_a", "mean_b")
+                             else (n,))
+            host[k] = np.asarray(v)
+        svo._fill_host(host)
         return svo
 
 

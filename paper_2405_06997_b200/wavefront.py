@@ -229,9 +229,21 @@ class PassRunner:
 
         weakref.finalize(self, _release_graph, self.ws.data_ptr())
 
-    def launch(self, sample_index, want_stats=True):
-        """Enqueue one pass; with want_stats the call synchronises and fills self.stats."""
+    def launch(self, sample_index, want_stats=True, sample_list=None):
+        """Enqueue one pass; with want_stats the call synchronises and fills self.stats.
+        sample_list: the pass's sample indices when they are not sample_index,
+        sample_index + 1, ... (any list, as the reference accepts)."""
         self.pc.sample_index = int(sample_index)
+        if sample_list is not None:
+            lst = np.asarray(sample_list, dtype=np.int64).reshape(-1)
+            if len(lst) != self.n_samples or lst[0] != sample_index:
+                raise ValueError("sample_list must hold n_samples entries starting at sample_index")
+            if getattr(self, "_samples_dev", None) is None:
+                self._samples_dev = _dev.empty((self.n_samples,), np.int64)
+            self._samples_dev.copy_(_dev.upload(lst), non_blocking=False)
+            self.pc.sample_list = self._samples_dev.data_ptr()
+        else:
+            self.pc.sample_list = None
         _lib.call("wfpg_render_pass", C.byref(self.scene.abi()),
                   C.byref(self.svo_abi) if self.svo is not None else None, C.byref(self.cam),
                   C.byref(self.pc), C.byref(self.state.abi()), _lib.ptr(self.frame),
@@ -282,19 +294,19 @@ def pinned_frame(scene):
 
 
 def render_pass(scene, svo, cfg, sample_indices, collect_bin_image=False, out=None):
-    """One wavefront pass over every pixel for each sample index (consecutive
-    indices); returns (frame (H,W,3), PassStats).  ``out`` (optional, e.g.
+    """One wavefront pass over every pixel for each sample index (any list;
+    bins use the first index's streams); returns (frame (H,W,3), PassStats).  ``out`` (optional, e.g.
     from pinned_frame) receives the frame instead of a fresh array."""
     samples = np.asarray(sample_indices, dtype=np.int64).reshape(-1)
     if len(samples) == 0:
         raise ValueError("render_pass needs at least one sample index")
-    if np.any(np.diff(samples) != 1):
-        raise ValueError("render_pass on the device takes consecutive sample indices")
     if svo is not None:
         cfg.validate(svo.depth)
     collect = bool(collect_bin_image) and svo is not None
     r = _runner(scene, svo, cfg, len(samples), collect)
-    r.launch(int(samples[0]))
+    # any sample list (wavefront.py:207-215): consecutive lists need no table
+    consecutive = bool(np.all(np.diff(samples) == 1))
+    r.launch(int(samples[0]), sample_list=None if consecutive else samples)
     cam = scene.camera
     if out is not None:
         t = _dev.torch()
@@ -380,11 +392,25 @@ def render_sample(scene, svo, cfg, sample_index):
 
 def update_exitance(state, svo, deterministic=True):
     """Eq. 5 back-propagation of emitter radiance into the SVO leaves
-    (wavefront.py:286-332), followed by the bottom-up refresh.  Returns the
-    number of deposits."""
+    (wavefront.py:286-332).  Returns the dirty leaf ids (sorted int64, the
+    reference's return value, which its caller hands to svo.propagate_up);
+    the device refresh of the touched subtrees has already run, so that
+    call is a no-op refresh here.  ``update_exitance.last_deposits`` holds
+    the deposit count."""
+    lo, hi = int(svo.level_off[svo.depth]), int(svo.level_off[svo.depth + 1])
+    t = _dev.torch()
+    before = t.stack([svo.dev("weight_a")[lo:hi], svo.dev("weight_b")[lo:hi]]).clone()
     n_dep = _dev.zeros((1,), np.int32)
     ws = _dev.workspace(_lib.load().wfpg_update_exitance_workspace_bytes(state.n, state.max_depth))
     _lib.call("wfpg_update_exitance", C.byref(svo.abi()), C.byref(state.abi()),
               1 if deterministic else 0, _lib.ptr(n_dep), _lib.ptr(ws), ws.numel(),
               _dev.stream())
-    return int(_dev.download(n_dep)[0])
+    after = t.stack([svo.dev("weight_a")[lo:hi], svo.dev("weight_b")[lo:hi]])
+    # every deposit adds 1 to its leaf's side weight, so the touched leaves are
+    # exactly those whose weights changed
+    dirty = t.nonzero((after != before).any(dim=0)).reshape(-1) + lo
+    update_exitance.last_deposits = int(_dev.download(n_dep)[0])
+    return _dev.download(dirty).astype(np.int64)
+
+
+update_exitance.last_deposits = 0

@@ -83,3 +83,27 @@ def test_product_guiding_few_bins(scene_path):
     base = dict(max_depth=3, field_res=16, l_min=1, c_ray=1000, seed=4)
     _compare(sc, 16, [(0, dict(base, guided_depths=0)),
                       (1, dict(base, guided_depths=3, product=True))])
+
+
+def test_any_sample_list(scene_path):
+    """render_pass accepts any sample list (wavefront.py:198-215): a PT pass
+    over samples [3, 1] is the sample-major mean of the single-sample passes
+    3 and 1, bit for bit; a consecutive list needs no table and a reversed
+    one differs from it."""
+    from paper_2405_06997_b200 import svo, wavefront
+
+    sc = _scene(scene_path, 24, 16)
+    tree = svo.build_from_scene(sc, 32, seed=0)
+    cfg = wavefront.GuidingConfig(max_depth=4, guided_depths=0, field_res=16, l_min=2,
+                                  c_ray=8, seed=3)
+    f31, st = wavefront.render_pass(sc, tree, cfg, [3, 1])
+    f3, _ = wavefront.render_pass(sc, tree, cfg, [3])
+    f1, _ = wavefront.render_pass(sc, tree, cfg, [1])
+    np.testing.assert_array_equal(f31, (f3 + f1) / 2.0)
+    f13, _ = wavefront.render_pass(sc, tree, cfg, [1, 3])
+    np.testing.assert_array_equal(f13, (f1 + f3) / 2.0)
+    f57, _ = wavefront.render_pass(sc, tree, cfg, [5, 7])
+    f5, _ = wavefront.render_pass(sc, tree, cfg, [5])
+    f7, _ = wavefront.render_pass(sc, tree, cfg, [7])
+    np.testing.assert_array_equal(f57, (f5 + f7) / 2.0)
+    assert st.live_per_depth[0] == 2 * 24 * 16

@@ -119,10 +119,14 @@ def test_eq5_deposit_and_running_mean():
     st.dev["rec_T"].copy_(st.dev["rec_T"].new_tensor(rt))
     st.dev["emit_le"].fill_(8.0)
     st.dev["emit_depth"].fill_(2)
-    assert wavefront.update_exitance(st, tree) == 1
+    dirty = wavefront.update_exitance(st, tree)
+    assert wavefront.update_exitance.last_deposits == 1
     sums = tree.sum_a + tree.sum_b
     w = tree.weight_a + tree.weight_b
     k = int(np.flatnonzero(w)[0])
+    # the reference's return value: the dirty leaf ids (wavefront.py:266-269)
+    assert dirty.dtype == np.int64 and list(dirty) == [k]
+    tree.propagate_up(dirty)
     np.testing.assert_array_equal(sums[k], [2.0, 2.0, 2.0])
     means = (tree.mean_a.copy(), tree.mean_b.copy())
     wa, wb = tree.weight_a.copy(), tree.weight_b.copy()
