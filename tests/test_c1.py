@@ -1,0 +1,93 @@
+"""SURVEY 8(d) C1, the primary per-path equivalence configuration, against
+the reference's own C1 run (tests/golden/c1_golden.npz, make_golden.py
+gen_c1): Cornell 256x256, SVO R=256, D=4, N0=128, l_min 5, c_ray 512, seed
+0.  Pass 0 is PT-first (the SVO learns), then sample 1 guided plain and,
+from the same PT-first SVO state, sample 1 guided product.  The oracle (CPU)
+and the device pass (B200) must both reproduce the reference's bins at every
+depth and its paths."""
+
+import numpy as np
+import pytest
+
+SVO_STATE = ("sum_a", "sum_b", "weight_a", "weight_b")
+
+
+def _setup(golden, scene_path):
+    from paper_2405_06997_b200 import scene as S
+
+    G = golden("c1_golden.npz")
+    c = dict(zip([str(k) for k in G["cfg_keys"]], [int(v) for v in G["cfg_vals"]]))
+    sc = S.load_scene(scene_path("cornell.scene"))
+    cam = sc.camera
+    sc.camera = S.Camera(cam.position, cam.target, cam.up, cam.vfov_deg, c["W"], c["H"])
+    base = dict(max_depth=c["max_depth"], field_res=c["field_res"], l_min=c["l_min"],
+                c_ray=c["c_ray"], seed=c["seed"])
+    return G, c, sc, base
+
+
+def _check(G, tag, emit_depth, rec_pos, radiance, diag, min_identical):
+    same = emit_depth == G[tag + "_emit_depth"]
+    same &= np.abs(rec_pos[:, 1:] - G[tag + "_rec_pos"]).max(axis=(1, 2)) <= 1e-5 * diag
+    rel = (np.abs(radiance - G[tag + "_radiance"])
+           / np.maximum(np.abs(G[tag + "_radiance"]), 1e-12)).max(axis=1)
+    assert same.mean() >= min_identical, (tag, same.mean())
+    # radiance golden is float32: 1e-4 relative on every identical path
+    assert np.all(rel[same] <= 1e-4), (tag, rel[same].max())
+    return same.mean()
+
+
+def test_oracle_reproduces_the_reference_c1_run(golden, scene_path):
+    from oracle import render as OR
+
+    G, c, sc, base = _setup(golden, scene_path)
+    osc = OR.Scene(sc)
+    svo = OR.Svo.from_scene(sc, c["R"], c["svo_seed"])
+    st = {}
+    _, s = OR.render_pass(osc, svo, dict(base, guided_depths=0), 0, st)
+    assert st["bins"] == list(G["p0_bins"]) and st["rays"] == list(G["p0_rays"])
+    _check(G, "p0", s["emit_depth"], s["rec_pos"], s["radiance"], sc.diagonal, 1.0)
+    assert np.array_equal(svo.weight_a, G["p0_svo_weight_a"])
+    state = {k: getattr(svo, k).copy() for k in SVO_STATE + ("mean_a", "mean_b")}
+    for tag, product in (("p1", False), ("p1x", True)):
+        for k, v in state.items():
+            setattr(svo, k, v.copy())
+        st = {}
+        _, s = OR.render_pass(osc, svo, dict(base, guided_depths=c["max_depth"],
+                                             product=product), 1, st)
+        assert st["bins"] == list(G[tag + "_bins"]), tag
+        _check(G, tag, s["emit_depth"], s["rec_pos"], s["radiance"], sc.diagonal, 1.0)
+        assert np.array_equal(svo.weight_a, G[tag + "_svo_weight_a"]), tag
+
+
+@pytest.mark.gpu
+def test_device_reproduces_the_reference_c1_run(golden, scene_path):
+    from paper_2405_06997_b200 import svo, wavefront
+
+    G, c, sc, base = _setup(golden, scene_path)
+    tree = svo.build_from_scene(sc, c["R"], seed=c["svo_seed"])
+
+    def run(cfg, sample):
+        _, st = wavefront.render_pass(sc, tree, cfg, [sample])
+        state = wavefront._RUNNERS[next(iter(wavefront._RUNNERS))].state
+        return st, state.emit_depth, state.rec_pos, state.radiance
+
+    st, ed, rp, rad = run(wavefront.GuidingConfig(guided_depths=0, **base), 0)
+    assert st.bins_per_depth == list(G["p0_bins"]) and st.rays_per_depth == list(G["p0_rays"])
+    groups = np.zeros_like(G["p0_mat_groups"])
+    for d, g in enumerate(st.material_groups):
+        for m, k in g.items():
+            groups[d, m] = k
+    assert np.array_equal(groups, G["p0_mat_groups"])
+    _check(G, "p0", ed, rp, rad, sc.diagonal, 1.0)
+    assert np.array_equal(tree.weight_a, G["p0_svo_weight_a"])
+    assert np.array_equal(tree.sum_a.view(np.uint64), G["p0_svo_sum_a"].view(np.uint64))
+    state = {k: getattr(tree, k).copy() for k in SVO_STATE}
+    for tag, product in (("p1", False), ("p1x", True)):
+        for k, v in state.items():
+            setattr(tree, k, v)
+        tree.propagate_up()
+        st, ed, rp, rad = run(wavefront.GuidingConfig(guided_depths=c["max_depth"],
+                                                      product=product, **base), 1)
+        assert st.bins_per_depth == list(G[tag + "_bins"]), tag
+        assert st.rays_per_depth == list(G[tag + "_rays"]), tag
+        _check(G, tag, ed, rp, rad, sc.diagonal, 0.999)
