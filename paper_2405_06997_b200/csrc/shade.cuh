@@ -172,15 +172,65 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+// Per-path product layer (_kernels.pyx:1003-1019), register resident: cell
+// k = bj * 8 + bi is block_mean * (lum(albedo) / pi) * max(0, upper_dir . n_s)
+// floored at eps, a pure function of (slot, k, n_s, albedo), so the 64 cells
+// are never stored: one pass accumulates upsum (sequential over k, the
+// reference's order) and the 8 row sums (sequential over bi), and the
+// samplers / pdfs re-evaluate the few cells they need.
+struct ProductLayer {
+  const double* bs;  // block sums of the path's bin (8, 8)
+  double nsx, nsy, nsz;
+  double lum_pi;     // lum(albedo) / pi
+  double mm;         // m * m
+  double upsum;
+  double urow[8];
+};
+
+__device__ __forceinline__ double product_cell(const GuideView& g, const ProductLayer& L, int k) {
+  const double mean = __ldg(L.bs + k) / L.mm;
+  const double* ud = g.upper_dirs + 3 * k;
+  double cosf = __ldg(ud) * L.nsx + __ldg(ud + 1) * L.nsy + __ldg(ud + 2) * L.nsz;
+  if (cosf < 0.0) cosf = 0.0;
+  double val = mean * L.lum_pi * cosf;
+  if (val < g.eps) val = g.eps;
+  return val;
+}
+
+__device__ __forceinline__ void product_layer(const GuideView& g, int slot, double nsx,
+                                              double nsy, double nsz, double alx, double aly,
+                                              double alz, ProductLayer* L) {
+  L->bs = g.block_sums + (int64_t)slot * 64;
+  L->nsx = nsx;
+  L->nsy = nsy;
+  L->nsz = nsz;
+  L->lum_pi = (0.2126 * alx + 0.7152 * aly + 0.0722 * alz) / WFPG_PI;
+  L->mm = (double)(g.m * g.m);
+  double upsum = 0.0;
+#pragma unroll
+  for (int bj = 0; bj < 8; ++bj) {
+    double row = 0.0;
+#pragma unroll
+    for (int bi = 0; bi < 8; ++bi) {
+      const double v = product_cell(g, *L, bj * 8 + bi);
+      upsum += v;
+      row += v;
+    }
+    L->urow[bj] = row;
+  }
+  L->upsum = upsum;
+}
+
 // pdf_product_dir (_kernels.pyx:888-902)
-__device__ __forceinline__ double pdf_product(const GuideView& g, int slot, const double* upper,
-                                              double upsum, double dx, double dy, double dz) {
+__device__ __forceinline__ double pdf_product(const GuideView& g, int slot, const ProductLayer& L,
+                                              double dx, double dy, double dz) {
   int i, j;
   cell_of(g.n, dx, dy, dz, &i, &j);
   int bi = i / g.m, bj = j / g.m;
   double v = g.vals[((int64_t)slot * g.n + j) * g.n + i];
   double bs = g.block_sums[((int64_t)slot * 8 + bj) * 8 + bi];
-  return (upper[bj * 8 + bi] / upsum) * (v / bs) * (double)(g.n * g.n) / (4.0 * WFPG_PI);
+  return (product_cell(g, L, bj * 8 + bi) / L.upsum) * (v / bs) * (double)(g.n * g.n) /
+         (4.0 * WFPG_PI);
 }
 
 // plain guided sample (_kernels.pyx:1093-1100): marginal then on-the-fly conditional
@@ -196,29 +246,62 @@ __device__ __forceinline__ void sample_plain(const GuideView& g, int slot, doubl
 }
 
 // product guided sample (_kernels.pyx:1101-1127)
-__device__ __forceinline__ void sample_product(const GuideView& g, int slot, const double* upper,
-                                               double upsum, double s1, double s2, double s3,
-                                               double s4, double* wx, double* wy, double* wz) {
+__device__ __forceinline__ void sample_product(const GuideView& g, int slot, const ProductLayer& L,
+                                               double s1, double s2, double s3, double s4,
+                                               double* wx, double* wy, double* wz) {
   const int n = g.n, m = g.m;
-  double urow[8], ucdf[8], fv, fu;
-  for (int bj = 0; bj < 8; ++bj) {
-    urow[bj] = 0.0;
-    for (int bi = 0; bi < 8; ++bi) urow[bj] += upper[bj * 8 + bi];
+  double fv, fu;
+  // upper row: running CDF of urow / upsum (sequential, as the reference)
+  int bj = 7;
+  {
+    double prev = 0.0, cur = 0.0;
+    for (int r = 0; r < 8; ++r) {
+      cur = r == 0 ? L.urow[0] / L.upsum : prev + L.urow[r] / L.upsum;
+      if (cur > s1 || r == 7) {
+        bj = r;
+        break;
+      }
+      prev = cur;
+    }
+    fv = residual(s1, bj > 0 ? prev : 0.0, cur);
   }
-  ucdf[0] = urow[0] / upsum;
-  for (int bj = 1; bj < 8; ++bj) ucdf[bj] = ucdf[bj - 1] + urow[bj] / upsum;
-  int bj = invert_cdf(ucdf, 8, s1, &fv);
-  ucdf[0] = upper[bj * 8] / urow[bj];
-  for (int bi = 1; bi < 8; ++bi) ucdf[bi] = ucdf[bi - 1] + upper[bj * 8 + bi] / urow[bj];
-  int bi = invert_cdf(ucdf, 8, s2, &fu);
+  int bi = 7;
+  {
+    const double rs = L.urow[bj];
+    double prev = 0.0, cur = 0.0;
+    for (int c = 0; c < 8; ++c) {
+      const double v = product_cell(g, L, bj * 8 + c);
+      cur = c == 0 ? v / rs : prev + v / rs;
+      if (cur > s2 || c == 7) {
+        bi = c;
+        break;
+      }
+      prev = cur;
+    }
+    fu = residual(s2, bi > 0 ? prev : 0.0, cur);
+  }
   // block rows of the selected block: rows[r] = 0 + pairwise(row r), the block
   // marginal is cumsum(rows) / block_sum (guiding.py:304-309)
   const double* blk = g.vals + ((int64_t)slot * n + bj * m) * n + bi * m;
-  double bsum = g.block_sums[((int64_t)slot * 8 + bj) * 8 + bi];
-  double rows[16];
-  for (int r = 0; r < m; ++r) rows[r] = __dadd_rn(0.0, pairwise_row(blk + (int64_t)r * n, m));
-  int jin = invert_cumsum(rows, 1, m, bsum, s3, &fv);
-  int iin = invert_cumsum(blk + (int64_t)jin * n, 1, m, rows[jin], s4, &fu);
+  const double bsum = g.block_sums[((int64_t)slot * 8 + bj) * 8 + bi];
+  int jin = m - 1;
+  double rowj = 0.0;
+  {
+    double run = 0.0, prev = 0.0, cur = 0.0;
+    for (int r = 0; r < m; ++r) {
+      const double rr = __dadd_rn(0.0, pairwise_row(blk + (int64_t)r * n, m));
+      run = r == 0 ? rr : __dadd_rn(run, rr);
+      cur = __ddiv_rn(run, bsum);
+      if (cur > s3 || r == m - 1) {
+        jin = r;
+        rowj = rr;
+        break;
+      }
+      prev = cur;
+    }
+    fv = residual(s3, jin > 0 ? prev : 0.0, cur);
+  }
+  int iin = invert_cumsum(blk + (int64_t)jin * n, 1, m, rowj, s4, &fu);
   int gj = bj * m + jin, gi = bi * m + iin;
   octa_uv_to_dir_k((gi + fu) / n, (gj + fv) / n, wx, wy, wz);
 }

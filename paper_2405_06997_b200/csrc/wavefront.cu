@@ -217,24 +217,11 @@ __device__ void shade_path(int64_t p, int depth, const SceneView& sa, const Guid
   const int slot = (g.mode > 0 && bin_slot) ? bin_slot[p] : -1;
   const bool guided = slot >= 0;
 
-  double upper[64];
-  double upsum = 1.0;
-  if (guided && g.mode == 2) {
-    double alb_lum = 0.2126 * alx + 0.7152 * aly + 0.0722 * alz;
-    upsum = 0.0;
-    const double* bs = g.block_sums + (int64_t)slot * 64;
-    const double mm = (double)(g.m * g.m);
-    for (int k = 0; k < 64; ++k) {
-      double mean = bs[k] / mm;
-      const double* ud = g.upper_dirs + 3 * k;
-      double cosf = ud[0] * nsx + ud[1] * nsy + ud[2] * nsz;
-      if (cosf < 0.0) cosf = 0.0;
-      double val = mean * (alb_lum / WFPG_PI) * cosf;
-      if (val < g.eps) val = g.eps;
-      upper[k] = val;
-      upsum += val;
-    }
-  }
+  // product layer (_kernels.pyx:1003-1019): built after the shadow ray (a
+  // pure function of the path's bin, n_s and albedo) so its registers are
+  // not live across the occlusion loop
+  ProductLayer layer;
+  bool have_layer = false;
 
   // ---- next-event estimation (2 draws) ----
   {
@@ -281,8 +268,12 @@ __device__ void shade_path(int64_t p, int depth, const SceneView& sa, const Guid
         if (!blocked) {
           double p_cont;
           if (guided) {
+            if (g.mode == 2) {
+              product_layer(g, slot, nsx, nsy, nsz, alx, aly, alz, &layer);
+              have_layer = true;
+            }
             double pg = g.mode == 1 ? pdf_plain_cell(g, slot, nci, ncj)
-                                    : pdf_product(g, slot, upper, upsum, lx, ly, lz);
+                                    : pdf_product(g, slot, layer, lx, ly, lz);
             p_cont = 0.5 * pg + 0.5 * (cos_s / WFPG_PI);
           } else {
             p_cont = cos_s / WFPG_PI;
@@ -316,6 +307,8 @@ __device__ void shade_path(int64_t p, int depth, const SceneView& sa, const Guid
 
   // ---- continuation ----
   double wx = 0.0, wy = 0.0, wz = 1.0, cos_rel, pdf_mix;
+  if (guided && g.mode == 2 && !have_layer)
+    product_layer(g, slot, nsx, nsy, nsz, alx, aly, alz, &layer);
   if (guided) {
     double coin = u01(kk, c);
     c += 1;
@@ -327,7 +320,7 @@ __device__ void shade_path(int64_t p, int depth, const SceneView& sa, const Guid
       } else {
         double s1 = u01(kk, c), s2 = u01(kk, c + 1), s3 = u01(kk, c + 2), s4 = u01(kk, c + 3);
         c += 4;
-        sample_product(g, slot, upper, upsum, s1, s2, s3, s4, &wx, &wy, &wz);
+        sample_product(g, slot, layer, s1, s2, s3, s4, &wx, &wy, &wz);
       }
     } else {
       double s1 = u01(kk, c), s2 = u01(kk, c + 1);
@@ -336,7 +329,7 @@ __device__ void shade_path(int64_t p, int depth, const SceneView& sa, const Guid
     }
     cos_rel = wx * nsx + wy * nsy + wz * nsz;
     double pg = g.mode == 1 ? pdf_plain(g, slot, wx, wy, wz)
-                            : pdf_product(g, slot, upper, upsum, wx, wy, wz);
+                            : pdf_product(g, slot, layer, wx, wy, wz);
     double pb = fmax(cos_rel, 0.0) / WFPG_PI;
     pdf_mix = 0.5 * pg + 0.5 * pb;
   } else {

@@ -143,3 +143,19 @@ def test_oracle_render_pass(rsetup, tag, guided, product, sample):
     assert np.all(rel[same] <= 1e-4)
     np.testing.assert_allclose(svo.sum_a, R[f"{tag}_svo_sum_a"], rtol=1e-9, atol=1e-12)
     assert np.array_equal(svo.weight_a, R[f"{tag}_svo_weight_a"])
+
+
+def test_oracle_c2_svo_equals_the_reference_build(golden, scene_path):
+    """The oracle's R=1024 build (C2's SVO, ~1 min here) against the
+    reference's own build digests (make_golden.py gen_r1024)."""
+    import hashlib
+
+    G = golden("r1024_golden.npz")
+    sc0 = _scene(scene_path)
+    svo = OR.Svo.from_scene(sc0, 1024, 0)
+    dig = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]  # noqa: E731
+    assert np.array_equal(svo.level_off, G["level_off"])
+    for k, dt in (("codes", np.uint64), ("child_base", np.int64), ("child_mask", np.uint8),
+                  ("parent", np.int64)):
+        assert dig(np.asarray(svo.d[k]).astype(dt)) == str(G[k]), k
+    assert dig(svo.normal) == str(G["normal"])
