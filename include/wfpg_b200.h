@@ -168,6 +168,9 @@ typedef struct wfpg_guide {
   double* cum;               /* optional (B,n,n) unnormalised row prefix sums
                                 (np.cumsum order); lets the plain sampler invert the
                                 conditional CDF with a binary search */
+  double* block_rows;        /* optional (B,8,8,n/8) product mode: row sums of every
+                                block row (guiding.py:304 `rows`); the product sampler's
+                                block marginal then reads them instead of re-summing */
 } wfpg_guide;
 
 /* Knobs of one render pass: wavefront.py:21-50 (GuidingConfig). */

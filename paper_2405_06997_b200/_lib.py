@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libwfpg_b200.so")
+# WFPG_LIB overrides the library path (A/B measurements of alternative builds)
+LIB_PATH = os.environ.get("WFPG_LIB") or os.path.join(_HERE, "libwfpg_b200.so")
 
 c_i32 = C.c_int32
 c_i64 = C.c_int64
@@ -69,6 +70,7 @@ class Guide(C.Structure):
         ("mode", c_i32), ("n", c_i32), ("capacity", c_i32), ("eps", c_dbl),
         ("vals", c_vp), ("row_sum", c_vp), ("marg", c_vp), ("total", c_vp),
         ("block_sums", c_vp), ("n_bins", c_vp), ("upper_dirs", c_vp), ("cum", c_vp),
+        ("block_rows", c_vp),
     ]
 
 

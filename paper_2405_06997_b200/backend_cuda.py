@@ -182,7 +182,9 @@ def _guide_abi(guide):
     g.marg, g.total = keep["marg"].data_ptr(), keep["total"].data_ptr()
     if g.mode == 2:
         keep["block_sums"] = _dev.zeros((max(b, 1), 8, 8), np.float64)
+        keep["block_rows"] = _dev.zeros((max(b, 1), 8, 8, max(1, n // 8)), np.float64)
         g.block_sums = keep["block_sums"].data_ptr()
+        g.block_rows = keep["block_rows"].data_ptr()
     g.upper_dirs = keep["upper"].data_ptr()
     if b:
         _lib.call("wfpg_guide_fill", C.byref(g), b, _dev.stream())

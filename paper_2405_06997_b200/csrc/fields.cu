@@ -245,7 +245,9 @@ __device__ __forceinline__ void ph_mark(int k) {
 }
 #endif
 
-template <int N>
+// PRODUCT: block sums (+ block row sums) for the product sampler; a separate
+// instantiation so the plain kernel carries none of its registers
+template <int N, bool PRODUCT>
 __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks)
     k_fields(SceneView s, SvoView v, const double* __restrict__ origins,
              const double* __restrict__ jitters, int64_t nb_max, const int32_t* __restrict__ nb_dev,
@@ -381,7 +383,22 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
         out.row_sum[b * N + j] = r;
       }
     }
-    if (out.block_sums) {
+    if (PRODUCT && out.block_sums && out.block_rows) {
+      // every (block, row) pair in parallel, then the sequential sum of each
+      // block's rows (guiding.py:302-304 order)
+      constexpr int M = N / 8;
+      double* br = out.block_rows + b * 64 * M;
+      for (int t = threadIdx.x; t < 64 * M; t += blockDim.x) {
+        const int q = t / M, r = t % M, bj = q / 8, bi = q % 8;
+        br[t] = __dadd_rn(0.0, pairwise_row(F + (bj * M + r) * S + bi * M, M));
+      }
+      __syncthreads();
+      for (int q = threadIdx.x; q < 64; q += blockDim.x) {
+        double acc = 0.0;
+        for (int r = 0; r < M; ++r) acc = __dadd_rn(acc, br[q * M + r]);
+        out.block_sums[b * 64 + q] = acc;
+      }
+    } else if (PRODUCT && out.block_sums) {
       constexpr int M = N / 8;
       for (int q = threadIdx.x; q < 64; q += blockDim.x) {
         const int bj = q / 8, bi = q % 8;
@@ -437,8 +454,8 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
   }
 }
 
-template <int N>
-static int launch_fields_n(const SceneView& s, const SvoView& v, const double* origins,
+template <int N, bool PRODUCT>
+static int launch_fields_n_(const SceneView& s, const SvoView& v, const double* origins,
                            const double* jitters, int64_t nb_max, const int32_t* nb_dev,
                            const BlurParams& bp, const FieldOut& out, cudaStream_t st) {
   constexpr int T = FieldCfg<N>::kThreads;
@@ -446,21 +463,30 @@ static int launch_fields_n(const SceneView& s, const SvoView& v, const double* o
                 (s.brute ? sizeof(TriBin) * s.n_tris : 0);
   static size_t configured = 0;
   if (smem > configured) {
-    WFPG_CUDA(cudaFuncSetAttribute(k_fields<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    WFPG_CUDA(cudaFuncSetAttribute(k_fields<N, PRODUCT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
     configured = smem;
   }
   int per_sm = 0;
-  WFPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fields<N>, T, smem));
+  WFPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fields<N, PRODUCT>, T, smem));
   if (per_sm < 1) {
     set_error("fields: kernel does not fit (smem %zu)", smem);
     return WFPG_ERR_ARG;
   }
   int64_t grid = std::min<int64_t>(nb_max, (int64_t)kNumSMs * per_sm);
   if (grid < 1) return WFPG_OK;
-  k_fields<N><<<(unsigned)grid, T, smem, st>>>(s, v, origins, jitters, nb_max, nb_dev, bp, out);
+  k_fields<N, PRODUCT><<<(unsigned)grid, T, smem, st>>>(s, v, origins, jitters, nb_max, nb_dev, bp, out);
   WFPG_CHECK_LAUNCH("k_fields");
   return WFPG_OK;
+}
+
+template <int N>
+static int launch_fields_n(const SceneView& s, const SvoView& v, const double* origins,
+                           const double* jitters, int64_t nb_max, const int32_t* nb_dev,
+                           const BlurParams& bp, const FieldOut& out, cudaStream_t st) {
+  return out.block_sums
+             ? launch_fields_n_<N, true>(s, v, origins, jitters, nb_max, nb_dev, bp, out, st)
+             : launch_fields_n_<N, false>(s, v, origins, jitters, nb_max, nb_dev, bp, out, st);
 }
 
 int launch_fields(const SceneView& s, const SvoView& v, const double* origins,
@@ -528,7 +554,8 @@ __global__ void k_guide_expand(GuideView g, int64_t nb, double* cond, double* pd
 // GuideTables.fill_batch on caller-provided floored values (guiding.py:293-309)
 __global__ void k_guide_fill(const double* __restrict__ vals, int n, int64_t nb,
                              double* __restrict__ row_sum, double* __restrict__ marg,
-                             double* __restrict__ total, double* __restrict__ block_sums) {
+                             double* __restrict__ total, double* __restrict__ block_sums,
+                             double* __restrict__ block_rows) {
   extern __shared__ double rs[];
   for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
     const double* v = vals + b * (int64_t)n * n;
@@ -542,8 +569,11 @@ __global__ void k_guide_fill(const double* __restrict__ vals, int n, int64_t nb,
       for (int q = threadIdx.x; q < 64; q += blockDim.x) {
         const int bj = q / 8, bi = q % 8;
         double acc = 0.0;
-        for (int r = 0; r < M; ++r)
-          acc = __dadd_rn(acc, __dadd_rn(0.0, pairwise_row(v + (int64_t)(bj * M + r) * n + bi * M, M)));
+        for (int r = 0; r < M; ++r) {
+          const double rr = __dadd_rn(0.0, pairwise_row(v + (int64_t)(bj * M + r) * n + bi * M, M));
+          if (block_rows) block_rows[(b * 64 + q) * M + r] = rr;
+          acc = __dadd_rn(acc, rr);
+        }
         block_sums[b * 64 + q] = acc;
       }
     }
@@ -575,7 +605,8 @@ extern "C" int wfpg_guide_fill(wfpg_guide* guide, int64_t n_bins, void* stream) 
   int grid = (int)std::min<int64_t>(n_bins, kNumSMs * 8);
   k_guide_fill<<<grid, 128, sizeof(double) * guide->n, as_stream(stream)>>>(
       guide->vals, guide->n, n_bins, guide->row_sum, guide->marg, guide->total,
-      guide->mode == 2 ? guide->block_sums : nullptr);
+      guide->mode == 2 ? guide->block_sums : nullptr,
+      guide->mode == 2 ? guide->block_rows : nullptr);
   WFPG_CHECK_LAUNCH("k_guide_fill");
   return WFPG_OK;
 }
@@ -600,6 +631,7 @@ extern "C" int wfpg_generate_fields(const wfpg_scene* scene, const wfpg_svo* svo
   for (int k = 0; k <= 2 * blur_radius && blur_radius > 0; ++k) bp.w[k] = blur_w[k];
   FieldOut out{guide->vals, guide->row_sum, guide->marg, guide->total,
                guide->mode == 2 ? guide->block_sums : nullptr, guide->eps, guide->cum};
+  out.block_rows = guide->mode == 2 ? guide->block_rows : nullptr;
   guide->n = n;
   return launch_fields(make_scene_view(scene), make_view(svo), origins, jitters, n_bins,
                        n_bins_dev, n, bp, out, as_stream(stream));

@@ -23,6 +23,10 @@ struct FieldOut {
   // stay indexed by bin); nb_max / nb_dev then count work items.  Multi-GPU
   // ranks generate only the bins their own paths belong to.
   const int32_t* bin_list = nullptr;
+  // optional (B, 8, 8, n/8) product-mode block row sums (0 + pairwise row
+  // sum of each row of each 8x8 block, guiding.py:304): the product sampler
+  // reads its block marginal from here instead of re-summing the rows
+  double* block_rows = nullptr;
 };
 
 int launch_fields(const SceneView& s, const SvoView& v, const double* origins,

@@ -358,6 +358,7 @@ struct PassLayout {
   double* marg;
   double* tot;
   double* block_sums;
+  double* block_rows;
   double* cum;
   int32_t* bin_ctr;  // dynamic bin scheduling of the field kernels
   uint8_t* dirty;
@@ -446,6 +447,7 @@ static void carve_pass(Arena& a, const wfpg_svo* svo, const wfpg_camera* cam,
       L.marg = a.take<double>(L.cap * (int64_t)L.n0);
       L.tot = a.take<double>(L.cap);
       L.block_sums = cfg->product ? a.take<double>(L.cap * 64) : nullptr;
+      L.block_rows = cfg->product ? a.take<double>(L.cap * 8 * (int64_t)L.n0) : nullptr;
       L.cum = a.take<double>(L.cap * (int64_t)L.n0 * L.n0);
       L.bin_ctr = a.take<int32_t>(4);
     }
@@ -687,6 +689,7 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
         FieldOut fo{L.vals, L.row_sum, L.marg, L.tot, cfg->product ? L.block_sums : nullptr,
                     cfg->epsilon, L.cum, L.bin_ctr};
         // multi-GPU: only the bins holding this rank's paths
+        fo.block_rows = cfg->product ? L.block_rows : nullptr;
         const int32_t* work_n = global ? L.n_need : L.n_bins;
         fo.bin_list = global ? L.need_list : nullptr;
         WFPG_CUDA(cudaMemsetAsync(L.bin_ctr, 0, sizeof(int32_t), st));
@@ -709,6 +712,7 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
         gv.marg = L.marg;
         gv.total = L.tot;
         gv.block_sums = L.block_sums;
+        gv.block_rows = cfg->product ? L.block_rows : nullptr;
         gv.cum = L.cum;
         gv.upper_dirs = cfg->upper_dirs;
         slots = L.bin_slot;

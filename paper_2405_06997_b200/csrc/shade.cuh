@@ -17,6 +17,7 @@ struct GuideView {
   const double* block_sums;
   const double* upper_dirs;  // (8,8,3) host-numpy octahedral cell centres
   const double* cum;         // optional row prefix sums (plain sampler fast path)
+  const double* block_rows;  // optional (B,8,8,m) block row sums (product sampler)
 };
 
 // upper_bound (_kernels.pyx:802-812)
@@ -284,12 +285,15 @@ __device__ __forceinline__ void sample_product(const GuideView& g, int slot, con
   // marginal is cumsum(rows) / block_sum (guiding.py:304-309)
   const double* blk = g.vals + ((int64_t)slot * n + bj * m) * n + bi * m;
   const double bsum = g.block_sums[((int64_t)slot * 8 + bj) * 8 + bi];
+  const double* brows =
+      g.block_rows ? g.block_rows + (((int64_t)slot * 8 + bj) * 8 + bi) * m : nullptr;
   int jin = m - 1;
   double rowj = 0.0;
   {
     double run = 0.0, prev = 0.0, cur = 0.0;
     for (int r = 0; r < m; ++r) {
-      const double rr = __dadd_rn(0.0, pairwise_row(blk + (int64_t)r * n, m));
+      const double rr =
+          brows ? __ldg(brows + r) : __dadd_rn(0.0, pairwise_row(blk + (int64_t)r * n, m));
       run = r == 0 ? rr : __dadd_rn(run, rr);
       cur = __ddiv_rn(run, bsum);
       if (cur > s3 || r == m - 1) {

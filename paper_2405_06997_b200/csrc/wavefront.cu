@@ -537,6 +537,7 @@ GuideView make_guide_view(const wfpg_guide* g) {
   v.block_sums = g->block_sums;
   v.upper_dirs = g->upper_dirs;
   v.cum = g->cum;
+  v.block_rows = g->mode == 2 ? g->block_rows : nullptr;
   return v;
 }
 

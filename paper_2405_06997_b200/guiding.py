@@ -212,6 +212,8 @@ class GuideTables:
         self.d_marg = _dev.zeros((b, n), np.float64)
         self.d_total = _dev.zeros((b,), np.float64)
         self.d_block_sums = _dev.zeros((b, 8, 8), np.float64) if mode == 2 else None
+        self.d_block_rows = (_dev.zeros((b, 8, 8, max(1, n // 8)), np.float64) if mode == 2
+                             else None)
         self.d_cum = _dev.zeros((b, n, n), np.float64)
         self._expanded = None
         self._cum_valid = False
@@ -227,6 +229,7 @@ class GuideTables:
         g.marg = self.d_marg.data_ptr()
         g.total = self.d_total.data_ptr()
         g.block_sums = self.d_block_sums.data_ptr() if self.d_block_sums is not None else None
+        g.block_rows = self.d_block_rows.data_ptr() if self.d_block_rows is not None else None
         g.n_bins = None
         g.upper_dirs = upper_dirs_device().data_ptr()
         g.cum = self.d_cum.data_ptr() if self._cum_valid else None

@@ -29,10 +29,14 @@ import numpy as np
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, REPO)
 
-SCENES = {"c2": ("cornell.scene", 1024), "c3": ("c3_two_rooms.scene", 2048)}
+SCENES = {"c2": ("cornell.scene", 1024), "c3": ("c3_two_rooms.scene", 2048),
+          "enclosed": ("cornell_enclosed.scene", 256)}
 
 
-def _runners(scene, svo, conf):
+def _runners(scene, svo, conf, k=1):
+    """Pass i (1-based) -> its PassRunner; every pass renders k samples per
+    pixel (render_pass with a k-entry sample list: one set of fields per k
+    samples, wavefront.py:198-215)."""
     from paper_2405_06997_b200 import cli, wavefront
 
     guided = conf.guided_depths if conf.mode != "pt" else 0
@@ -44,47 +48,57 @@ def _runners(scene, svo, conf):
             c = cli._pass_cfg(conf, g)
             if svo is not None:
                 c.l_min = conf.effective_lmin(svo.depth)
-            runners[g] = wavefront.PassRunner(scene, svo, c, 1)
+            runners[g] = wavefront.PassRunner(scene, svo, c, k)
         return runners[g]
 
     return lambda i: runner(0 if (pt_first and i == 1) else guided)
 
 
-def pass_ms(scene, svo, conf, reps=10):
+def pass_ms(scene, svo, conf, reps=10, k=1):
     """Steady-state device time of one pass (graph replay), CUDA events."""
     import torch
 
-    get = _runners(scene, svo, conf)
+    get = _runners(scene, svo, conf, k)
     r = get(2)  # a guided pass (or the PT pass in pt mode)
-    for k in range(3):  # eager, capture, replay
-        r.launch(k + 2, want_stats=False)
+    for j in range(3):  # eager, capture, replay
+        r.launch((j + 2) * k, want_stats=False)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for k in range(reps):
-        r.launch(k + 5, want_stats=False)
+    for j in range(reps):
+        r.launch((j + 5) * k, want_stats=False)
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps
 
 
-def curve(scene, svo, conf, max_spp, checkpoints, ref):
-    """Accumulate passes 1..max_spp; [(spp, relMSE, mse)] at the checkpoints
-    and at max_spp (the accumulated frame when ref is None)."""
+def curve(scene, svo, conf, max_spp, checkpoints, ref, k=1):
+    """Accumulate passes of k samples up to max_spp samples; [(spp, relMSE,
+    mse)] at the checkpoints and at max_spp (the accumulated frame when ref
+    is None)."""
     from paper_2405_06997_b200 import accumulation as A
 
     cam = scene.camera
-    get = _runners(scene, svo, conf)
+    get = _runners(scene, svo, conf, k)
     buf = A.AccumulationBuffer(cam.height, cam.width, conf.heuristic)
     out = []
-    for i in range(1, max_spp + 1):
+    for i in range(1, max_spp // k + 1):
         r = get(i)
-        r.launch(i - 1, want_stats=False)
+        r.launch((i - 1) * k, want_stats=False)
         buf.add_sample(r.frame, i)
-        if ref is not None and (i in checkpoints or i == max_spp):
+        spp = i * k
+        if ref is not None and (spp in checkpoints or i == max_spp // k):
             f = buf.resolve()
-            out.append((i, A.rel_mse(f, ref), A.mse(f, ref)))
+            out.append((spp, A.rel_mse(f, ref), A.mse(f, ref)))
     return out, buf
+
+
+def _bins_per_depth(scene, svo, conf, k):
+    """Bins per depth of one more guided pass on a copy-free probe (stats)."""
+    get = _runners(scene, svo, conf, k)
+    r = get(2)
+    r.launch(10_000 * k, want_stats=True)
+    return r, r.pass_stats().bins_per_depth
 
 
 def main():
@@ -104,6 +118,10 @@ def main():
     ap.add_argument("--guided-depths", type=int, default=4)
     ap.add_argument("--field-res", type=int, default=128)
     ap.add_argument("--skip-pt", action="store_true", help="guided curve only")
+    ap.add_argument("--lmin", type=int, default=5)
+    ap.add_argument("--c-ray", type=int, default=512)
+    ap.add_argument("--spp-per-pass", type=int, default=1,
+                    help="samples per guided pass (one set of fields per pass)")
     args = ap.parse_args()
 
     import torch
@@ -131,7 +149,8 @@ def main():
     cps = {1 << k for k in range(0, 20)}
     g_conf = cli.RunConfig(path, mode=args.mode, spp=args.spp, depth=args.depth, svo_res=res,
                            seed=7, guided_depths=min(args.guided_depths, args.depth),
-                           field_res=args.field_res)
+                           field_res=args.field_res, lmin=args.lmin, cray=args.c_ray)
+    kpp = args.spp_per_pass
     p_conf = cli.RunConfig(path, mode="pt", spp=1 << 30, depth=args.depth, seed=7)
     # steady-state costs: SVO build, guided pass (on a scratch SVO), PT pass
     cur = torch.cuda.current_stream()
@@ -142,12 +161,13 @@ def main():
     b1.record(cur)
     torch.cuda.synchronize()
     build_ms = b0.elapsed_time(b1)
-    g_ms = pass_ms(sc, scratch, g_conf)
+    g_ms = pass_ms(sc, scratch, g_conf, k=kpp) / kpp  # per sample
     p_ms = pass_ms(sc, None, p_conf)
     del scratch
     # quality: guided to spp; unguided to the spp that costs the same time
     tree = svo_mod.build_from_scene(sc, res, seed=g_conf.seed)
-    g_pts, _ = curve(sc, tree, g_conf, args.spp, cps, ref)
+    g_pts, _ = curve(sc, tree, g_conf, args.spp, cps, ref, k=kpp)
+    _, bins = _bins_per_depth(sc, tree, g_conf, kpp)
     budget = build_ms + args.spp * g_ms
     pt_spp = max(args.spp, int(budget / p_ms))
     p_pts = [(0, float("nan"), float("nan"))] if args.skip_pt else \
@@ -157,6 +177,8 @@ def main():
         "bench": "relmse", "scene": args.scene, "image": [args.width, args.height],
         "svo_res": res, "max_depth": args.depth, "mode": args.mode,
         "guided_depths": g_conf.guided_depths, "field_res": g_conf.field_res,
+        "l_min": g_conf.effective_lmin(tree.depth), "c_ray": g_conf.cray,
+        "spp_per_pass": kpp, "bins_per_depth": bins,
         "reference": {"spp": args.ref_spp, "seed": 1_000_003, "kind": "unguided PT"},
         "svo_build_ms": build_ms, "guided_pass_ms": g_ms, "pt_pass_ms": p_ms,
         "guided": [{"spp": s_, "ms": build_ms + s_ * g_ms, "rel_mse": r, "mse": e}
