@@ -6,7 +6,7 @@ OUT=${OUT:-gpurun_out/relmse_r2.jsonl}
 SPP=${SPP:-64}
 mkdir -p gpurun_out
 for sc in c3 enclosed c2; do
-  REF=gpurun_out/ref_${sc}.npy
+  REF=/tmp/ref_${sc}.npy
   first=1
   for res in 128 256; do
     for mode in wfpg wfpg-product; do
