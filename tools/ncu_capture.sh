@@ -1,6 +1,7 @@
 #!/bin/bash
 # One `ncu --set full` capture per kernel regex of the C2 bench workload
-# (first guided pass), reports into gpurun_out/ncu_<tag>.ncu-rep.
+# (first guided pass); exports the raw metrics and the source/SASS page as CSV
+# next to gpurun_out/ncu_<tag>.log and drops the report unless KEEP_REP=1.
 #   tools/ncu_capture.sh tag:regex[:skip] ... [-- extra bench args]
 EXTRA=""
 SPECS=()
@@ -10,8 +11,12 @@ while [ $# -gt 0 ]; do
 done
 for spec in "${SPECS[@]}"; do
   IFS=: read -r tag rx skip <<< "$spec"
+  rep="/tmp/ncu_$tag"
   ncu --set full --import-source on --clock-control none -k "regex:$rx" -s "${skip:-0}" -c 1 \
-      -f -o "gpurun_out/ncu_$tag" python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
+      -f -o "$rep" python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
       --no-e2e $EXTRA > "gpurun_out/ncu_$tag.log" 2>&1
   echo "$tag rc=$?"
+  ncu -i "$rep.ncu-rep" --page raw --csv > "gpurun_out/ncu_${tag}_raw.csv" 2>/dev/null
+  ncu -i "$rep.ncu-rep" --page source --csv --print-source sass > "gpurun_out/ncu_${tag}_sass.csv" 2>/dev/null
+  [ "${KEEP_REP:-0}" = 1 ] && cp "$rep.ncu-rep" gpurun_out/
 done
