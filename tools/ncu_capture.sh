@@ -12,7 +12,7 @@ done
 for spec in "${SPECS[@]}"; do
   IFS=: read -r tag rx skip <<< "$spec"
   rep="/tmp/ncu_$tag"
-  ncu --set full --import-source on --clock-control none -k "regex:$rx" -s "${skip:-0}" -c 1 \
+  ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:$rx" -s "${skip:-0}" -c 1 \
       -f -o "$rep" python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
       --no-e2e $EXTRA > "gpurun_out/ncu_$tag.log" 2>&1
   echo "$tag rc=$?"
