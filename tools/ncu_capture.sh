@@ -17,6 +17,6 @@ for spec in "${SPECS[@]}"; do
       --no-e2e $EXTRA > "gpurun_out/ncu_$tag.log" 2>&1
   echo "$tag rc=$?"
   ncu -i "$rep.ncu-rep" --page raw --csv > "gpurun_out/ncu_${tag}_raw.csv" 2>/dev/null
-  ncu -i "$rep.ncu-rep" --page source --csv --print-source sass > "gpurun_out/ncu_${tag}_sass.csv" 2>/dev/null
+  ncu -i "$rep.ncu-rep" --page source --csv --print-source cuda,sass > "gpurun_out/ncu_${tag}_sass.csv" 2>/dev/null
   [ "${KEEP_REP:-0}" = 1 ] && cp "$rep.ncu-rep" gpurun_out/
 done
