@@ -257,6 +257,17 @@ typedef struct wfpg_pass_config {
    * bins' streams use sample_index, the list's first entry, as the
    * reference does (samples[0], wavefront.py:264). */
   const int64_t* sample_list;
+  /* Multi-GPU bin ownership, per depth (index = depth, 0 unused): an upper
+   * estimate of that depth's global bin count (e.g. 1.05x the previous
+   * pass's), or 0.  With an estimate E > 0 and comm set, rank r generates
+   * the fields of the bins [r*S, (r+1)*S), S = ceil(E / W), and the floored
+   * values of all bins are all-gathered (S * n * n doubles per rank); every
+   * rank then derives the other bins' tables from those values (bitwise the
+   * owners' tables).  When the depth's actual bin count exceeds W * S, every
+   * rank falls back to generating the bins its own paths use (exact either
+   * way).  0: that fallback policy always (right for depth 1, whose bins
+   * split with the image). */
+  int32_t own_bins[32];
 } wfpg_pass_config;
 
 /* Per-pass statistics returned to the host: wavefront.py:81-85 (PassStats). */

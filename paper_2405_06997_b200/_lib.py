@@ -94,6 +94,7 @@ class PassConfig(C.Structure):
         ("comm", c_vp),
         ("dep_wire_capacity", c_i64),
         ("sample_list", c_vp),
+        ("own_bins", c_i32 * 32),
     ]
 
 

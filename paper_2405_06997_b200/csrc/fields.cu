@@ -591,6 +591,84 @@ __global__ void k_guide_fill(const double* __restrict__ vals, int n, int64_t nb,
   }
 }
 
+// Multi-GPU bin ownership (render.cu): every rank generated the fields of
+// its own contiguous bin range [own_lo, own_hi) and the values of all bins
+// were all-gathered into `src` (standard bin order).  This fills every other
+// bin's tables from those values — values, row sums, marginal, total, row
+// prefix sums and (product) block row sums / block sums — with the field
+// kernel's arithmetic (numpy pairwise row sums, sequential cumsums), so the
+// tables equal the ones the owning rank computed, bit for bit.  Runs only when
+// *own_ok (the bin count fitted the ownership ranges).
+__global__ void k_own_fill(const double* __restrict__ src, int n, const int32_t* __restrict__ n_bins,
+                           const int32_t* __restrict__ own_ok, int64_t own_lo, int64_t own_hi,
+                           double* __restrict__ vals, double* __restrict__ cum,
+                           double* __restrict__ row_sum, double* __restrict__ marg,
+                           double* __restrict__ total, double* __restrict__ block_sums,
+                           double* __restrict__ block_rows) {
+  extern __shared__ double rs[];
+  if (!*own_ok) return;
+  const int64_t nb = *n_bins;
+  const int64_t nn = (int64_t)n * n;
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    if (b >= own_lo && b < own_hi) continue;  // generated here
+    const double* v = src + b * nn;
+    double* dv = vals + b * nn;
+    for (int64_t c = threadIdx.x; c < nn; c += blockDim.x) dv[c] = v[c];
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      const double* row = v + (int64_t)j * n;
+      double r = __dadd_rn(0.0, pairwise_row(row, n));
+      rs[j] = r;
+      row_sum[b * n + j] = r;
+      if (cum) {
+        double run = row[0];
+        double* cr = cum + b * nn + (int64_t)j * n;
+        cr[0] = run;
+        for (int i = 1; i < n; ++i) {
+          run = __dadd_rn(run, row[i]);
+          cr[i] = run;
+        }
+      }
+    }
+    if (block_sums) {
+      const int M = n / 8;
+      for (int q = threadIdx.x; q < 64; q += blockDim.x) {
+        const int bj = q / 8, bi = q % 8;
+        double acc = 0.0;
+        for (int r = 0; r < M; ++r) {
+          const double rr = __dadd_rn(0.0, pairwise_row(v + (int64_t)(bj * M + r) * n + bi * M, M));
+          if (block_rows) block_rows[(b * 64 + q) * M + r] = rr;
+          acc = __dadd_rn(acc, rr);
+        }
+        block_sums[b * 64 + q] = acc;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double tot = __dadd_rn(0.0, pairwise_row(rs, n));
+      total[b] = tot;
+      double run = 0.0;
+      for (int j = 0; j < n; ++j) {
+        run = j == 0 ? rs[0] : __dadd_rn(run, rs[j]);
+        rs[j] = run;
+      }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += blockDim.x) marg[b * n + j] = __ddiv_rn(rs[j], total[b]);
+    __syncthreads();
+  }
+}
+
+int launch_own_fill(const double* src, int n, const int32_t* n_bins, const int32_t* own_ok,
+                    int64_t own_lo, int64_t own_hi, int64_t cap, const FieldOut& out,
+                    cudaStream_t st) {
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cap, (int64_t)kNumSMs * 8));
+  k_own_fill<<<grid, 128, sizeof(double) * n, st>>>(src, n, n_bins, own_ok, own_lo, own_hi,
+                                                   out.vals, out.cum, out.row_sum, out.marg,
+                                                   out.total, out.block_sums, out.block_rows);
+  WFPG_CHECK_LAUNCH("k_own_fill");
+  return WFPG_OK;
+}
+
 }  // namespace wfpg
 
 using namespace wfpg;

@@ -33,4 +33,10 @@ int launch_fields(const SceneView& s, const SvoView& v, const double* origins,
                   const double* jitters, int64_t nb_max, const int32_t* nb_dev, int n,
                   const BlurParams& bp, const FieldOut& out, cudaStream_t st);
 
+// multi-GPU bin ownership: tables of the bins other ranks generated, from the
+// all-gathered values (bitwise the owners' tables)
+int launch_own_fill(const double* src, int n, const int32_t* n_bins, const int32_t* own_ok,
+                    int64_t own_lo, int64_t own_hi, int64_t cap, const FieldOut& out,
+                    cudaStream_t st);
+
 }  // namespace wfpg

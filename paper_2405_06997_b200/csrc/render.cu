@@ -257,6 +257,20 @@ __global__ void k_bin_setup_global(const int32_t* __restrict__ n_bins,
   }
 }
 
+// work-list flags of a guided depth: with bin ownership (own_hi > own_lo) the
+// rank's own bin range when the bin count fits W ranges (*own_ok), else (and
+// without ownership) the bins holding at least one of the rank's paths
+__global__ void k_work_flags(const int32_t* __restrict__ need, const int32_t* __restrict__ n_bins,
+                             int64_t cap, int64_t own_lo, int64_t own_hi, int64_t own_total,
+                             int32_t* __restrict__ own_ok, uint32_t* __restrict__ flags) {
+  const int64_t nb = *n_bins;
+  const bool own = own_hi > own_lo && nb <= own_total;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *own_ok = own ? 1 : 0;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < cap;
+       b += (int64_t)gridDim.x * blockDim.x)
+    flags[b] = (b < nb && (own ? (b >= own_lo && b < own_hi) : need[b] != 0)) ? 1u : 0u;
+}
+
 // bins that hold at least one of this rank's paths -> work list of the fields
 __global__ void k_need_list(const int32_t* __restrict__ need, const uint32_t* __restrict__ scan,
                             const int32_t* __restrict__ n_bins, int32_t* __restrict__ list,
@@ -266,14 +280,6 @@ __global__ void k_need_list(const int32_t* __restrict__ need, const uint32_t* __
        b += (int64_t)gridDim.x * blockDim.x)
     if (need[b]) list[scan[b]] = (int32_t)b;
   if (blockIdx.x == 0 && threadIdx.x == 0) *n_list = (int32_t)*total;
-}
-
-__global__ void k_need_flags(const int32_t* __restrict__ need, const int32_t* __restrict__ n_bins,
-                             int64_t cap, uint32_t* __restrict__ flags) {
-  const int64_t nb = *n_bins;
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < cap;
-       b += (int64_t)gridDim.x * blockDim.x)
-    flags[b] = (b < nb && need[b]) ? 1u : 0u;
 }
 
 // Deposit wire (fixed capacity per rank): record 0 = count, then up to `cap`
@@ -391,6 +397,9 @@ struct PassLayout {
   double* wdep_rad;
   int32_t* wdep_n;
   int32_t* status;
+  double* own_recv;   // all-gathered field values (bin ownership)
+  int32_t* own_ok;
+  int64_t own_seg[kMaxDepth + 1];  // S per depth (0: no ownership)
   size_t scratch_off;
 };
 
@@ -478,6 +487,22 @@ static void carve_pass(Arena& a, const wfpg_svo* svo, const wfpg_camera* cam,
     L.wdep_rad = a.take<double>(3 * wm);
     L.wdep_n = a.take<int32_t>(4);
     L.status = a.take<int32_t>(4);
+    // bin ownership per guided depth: S = ceil(E / W) bins per rank, usable
+    // when the W ranges fit the tables
+    int64_t recv = 0;
+    for (int d = 0; d <= kMaxDepth; ++d) {
+      L.own_seg[d] = 0;
+      if (d < 1 || d > cfg->guided_depths || d > cfg->max_depth || cfg->own_bins[d] <= 0) continue;
+      const int64_t S = ceil_div(cfg->own_bins[d], L.world);
+      if (S * L.world > L.cap) continue;
+      const int64_t n = std::max(8, cfg->field_res >> (d - 1));
+      L.own_seg[d] = S;
+      recv = std::max(recv, S * L.world * n * n);
+    }
+    L.own_recv = recv ? a.take<double>(recv) : nullptr;
+    L.own_ok = a.take<int32_t>(4);
+  } else {
+    for (int d = 0; d <= kMaxDepth; ++d) L.own_seg[d] = 0;
   }
   L.scratch_off = a.off;
   size_t scratch = std::max(scan_ws_bytes(P + 1), partition_ws_bytes(P));
@@ -659,8 +684,10 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
           size_t mk = scratch.off;
           uint32_t* nflags = scratch.take<uint32_t>(L.cap + 1);
           uint32_t* nscan = scratch.take<uint32_t>(L.cap + 1);
-          k_need_flags<<<bgrid, 128, 0, st>>>(L.need, L.n_bins, L.cap, nflags);
-          WFPG_CHECK_LAUNCH("k_need_flags");
+          const int64_t S = L.own_seg[depth];
+          k_work_flags<<<bgrid, 128, 0, st>>>(L.need, L.n_bins, L.cap, L.rank * S,
+                                              (L.rank + 1) * S, S * L.world, L.own_ok, nflags);
+          WFPG_CHECK_LAUNCH("k_work_flags");
           WFPG_TRY(scan_u32(nflags, nscan, L.cap, nullptr, L.total, scratch, st));
           k_need_list<<<bgrid, 128, 0, st>>>(L.need, nscan, L.n_bins, L.need_list, L.total,
                                              L.n_need);
@@ -701,6 +728,14 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
         if (prof) {
           k_stamp_end<<<1, 1, 0, st>>>(prof, depth, n, work_n);
           WFPG_CHECK_LAUNCH("k_stamp_end");
+        }
+        if (global && L.own_seg[depth] > 0) {
+          // bin ownership: everyone's floored values, then the other ranks'
+          // bins' tables derived locally (bitwise the owners')
+          const int64_t S = L.own_seg[depth], nn = (int64_t)n * n;
+          WFPG_TRY(comm_all_gather(comm, L.vals + L.rank * S * nn, L.own_recv, S * nn, kF64, st));
+          WFPG_TRY(launch_own_fill(L.own_recv, n, L.n_bins, L.own_ok, L.rank * S,
+                                   (L.rank + 1) * S, L.cap, fo, st));
         }
         gv.mode = cfg->product ? 2 : 1;
         gv.n = n;

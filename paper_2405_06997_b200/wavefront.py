@@ -229,6 +229,21 @@ class PassRunner:
 
         weakref.finalize(self, _release_graph, self.ws.data_ptr())
 
+    def set_ownership(self, bins_per_depth, margin=1.05, slack=64, first_depth=2):
+        """Multi-GPU bin ownership for the guided depths >= first_depth
+        (wfpg_pass_config.own_bins): each rank generates 1/W of the bins and
+        the values are all-gathered.  bins_per_depth: the global bin counts of
+        a previous pass (PassStats.bins_per_depth, identical on every rank);
+        the estimate E = margin * bins + slack, and a pass whose bins exceed
+        W * ceil(E / W) falls back to the exact needed-bin policy."""
+        for d in range(32):
+            self.pc.own_bins[d] = 0
+        if self.comm is None:
+            return
+        for d, b in enumerate(bins_per_depth, start=1):
+            if first_depth <= d <= min(31, int(self.cfg.guided_depths)):
+                self.pc.own_bins[d] = int(b * margin) + int(slack)
+
     def launch(self, sample_index, want_stats=True, sample_list=None):
         """Enqueue one pass; with want_stats the call synchronises and fills self.stats.
         sample_list: the pass's sample indices when they are not sample_index,

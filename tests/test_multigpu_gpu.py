@@ -47,7 +47,7 @@ def _one_gpu(sc, c, pt, g, samples):
     return tree, out
 
 
-def _ranks(sc, c, pt, g, samples, world, wire_capacity=0):
+def _ranks(sc, c, pt, g, samples, world, wire_capacity=0, own=None):
     import torch
 
     from paper_2405_06997_b200 import multigpu, svo, wavefront
@@ -73,6 +73,8 @@ def _ranks(sc, c, pt, g, samples, world, wire_capacity=0):
                     run = runners[0 if s == 0 else 1]
                     run.launch(s, want_stats=True)
                     frames.append((run.frame.cpu().numpy().copy(), run.pass_stats()))
+                    if own is not None and s > 0:  # bin ownership from the next pass on
+                        run.set_ownership(*own(frames[-1][1]))
                 comm.settle()
                 torch.cuda.synchronize()
                 res[r] = (tree, frames)
@@ -201,3 +203,64 @@ def test_nccl_communicator_world1_graph(golden, scene_path):
         comm.close()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,product,mode", [(2, False, "own"), (3, False, "own"),
+                                                (2, True, "own"), (2, False, "fallback")])
+def test_bin_ownership_reproduces_the_one_gpu_passes(golden, scene_path, world, product, mode):
+    """Depths >= 2 with bin ownership: each rank generates its own bin range,
+    the floored values are all-gathered and the other bins' tables derived
+    locally — frames, bins and SVOs stay the 1-GPU ones bit for bit.  The
+    fallback (more bins than the ownership ranges hold) must be exact too."""
+    c, sc = _setup(golden, scene_path)
+    pt, g = _cfgs(c, product)
+    samples = [0, 1, 2, 3]
+    one, ref = _one_gpu(sc, c, pt, g, samples)
+    if mode == "own":
+        own = lambda st: (st.bins_per_depth,)  # noqa: E731
+    else:
+        own = lambda st: ([1] * len(st.bins_per_depth), 0.0, 1)  # noqa: E731
+    ranks = _ranks(sc, c, pt, g, samples, world, own=own)
+    for k, s in enumerate(samples):
+        frame = np.concatenate([rk[1][k][0] for rk in ranks]).reshape(ref[k][0].shape)
+        np.testing.assert_array_equal(frame, ref[k][0], err_msg=f"sample {s}")
+        if s > 0:
+            for rk in ranks:
+                assert rk[1][k][1].bins_per_depth == ref[k][1].bins_per_depth
+    for tree, _ in ranks:
+        for key in SVO_KEYS:
+            assert np.array_equal(getattr(tree, key).view(np.uint64),
+                                  getattr(one, key).view(np.uint64)), key
+
+
+def test_bin_ownership_splits_the_field_work(golden, scene_path):
+    """With ownership the ranks' depth >= 2 field launches together generate
+    about the bins of one GPU (not W times them)."""
+    import ctypes as C
+
+    from paper_2405_06997_b200 import _lib
+
+    c, sc = _setup(golden, scene_path, 64, 64)
+    pt, g = _cfgs(c, False)
+    lib = _lib.load()
+    D = c["max_depth"]
+
+    def field_bins():
+        cones = (C.c_double * (D + 1))()
+        nl = (C.c_int64 * (D + 1))()
+        ms = (C.c_double * (D + 1))()
+        lib.wfpg_profile_read(ms, cones, nl, D)
+        lib.wfpg_profile_enable(1)
+        return [cones[d] / max(8, c["field_res"] >> (d - 1)) ** 2 for d in range(1, D + 1)]
+
+    one, ref = _one_gpu(sc, c, pt, g, [0, 1, 2])
+    lib.wfpg_profile_enable(1)
+    _one_gpu(sc, c, pt, g, [0, 1, 2])
+    single = field_bins()
+    world = 2
+    _ranks(sc, c, pt, g, [0, 1, 2], world, own=lambda st: (st.bins_per_depth,))
+    both = field_bins()
+    lib.wfpg_profile_enable(0)
+    # sample 2 ran with ownership at depths >= 2: the ranks' bins add up to
+    # the single GPU's (plus the needed-bin depth-1 overlap and sample 1)
+    assert both[1] < 1.6 * single[1], (both, single)
