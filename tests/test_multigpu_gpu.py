@@ -253,14 +253,16 @@ def test_bin_ownership_splits_the_field_work(golden, scene_path):
         lib.wfpg_profile_enable(1)
         return [cones[d] / max(8, c["field_res"] >> (d - 1)) ** 2 for d in range(1, D + 1)]
 
-    one, ref = _one_gpu(sc, c, pt, g, [0, 1, 2])
+    samples = [0, 1, 2, 3]
+    one, ref = _one_gpu(sc, c, pt, g, samples)
     lib.wfpg_profile_enable(1)
-    _one_gpu(sc, c, pt, g, [0, 1, 2])
+    _one_gpu(sc, c, pt, g, samples)
     single = field_bins()
     world = 2
-    _ranks(sc, c, pt, g, [0, 1, 2], world, own=lambda st: (st.bins_per_depth,))
+    _ranks(sc, c, pt, g, samples, world, own=lambda st: (st.bins_per_depth,))
     both = field_bins()
     lib.wfpg_profile_enable(0)
-    # sample 2 ran with ownership at depths >= 2: the ranks' bins add up to
-    # the single GPU's (plus the needed-bin depth-1 overlap and sample 1)
-    assert both[1] < 1.6 * single[1], (both, single)
+    # samples 2 and 3 ran with ownership at depths >= 2: at most
+    # (W + 2) / 3 = 1.33x the single GPU's depth-2 bins (sample 1 is fully
+    # replicated at worst); without ownership it would approach W = 2x
+    assert both[1] < 1.45 * single[1], (both, single)
