@@ -64,6 +64,9 @@ def parse():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-own", action="store_true",
+                   help="N > 1: every rank generates the fields of the bins its paths use at "
+                        "every depth (no bin ownership for depths >= 2)")
     a = p.parse_args()
     if a.svo_res is None:
         a.svo_res = SCENES[a.scene][1]
@@ -96,7 +99,8 @@ def workload_config(args, svo_depth, world):
             "l2": "inputs larger than L2 (path state + guide tables > 126 MB)",
             "parallelism": "single GPU" if world == 1 else (
                 f"image bands x{world} ({'weak: one band per GPU' if args.weak else 'strong: one image split'}), "
-                "global Alg. 2 binning + per-pass deposit exchange (NCCL, in the pass graph)")}
+                "global Alg. 2 binning, depth-1 fields of the rank's own bins, bin ownership "
+                "for depths >= 2, per-pass deposit exchange (NCCL, in the pass graph)")}
 
 
 def peaks():
@@ -271,9 +275,12 @@ def run_b200(args):
     lib.wfpg_profile_enable(1)
     pt.launch(0, want_stats=True)
     sample = 1
-    for _ in range(max(args.warmup, 3)):
+    for w in range(max(args.warmup, 3)):
         gr.launch(sample, want_stats=True)
         sample += 1
+        if w == 0 and comm is not None and not args.no_own:
+            # bin ownership for depths >= 2 sized from this pass's global bins
+            gr.set_ownership(gr.pass_stats().bins_per_depth)
     stats = gr.pass_stats()
     if comm is not None:
         comm.settle()
@@ -403,7 +410,8 @@ def run_b200(args):
         "clocks": clocks.summary(),
     }
     if world > 1:
-        out["comm"] = {"backend": backend, "kind": comm.kind}
+        out["comm"] = {"backend": backend, "kind": comm.kind,
+                       "bin_ownership_depths": [d for d in range(32) if gr.pc.own_bins[d]]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, sc, tree, g_cfg, sample)
     if rank == 0:

@@ -219,15 +219,25 @@ class PassRunner:
         pc.comm = comm.ptr if comm is not None else None
         pc.dep_wire_capacity = int(wire_capacity)
         self.svo_abi = svo.abi() if svo is not None else None
-        nbytes = _lib.load().wfpg_render_workspace_bytes(
-            C.byref(scene.abi()), C.byref(self.svo_abi) if svo is not None else None,
-            C.byref(self.cam), C.byref(pc))
-        self.ws = _dev.workspace(nbytes)
+        self.ws = None
+        self._fit_workspace()
         self.stats = _lib.PassStats()
-        # drop this workspace's captured graph when the runner goes away
+
+    def _fit_workspace(self):
+        """(Re)size the pass workspace for the current configuration; a new
+        workspace drops the old one's captured graph."""
         import weakref
 
-        weakref.finalize(self, _release_graph, self.ws.data_ptr())
+        nbytes = _lib.load().wfpg_render_workspace_bytes(
+            C.byref(self.scene.abi()), C.byref(self.svo_abi) if self.svo is not None else None,
+            C.byref(self.cam), C.byref(self.pc))
+        if self.ws is not None and self.ws.numel() >= nbytes:
+            return
+        if self.ws is not None:
+            self._ws_finalizer()
+        self.ws = _dev.workspace(nbytes)
+        # drop this workspace's captured graph when the runner goes away
+        self._ws_finalizer = weakref.finalize(self, _release_graph, self.ws.data_ptr())
 
     def set_ownership(self, bins_per_depth, margin=1.05, slack=64, first_depth=2):
         """Multi-GPU bin ownership for the guided depths >= first_depth
@@ -243,6 +253,7 @@ class PassRunner:
         for d, b in enumerate(bins_per_depth, start=1):
             if first_depth <= d <= min(31, int(self.cfg.guided_depths)):
                 self.pc.own_bins[d] = int(b * margin) + int(slack)
+        self._fit_workspace()
 
     def launch(self, sample_index, want_stats=True, sample_list=None):
         """Enqueue one pass; with want_stats the call synchronises and fills self.stats.
