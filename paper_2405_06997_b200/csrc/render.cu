@@ -272,13 +272,13 @@ __global__ void k_work_flags(const int32_t* __restrict__ need, const int32_t* __
 }
 
 // bins that hold at least one of this rank's paths -> work list of the fields
-__global__ void k_need_list(const int32_t* __restrict__ need, const uint32_t* __restrict__ scan,
+__global__ void k_need_list(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ scan,
                             const int32_t* __restrict__ n_bins, int32_t* __restrict__ list,
                             const uint32_t* __restrict__ total, int32_t* __restrict__ n_list) {
   const int64_t nb = *n_bins;
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb;
        b += (int64_t)gridDim.x * blockDim.x)
-    if (need[b]) list[scan[b]] = (int32_t)b;
+    if (flags[b]) list[scan[b]] = (int32_t)b;
   if (blockIdx.x == 0 && threadIdx.x == 0) *n_list = (int32_t)*total;
 }
 
@@ -689,7 +689,7 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
                                               (L.rank + 1) * S, S * L.world, L.own_ok, nflags);
           WFPG_CHECK_LAUNCH("k_work_flags");
           WFPG_TRY(scan_u32(nflags, nscan, L.cap, nullptr, L.total, scratch, st));
-          k_need_list<<<bgrid, 128, 0, st>>>(L.need, nscan, L.n_bins, L.need_list, L.total,
+          k_need_list<<<bgrid, 128, 0, st>>>(nflags, nscan, L.n_bins, L.need_list, L.total,
                                              L.n_need);
           WFPG_CHECK_LAUNCH("k_need_list");
           scratch.off = mk;

@@ -105,4 +105,5 @@ def test_b200_arm_two_ranks_gloo():
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "strong"
     assert d["config"]["image"] == [96, 64] and d["e2e"]["value"] > 0
     assert [r["paths_per_pass"] for r in d["per_rank"]] == [3072, 3072]
-    assert d["comm"] == {"backend": "gloo", "kind": "host"}
+    assert d["comm"]["backend"] == "gloo" and d["comm"]["kind"] == "host"
+    assert d["comm"]["bin_ownership_depths"] == [2, 3, 4]
