@@ -322,6 +322,7 @@ struct BuildWs {
   uint32_t* lvl_first;  // index of the first entry of each parent run ... (unused slot)
   uint32_t* leaf_start; // (L+1,)
   uint32_t* counts;     // (depth+1,) device level counts
+  int64_t* bases;       // (depth+2,) device offsets of the levels in lvl_codes
   int64_t cap_nodes;
 };
 
@@ -345,6 +346,7 @@ static void carve(Arena& a, int64_t F, int depth, BuildWs& w) {
   w.lvl_first = a.take<uint32_t>(1);
   w.leaf_start = a.take<uint32_t>(F + 1);
   w.counts = a.take<uint32_t>(depth + 2);
+  w.bases = a.take<int64_t>(depth + 2);
   w.cap_nodes = cap;
 }
 
@@ -395,6 +397,45 @@ __global__ void k_parent_level(const uint64_t* __restrict__ child, const uint32_
        k += (int64_t)gridDim.x * blockDim.x) {
     // exclusive scan of run-start flags: owner = inclusive - 1
     uint32_t o = scan[k] + flags[k] - 1u;
+    owner[k] = o;
+    if (flags[k]) parent_codes[o] = child[k] >> 3;
+  }
+}
+
+// Device-resident level bookkeeping of the structure phase: the levels are
+// packed bottom-up in lvl_codes, level l at bases[l] = bases[l+1] +
+// counts[l+1]; every per-level kernel reads its size and offsets from device
+// memory, so building the levels needs no host round trip (the capacity
+// node_capacity() bounds every level: count_l <= min(F, 8^l)).
+__global__ void k_level_base(const uint32_t* __restrict__ counts, int64_t* __restrict__ bases,
+                             int l) {
+  bases[l] = bases[l + 1] + (int64_t)counts[l + 1];
+}
+
+__global__ void k_run_flags_lvl(const uint64_t* __restrict__ lvl_codes,
+                                const int64_t* __restrict__ bases,
+                                const uint32_t* __restrict__ counts, int lvl, int shift,
+                                uint32_t* __restrict__ flags) {
+  const int64_t n = counts[lvl];
+  const uint64_t* codes = lvl_codes + bases[lvl];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    flags[i] = (i == 0 || (codes[i] >> shift) != (codes[i - 1] >> shift)) ? 1u : 0u;
+}
+
+__global__ void k_parent_level_lvl(uint64_t* __restrict__ lvl_codes,
+                                   uint32_t* __restrict__ lvl_owner,
+                                   const int64_t* __restrict__ bases,
+                                   const uint32_t* __restrict__ counts, int lvl,
+                                   const uint32_t* __restrict__ flags,
+                                   const uint32_t* __restrict__ scan) {
+  const int64_t n = counts[lvl];
+  const uint64_t* child = lvl_codes + bases[lvl];
+  uint32_t* owner = lvl_owner + bases[lvl];
+  uint64_t* parent_codes = lvl_codes + bases[lvl - 1];
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t o = scan[k] + flags[k] - 1u;  // inclusive scan - 1
     owner[k] = o;
     if (flags[k]) parent_codes[o] = child[k] >> 3;
   }
@@ -457,36 +498,32 @@ extern "C" int wfpg_svo_build_structure(wfpg_svo* svo, const int32_t* frag_coord
     WFPG_TRY(scan_u32(w.flags, w.scan, F, nullptr, cnt_leaf, a, st));
     a.off = mark;
   }
-  // level buffers are packed bottom-up: leaves at offset 0
-  std::vector<int64_t> lvl_base(depth + 1);
-  std::vector<uint32_t> lvl_count(depth + 1);
-  lvl_base[depth] = 0;
+  // level buffers are packed bottom-up: leaves at offset 0; sizes and
+  // offsets stay on the device until the single read-back below
+  WFPG_CUDA(cudaMemsetAsync(w.bases, 0, sizeof(int64_t) * (depth + 2), st));
   k_leaf_unique<<<grid, 256, 0, st>>>(w.codes, F, w.flags, w.scan, w.lvl_codes, w.leaf_start,
                                       cnt_leaf);
   WFPG_CHECK_LAUNCH("k_leaf_unique");
-  WFPG_CUDA(cudaMemcpyAsync(&lvl_count[depth], cnt_leaf, 4, cudaMemcpyDeviceToHost, st));
-  WFPG_CUDA(cudaStreamSynchronize(st));
   for (int l = depth - 1; l >= 0; --l) {
-    int64_t nc = lvl_count[l + 1];
-    int64_t cb = lvl_base[l + 1];
-    lvl_base[l] = cb + nc;
-    int64_t bound = l < 21 ? std::min<int64_t>(nc, (int64_t)1 << (3 * l)) : nc;
-    if (lvl_base[l] + bound > w.cap_nodes) {
-      set_error("svo build: node capacity exceeded");
-      return WFPG_ERR_CAPACITY;
-    }
-    int g = (int)std::min<int64_t>(ceil_div(nc, 256), (int64_t)kNumSMs * 8);
-    k_run_flags<<<g, 256, 0, st>>>(w.lvl_codes + cb, nc, nullptr, 3, w.flags);
-    WFPG_CHECK_LAUNCH("k_run_flags");
+    k_level_base<<<1, 1, 0, st>>>(w.counts, w.bases, l);
+    WFPG_CHECK_LAUNCH("k_level_base");
+    // level l + 1 holds at most min(F, 8^(l+1)) codes
+    const int64_t bound = l + 1 < 21 ? std::min<int64_t>(F, (int64_t)1 << (3 * (l + 1))) : F;
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(bound, 256), (int64_t)kNumSMs * 8));
+    k_run_flags_lvl<<<g, 256, 0, st>>>(w.lvl_codes, w.bases, w.counts, l + 1, 3, w.flags);
+    WFPG_CHECK_LAUNCH("k_run_flags_lvl");
     size_t mark = a.off;
-    WFPG_TRY(scan_u32(w.flags, w.scan, nc, nullptr, w.counts + l, a, st));
+    WFPG_TRY(scan_u32(w.flags, w.scan, bound, reinterpret_cast<const int32_t*>(w.counts + l + 1),
+                      w.counts + l, a, st));
     a.off = mark;
-    k_parent_level<<<g, 256, 0, st>>>(w.lvl_codes + cb, w.counts + l + 1, w.flags, w.scan,
-                                      w.lvl_owner + cb, w.lvl_codes + lvl_base[l]);
-    WFPG_CHECK_LAUNCH("k_parent_level");
-    WFPG_CUDA(cudaMemcpyAsync(&lvl_count[l], w.counts + l, 4, cudaMemcpyDeviceToHost, st));
-    WFPG_CUDA(cudaStreamSynchronize(st));
+    k_parent_level_lvl<<<g, 256, 0, st>>>(w.lvl_codes, w.lvl_owner, w.bases, w.counts, l + 1,
+                                          w.flags, w.scan);
+    WFPG_CHECK_LAUNCH("k_parent_level_lvl");
   }
+  std::vector<uint32_t> lvl_count(depth + 1);
+  WFPG_CUDA(cudaMemcpyAsync(lvl_count.data(), w.counts, sizeof(uint32_t) * (depth + 1),
+                            cudaMemcpyDeviceToHost, st));
+  WFPG_CUDA(cudaStreamSynchronize(st));
   int64_t off = 0;
   for (int l = 0; l <= depth; ++l) {
     svo->level_off[l] = off;
