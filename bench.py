@@ -64,6 +64,8 @@ def parse():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-overlap", action="store_true",
+                   help="one GPU: run the passes back to back on one stream (no PassPipeline)")
     p.add_argument("--no-own", action="store_true",
                    help="N > 1: every rank generates the fields of the bins its paths use at "
                         "every depth (no bin ownership for depths >= 2)")
@@ -275,13 +277,26 @@ def run_b200(args):
     lib.wfpg_profile_enable(1)
     pt.launch(0, want_stats=True)
     sample = 1
-    for w in range(max(args.warmup, 3)):
-        gr.launch(sample, want_stats=True)
-        sample += 1
-        if w == 0 and comm is not None and not args.no_own:
-            # bin ownership for depths >= 2 sized from this pass's global bins
-            gr.set_ownership(gr.pass_stats().bins_per_depth)
+    gr.launch(sample, want_stats=True)  # first guided pass: stats (bins per depth)
+    sample += 1
     stats = gr.pass_stats()
+    if comm is not None and not args.no_own:
+        # bin ownership for depths >= 2 sized from this pass's global bins
+        gr.set_ownership(stats.bins_per_depth)
+    # one GPU: consecutive passes on two streams, pass i+1's ray generation,
+    # intersection and first binning overlapping pass i's last depth and
+    # exitance update (wavefront.PassPipeline; same results as sequential
+    # passes).  Multi-GPU passes run back to back on one runner.
+    pipe = (wavefront.PassPipeline(sc, tree, g_cfg, runners=[gr, wavefront.PassRunner(
+        sc, tree, g_cfg, pixel_offset=off, n_pixels=npx)]) if world == 1 and not args.no_overlap
+        else None)
+    launch = (lambda s_: pipe.launch(s_)) if pipe else (lambda s_: gr.launch(s_, want_stats=False))
+    warmup = max(args.warmup, 5)  # >= 2 per pipeline runner: eager, then graph capture
+    for _ in range(warmup - 1):
+        launch(sample)
+        sample += 1
+    if pipe:
+        pipe.join()
     if comm is not None:
         comm.settle()
     torch.cuda.synchronize()
@@ -297,8 +312,10 @@ def run_b200(args):
         torch.cuda.synchronize()
         start.record(stream)
         for _ in range(args.steps):
-            gr.launch(sample, want_stats=False)
+            launch(sample)
             sample += 1
+        if pipe:
+            pipe.join()
         if comm is not None:
             comm.settle()  # the last pass's deposit exchange is part of the work
         end.record(stream)
@@ -397,6 +414,10 @@ def run_b200(args):
         "metric": METRIC,
         "value": value, "unit": "path samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "warmup_passes": {"guided": warmup, "pt_first": 1,
+                          "note": "untimed passes actually run before the timed region: at "
+                                  "least --warmup, and at least two per pipeline runner "
+                                  "(eager + CUDA-graph capture)"},
         "scaling": scaling(args), "vs_baseline": None, "dtype": "f64",
         "data": DATA.format(scene=SCENES[args.scene][0]),
         "config": workload_config(args, tree.depth, world),

@@ -268,6 +268,21 @@ typedef struct wfpg_pass_config {
    * way).  0: that fallback policy always (right for depth 1, whose bins
    * split with the image). */
   int32_t own_bins[32];
+  /* Inter-pass overlap on one GPU (optional cudaEvent_t handles, NULL = none;
+   * ignored with comm): passes on different streams may overlap where they
+   * touch disjoint state.  The pass waits for ev_wait_counters before its
+   * first Alg. 2 partition (the SVO's ray counters are shared) and for
+   * ev_wait_svo before it first reads or writes the SVO exitance (fields or
+   * the exitance update); it records ev_rec_counters after its last
+   * partition and ev_rec_svo after its exitance update.  Chaining pass i+1's
+   * waits on pass i's records keeps the reference's pass order for every
+   * SVO access (wavefront.FramePipeline), while pass i+1's ray generation,
+   * intersection and first binning overlap pass i's last depth and update.
+   * Captured graphs contain them as external event nodes. */
+  void* ev_wait_counters;
+  void* ev_wait_svo;
+  void* ev_rec_counters;
+  void* ev_rec_svo;
 } wfpg_pass_config;
 
 /* Per-pass statistics returned to the host: wavefront.py:81-85 (PassStats). */
@@ -300,6 +315,9 @@ int64_t wfpg_abi_offsetof(int32_t struct_id, const char* field);
 /* ------------------------------------------------------------------------ */
 
 typedef struct wfpg_comm wfpg_comm;
+/* A cudaEvent_t (timing disabled) for wfpg_pass_config's overlap events. */
+int wfpg_event_create(void** event);
+int wfpg_event_destroy(void* event);
 /* cudaMemcpyAsync(cudaMemcpyDefault) on `stream` + synchronise: lets a host
  * exchange callback stage device buffers without a CUDA binding of its own. */
 int wfpg_memcpy(void* dst, const void* src, size_t bytes, void* stream);

@@ -95,6 +95,8 @@ class PassConfig(C.Structure):
         ("dep_wire_capacity", c_i64),
         ("sample_list", c_vp),
         ("own_bins", c_i32 * 32),
+        ("ev_wait_counters", c_vp), ("ev_wait_svo", c_vp),
+        ("ev_rec_counters", c_vp), ("ev_rec_svo", c_vp),
     ]
 
 
@@ -125,6 +127,8 @@ _SIGS = {
     "wfpg_abi_sizeof": (c_i64, [c_i32]),
     "wfpg_abi_offsetof": (c_i64, [c_i32, C.c_char_p]),
     "wfpg_memcpy": (c_i32, [c_vp, c_vp, c_size, c_vp]),
+    "wfpg_event_create": (c_i32, [P(c_vp)]),
+    "wfpg_event_destroy": (c_i32, [c_vp]),
     "wfpg_comm_nccl_available": (c_i32, []),
     "wfpg_comm_nccl_unique_id": (c_i32, [c_vp]),
     "wfpg_comm_init_nccl": (c_i32, [c_i32, c_i32, c_vp, P(c_vp)]),

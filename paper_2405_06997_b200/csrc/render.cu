@@ -589,6 +589,25 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
   bp.radius = cfg->blur_radius;
   for (int k = 0; k <= 2 * bp.radius && bp.radius > 0; ++k) bp.w[k] = cfg->blur_w[k];
 
+  // inter-pass overlap events (single GPU): external event nodes under capture
+  const bool overlap = !comm;
+  cudaStreamCaptureStatus cap_status = cudaStreamCaptureStatusNone;
+  WFPG_CUDA(cudaStreamIsCapturing(st, &cap_status));
+  const bool capturing = cap_status == cudaStreamCaptureStatusActive;
+  auto wait_ev = [&](void* ev) -> int {
+    if (overlap && ev)
+      WFPG_CUDA(cudaStreamWaitEvent(st, (cudaEvent_t)ev, capturing ? cudaEventWaitExternal : 0));
+    return WFPG_OK;
+  };
+  auto rec_ev = [&](void* ev) -> int {
+    if (overlap && ev)
+      WFPG_CUDA(cudaEventRecordWithFlags((cudaEvent_t)ev, st,
+                                         capturing ? cudaEventRecordExternal : 0));
+    return WFPG_OK;
+  };
+  bool counters_waited = false, svo_waited = false;
+  if (!svo) WFPG_TRY(rec_ev(cfg->ev_rec_counters));
+
   for (int depth = 1; depth <= cfg->max_depth; ++depth) {
     // live queue (np.nonzero(state.alive), wavefront.py:227)
     k_flags_alive<<<grid, 256, 0, st>>>(paths->alive, P, L.flags);
@@ -629,6 +648,10 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
       const bool want_image = depth == 1 && cfg->bin_image;
       if (guided_depth || want_image) {
         WFPG_CUDA(cudaMemsetAsync(L.bin_slot, 0xFF, sizeof(int32_t) * P, st));
+      }
+      if (!counters_waited) {  // the previous pass's partitions are done with the counters
+        WFPG_TRY(wait_ev(cfg->ev_wait_counters));
+        counters_waited = true;
       }
       // bin slots of guided depths are written by the partition itself
       PartitionOut po{L.bin_node, L.bin_start, L.bin_count, nullptr, L.n_bins,
@@ -705,6 +728,7 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
         WFPG_CHECK_LAUNCH("k_bin_setup");
         scratch.off = mark;
       }
+      if (depth == cfg->max_depth) WFPG_TRY(rec_ev(cfg->ev_rec_counters));
       if (want_image) {
         int igrid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(L.n_pix, 256), kNumSMs * 8));
         k_bin_image<<<igrid, 256, 0, st>>>(L.bin_slot, L.bin_node, L.n_pix, P / L.n_pix,
@@ -723,6 +747,10 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
         if (prof) {
           k_stamp_begin<<<1, 1, 0, st>>>(prof, depth);
           WFPG_CHECK_LAUNCH("k_stamp_begin");
+        }
+        if (!svo_waited) {  // the previous pass's exitance update is complete
+          WFPG_TRY(wait_ev(cfg->ev_wait_svo));
+          svo_waited = true;
         }
         WFPG_TRY(launch_fields(sv, vv, L.origins, L.jitters, L.cap, work_n, n, bp, fo, st));
         if (prof) {
@@ -757,6 +785,7 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
                           cfg->russian_roulette != 0, cfg->rr_depth, st));
   }
 
+  if (svo && !svo_waited) WFPG_TRY(wait_ev(cfg->ev_wait_svo));
   if (multi) {
     // Eq. 5 deposits of every rank, splatted in global path order (bands are
     // rank-ordered), so each rank's SVO update equals the 1-GPU update
@@ -810,6 +839,7 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
                              paths->rec_pos, cfg->max_depth + 1, P, cfg->deterministic,
                              &L.stats->deposits, scratch, st, 2, L.dirty));
   }
+  if (svo) WFPG_TRY(rec_ev(cfg->ev_rec_svo));
   k_frame<<<(int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(L.n_pix, 256), kNumSMs * 8)), 256,
             0, st>>>(paths->radiance, L.n_pix, cfg->n_samples, frame);
   WFPG_CHECK_LAUNCH("k_frame");
@@ -949,22 +979,29 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
     // graphs are captured / replayed on a private non-blocking stream joined to
     // the caller's stream with events (the legacy default stream cannot be
     // captured)
-    static cudaStream_t gs = nullptr;
+    static cudaStream_t gs0 = nullptr;
     static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    if (!gs) {
-      WFPG_CUDA(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking));
+    if (!gs0) {
+      WFPG_CUDA(cudaStreamCreateWithFlags(&gs0, cudaStreamNonBlocking));
       WFPG_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
       WFPG_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
     }
-    if (ge || seen) {
+    // a caller's own stream is captured / replayed on directly (so passes on
+    // different streams can overlap); the legacy default stream cannot be
+    // captured, so its passes go through a private stream joined by events
+    const bool own_stream = st != nullptr && st != cudaStreamLegacy && st != cudaStreamPerThread;
+    cudaStream_t gs = own_stream ? st : gs0;
+    if ((ge || seen) && !own_stream) {
       WFPG_CUDA(cudaEventRecord(ev_fork, st));
       WFPG_CUDA(cudaStreamWaitEvent(gs, ev_fork, 0));
     }
     if (ge) {
       WFPG_CUDA(cudaGraphLaunch(ge->exec, gs));
       count_launch(ge->kernels);
-      WFPG_CUDA(cudaEventRecord(ev_join, gs));
-      WFPG_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
+      if (!own_stream) {
+        WFPG_CUDA(cudaEventRecord(ev_join, gs));
+        WFPG_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
+      }
     } else if (!seen) {
       // first pass of this configuration runs eagerly (one-time kernel attribute
       // setup happens outside any capture); the next one is captured
@@ -1001,8 +1038,10 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
       g_graphs.push_back({workspace, key, exec, kernels});
       WFPG_CUDA(cudaGraphLaunch(exec, gs));
       count_launch(kernels);
-      WFPG_CUDA(cudaEventRecord(ev_join, gs));
-      WFPG_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
+      if (!own_stream) {
+        WFPG_CUDA(cudaEventRecord(ev_join, gs));
+        WFPG_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
+      }
     }
   }
 

@@ -28,6 +28,23 @@ void count_launch(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxe
 
 extern "C" int wfpg_abi_version(void) { return WFPG_ABI_VERSION; }
 
+extern "C" int wfpg_event_create(void** event) {
+  if (!event) {
+    wfpg::set_error("wfpg_event_create: bad arguments");
+    return WFPG_ERR_ARG;
+  }
+  cudaEvent_t e;
+  cudaError_t err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  if (err != cudaSuccess) return wfpg::cuda_status(err, "cudaEventCreateWithFlags");
+  *event = (void*)e;
+  return WFPG_OK;
+}
+
+extern "C" int wfpg_event_destroy(void* event) {
+  if (event) cudaEventDestroy((cudaEvent_t)event);
+  return WFPG_OK;
+}
+
 extern "C" int wfpg_memcpy(void* dst, const void* src, size_t bytes, void* stream) {
   if (bytes == 0) return WFPG_OK;
   if (!dst || !src) {

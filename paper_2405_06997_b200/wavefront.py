@@ -351,15 +351,89 @@ def render_pass(scene, svo, cfg, sample_indices, collect_bin_image=False, out=No
     return frame, r.pass_stats()
 
 
+class _Event:
+    """A native cudaEvent_t (wfpg_event_create) for the overlap chain."""
+
+    def __init__(self):
+        self.h = C.c_void_p()
+        _lib.call("wfpg_event_create", C.byref(self.h))
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown
+        try:
+            _lib.load().wfpg_event_destroy(self.h)
+        except Exception:
+            pass
+
+
+class PassPipeline:
+    """Consecutive passes of one configuration on two streams that overlap
+    where the reference's pass order allows (wfpg_pass_config ev_*): pass
+    i+1's ray generation, depth-1 intersection and binning run while pass i
+    finishes its last depth and its exitance update; every SVO access (the
+    Alg. 2 counters, the exitance read by the fields and written by the
+    update) still happens in pass order, so the results equal calling
+    render_pass once per sample, bit for bit.  Two PassRunners alternate
+    (two path states, frames and workspaces); ``launch(sample)`` returns the
+    runner of that pass; ``join()`` makes the caller's stream wait for all
+    of them."""
+
+    def __init__(self, scene, svo, cfg, runners=None):
+        t = _dev.torch()
+        if svo is not None:
+            cfg.validate(svo.depth)
+        self.runners = runners or [PassRunner(scene, svo, cfg) for _ in range(2)]
+        self.streams = [t.cuda.Stream() for _ in self.runners]
+        self.rec_counters = [_Event() for _ in self.runners]
+        self.rec_svo = [_Event() for _ in self.runners]
+        self.done = [t.cuda.Event() for _ in self.runners]
+        n = len(self.runners)
+        for k, r in enumerate(self.runners):
+            prev = (k - 1) % n
+            r.pc.ev_wait_counters = self.rec_counters[prev].h.value
+            r.pc.ev_wait_svo = self.rec_svo[prev].h.value
+            r.pc.ev_rec_counters = self.rec_counters[k].h.value
+            r.pc.ev_rec_svo = self.rec_svo[k].h.value
+        self.k = 0
+        self._forked = False
+
+    def _fork(self):
+        t = _dev.torch()
+        cur = t.cuda.current_stream()
+        for s in self.streams:
+            s.wait_stream(cur)
+        self._forked = True
+
+    def launch(self, sample, want_stats=False, before=None):
+        """Enqueue the next pass; `before` (optional) is a torch event the
+        pass's stream waits for first (e.g. its frame's previous copy)."""
+        t = _dev.torch()
+        if not self._forked:
+            self._fork()
+        slot = self.k % len(self.runners)
+        self.k += 1
+        r = self.runners[slot]
+        with t.cuda.stream(self.streams[slot]):
+            if before is not None:
+                self.streams[slot].wait_event(before)
+            r.launch(int(sample), want_stats=want_stats)
+            self.done[slot].record(self.streams[slot])
+        return slot, r
+
+    def join(self):
+        t = _dev.torch()
+        cur = t.cuda.current_stream()
+        for s in self.streams:
+            cur.wait_stream(s)
+        self._forked = False
+
+
 class FramePipeline:
     """Consecutive single-sample passes whose frames arrive in page-locked host
-    memory, with the device-to-host copy of pass i overlapped with pass i+1.
-
-    Two PassRunners alternate (two frame buffers, two path states), the copy
-    runs on its own stream after an event recorded at the end of each pass,
-    and a runner only writes its frame again once that frame's previous copy
-    has finished.  Passes still run back to back on the caller's stream, so
-    the SVO learning sequence is exactly that of calling render_pass once per
+    memory: the passes run as a PassPipeline (pass i+1's start overlapping
+    pass i's end on a second stream), the device-to-host copy of pass i runs
+    on a copy stream overlapped with pass i+1, and a runner only writes its
+    frame again once that frame's previous copy has finished.  The SVO
+    learning sequence is exactly that of calling render_pass once per
     sample.  ``run(samples)`` yields (sample_index, frame, stats) with the
     frame an (H, W, 3) view of a pinned buffer that stays valid until the
     iterator advances twice more; stats are collected only if want_stats.
@@ -367,27 +441,21 @@ class FramePipeline:
 
     def __init__(self, scene, svo, cfg, want_stats=False):
         t = _dev.torch()
-        if svo is not None:
-            cfg.validate(svo.depth)
         self.scene, self.svo, self.cfg = scene, svo, cfg
         self.want_stats = want_stats
-        self.runners = [PassRunner(scene, svo, cfg) for _ in range(2)]
+        self.pipe = PassPipeline(scene, svo, cfg)
+        self.runners = self.pipe.runners
         self.host = [pinned_frame(scene) for _ in range(2)]
         self.copy_stream = t.cuda.Stream()
-        self.pass_done = [t.cuda.Event() for _ in range(2)]
         self.copy_done = [t.cuda.Event() for _ in range(2)]
         self.copied = [False, False]
 
     def _submit(self, k, sample):
         t = _dev.torch()
-        cur = t.cuda.current_stream()
         slot = k % 2
-        r = self.runners[slot]
-        if self.copied[slot]:  # frame buffer of this runner still being read?
-            cur.wait_event(self.copy_done[slot])
-        r.launch(int(sample), want_stats=self.want_stats)
-        self.pass_done[slot].record(cur)
-        self.copy_stream.wait_event(self.pass_done[slot])
+        before = self.copy_done[slot] if self.copied[slot] else None
+        slot, r = self.pipe.launch(int(sample), want_stats=self.want_stats, before=before)
+        self.copy_stream.wait_event(self.pipe.done[slot])
         with t.cuda.stream(self.copy_stream):
             dst = t.from_numpy(self.host[slot]).view(-1, 3)
             dst.copy_(r.frame, non_blocking=True)
@@ -409,6 +477,7 @@ class FramePipeline:
             pending = (slot, s)
         if pending is not None:
             yield self._deliver(*pending)
+        self.pipe.join()
 
 
 def render_sample(scene, svo, cfg, sample_index):

@@ -284,3 +284,39 @@ def test_partition_matches_oracle_at_scale(scene_path, res, l_min, c_ray):
     bins = wavefront.partition_spatial(tree, pos, np.arange(len(pos)), l_min, c_ray)
     assert [b.node for b in bins] == list(nodes)
     assert all(np.array_equal(b.members, m) for b, m in zip(bins, members))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("product", [False, True])
+def test_pass_pipeline_equals_sequential_passes(golden, scene_path, product):
+    """wavefront.PassPipeline (two runners on two streams, pass i+1's start
+    overlapping pass i's end, CUDA graphs captured and replayed) renders
+    exactly what sequential render_pass calls render: frames and SVO arrays
+    bit for bit (the overlap events keep every SVO access in pass order)."""
+    import torch
+
+    from paper_2405_06997_b200 import scene as S, svo, wavefront
+
+    sc = S.load_scene(scene_path("cornell.scene"))
+    cam = sc.camera
+    sc.camera = S.Camera(cam.position, cam.target, cam.up, cam.vfov_deg, 96, 64)
+    base = dict(max_depth=4, field_res=32, l_min=3, c_ray=16, seed=3, product=product)
+    pt = wavefront.GuidingConfig(guided_depths=0, **base)
+    g = wavefront.GuidingConfig(guided_depths=4, **base)
+    seq = svo.build_from_scene(sc, 64, seed=0)
+    wavefront.render_pass(sc, seq, pt, [0])
+    want = [wavefront.render_pass(sc, seq, g, [s])[0].copy() for s in range(1, 9)]
+    par = svo.build_from_scene(sc, 64, seed=0)
+    wavefront.render_pass(sc, par, pt, [0])
+    pipe = wavefront.PassPipeline(sc, par, g)
+    got = []
+    for s in range(1, 9):
+        _, r = pipe.launch(s)
+        with torch.cuda.stream(pipe.streams[(s - 1) % 2]):
+            got.append(r.frame.clone())
+    pipe.join()
+    torch.cuda.synchronize()
+    for s in range(8):
+        np.testing.assert_array_equal(got[s].cpu().numpy().reshape(want[s].shape), want[s])
+    for k in ("sum_a", "sum_b", "weight_a", "weight_b", "mean_a", "mean_b"):
+        assert np.array_equal(getattr(par, k).view(np.uint64), getattr(seq, k).view(np.uint64)), k
