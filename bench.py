@@ -370,14 +370,15 @@ def run_b200(args):
     e2e = None
     if world == 1 and not args.no_e2e:
         frame_bytes = npx * 3 * 8
-        pipe = wavefront.FramePipeline(sc, tree, g_cfg)
-        for _ in pipe.run(range(sample, sample + 3)):  # API warm-up (captures both graphs)
+        fpipe = wavefront.FramePipeline(sc, tree, g_cfg)
+        # API warm-up: two passes per pipeline runner (eager, graph capture)
+        for _ in fpipe.run(range(sample, sample + 4)):
             pass
-        sample += 3
+        sample += 4
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         checksum = 0.0
-        for _, f, _ in pipe.run(range(sample, sample + args.steps)):
+        for _, f, _ in fpipe.run(range(sample, sample + args.steps)):
             checksum += float(f[0, 0, 0])  # the host frame is read every step
         e2e_s = time.perf_counter() - t0
         sample += args.steps
