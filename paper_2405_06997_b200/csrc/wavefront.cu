@@ -130,10 +130,15 @@ __global__ void k_occluded(SceneView s, const double* __restrict__ orig,
 // ---------------------------------------------------------------------------
 // shading
 // ---------------------------------------------------------------------------
-__device__ void shade_path(int64_t p, int depth, const SceneView& sa, const GuideView& g,
-                           const PathsView& P, const double* hit_t, const int32_t* hit_tri,
-                           const int32_t* bin_slot, bool rr_enabled, int rr_depth,
-                           const TriRec* smt) {
+// BRUTE: shadow rays by brute force over the shared-memory triangles (small
+// scenes), else BVH traversal; separate instantiations keep the BVH
+// traversal's registers and stack out of the small-scene kernel
+template <bool BRUTE>
+__device__ __forceinline__ void shade_path(int64_t p, int depth, const SceneView& sa,
+                                           const GuideView& g, const PathsView& P,
+                                           const double* hit_t, const int32_t* hit_tri,
+                                           const int32_t* bin_slot, bool rr_enabled, int rr_depth,
+                                           const TriRec* smt) {
   int32_t tri = hit_tri[p];
   if (tri < 0) {
     P.alive[p] = 0;
@@ -261,10 +266,10 @@ __device__ void shade_path(int64_t p, int depth, const SceneView& sa, const Guid
         }
         // any-hit: brute force over the triangles in shared memory for small
         // scenes (the hit / no-hit answer does not depend on the traversal)
-        bool blocked = smt ? brute_occluded(smt, sa.n_tris, px, py, pz, lx, ly, lz, sa.ray_eps,
-                                            dist - sa.ray_eps)
-                           : bvh_occluded(sa, px, py, pz, lx, ly, lz, sa.ray_eps,
-                                          dist - sa.ray_eps);
+        bool blocked = BRUTE ? brute_occluded(smt, sa.n_tris, px, py, pz, lx, ly, lz,
+                                              sa.ray_eps, dist - sa.ray_eps)
+                             : bvh_occluded(sa, px, py, pz, lx, ly, lz, sa.ray_eps,
+                                            dist - sa.ray_eps);
         if (!blocked) {
           double p_cont;
           if (guided) {
@@ -360,6 +365,7 @@ __device__ void shade_path(int64_t p, int depth, const SceneView& sa, const Guid
   P.ctr[p] = c;
 }
 
+template <bool BRUTE>
 __global__ void __launch_bounds__(256, 3) k_shade(SceneView s, GuideView g, PathsView P, int depth,
                                                const int32_t* __restrict__ active, int64_t n_max,
                                                const int32_t* __restrict__ n_dev,
@@ -368,14 +374,14 @@ __global__ void __launch_bounds__(256, 3) k_shade(SceneView s, GuideView g, Path
                                                const int32_t* __restrict__ bin_slot, int rr,
                                                int rr_depth) {
   extern __shared__ TriRec smt_shade[];
-  if (s.brute) load_tris_smem(s, smt_shade);
+  if (BRUTE) load_tris_smem(s, smt_shade);
   __syncthreads();
   const int64_t n = dev_count(n_max, n_dev);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int64_t p = active ? active[i] : i;
-    shade_path(p, depth, s, g, P, hit_t, hit_tri, bin_slot, rr != 0, rr_depth,
-               s.brute ? smt_shade : nullptr);
+    shade_path<BRUTE>(p, depth, s, g, P, hit_t, hit_tri, bin_slot, rr != 0, rr_depth,
+                      smt_shade);
   }
 }
 
@@ -483,8 +489,12 @@ int launch_shade(const SceneView& s, const GuideView& g, const PathsView& P, int
   if (n_max <= 0) return WFPG_OK;
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_max, 256), kNumSMs * 8));
   const size_t smem = s.brute ? sizeof(TriRec) * s.n_tris : 0;
-  k_shade<<<grid, 256, smem, st>>>(s, g, P, depth, active, n_max, n_dev, hit_t, hit_tri,
-                                   bin_slot, rr ? 1 : 0, rr_depth);
+  if (s.brute)
+    k_shade<true><<<grid, 256, smem, st>>>(s, g, P, depth, active, n_max, n_dev, hit_t, hit_tri,
+                                           bin_slot, rr ? 1 : 0, rr_depth);
+  else
+    k_shade<false><<<grid, 256, smem, st>>>(s, g, P, depth, active, n_max, n_dev, hit_t, hit_tri,
+                                            bin_slot, rr ? 1 : 0, rr_depth);
   WFPG_CHECK_LAUNCH("k_shade");
   return WFPG_OK;
 }

@@ -9,10 +9,13 @@ identically on every rank.  A pass given a communicator
 the 1-GPU pass restricted to the band, path for path:
 
 * guided depths bin GLOBALLY: every rank all-gathers the Alg. 2 start nodes
-  of all ranks' lambert hits (one int32 per path), runs the same partition,
-  takes each bin's origin from the rank owning that path (an all-reduce of
-  bit patterns) and generates the fields of only the bins its own paths
-  belong to (depth-1 field work splits with the image; wavefront.py:98-195);
+  of all ranks' lambert hits (one int32 per path), runs the same partition
+  and takes each bin's origin from the rank owning that path (an all-reduce
+  of bit patterns; wavefront.py:98-195).  At depth 1 a rank generates the
+  fields of only the bins its own paths belong to (they split with the
+  image); at deeper depths, after ``PassRunner.set_ownership``, rank r
+  generates a contiguous 1/W of the bins and the floored values of all bins
+  are all-gathered, the other tables derived locally (bitwise the owners');
 * after the last depth every rank's Eq. 5 deposits are all-gathered and
   splatted in global path order (wavefront.py:286-332), so every rank's SVO
   equals the 1-GPU SVO bit for bit.
