@@ -184,14 +184,22 @@ struct ProductLayer {
   double nsx, nsy, nsz;
   double lum_pi;     // lum(albedo) / pi
   double mm;         // m * m
+  double inv_mm;     // 1 / (m * m), exact: m = n / 8 is a power of two
   double upsum;
   double urow[8];
 };
 
+// guiding.UPPER_DIRS (8,8,3), copied into constant memory by the shade
+// launcher: every lane reads cell k of its own layer at the same k, so the
+// reads are constant-cache broadcasts
+static __constant__ double c_upper_dirs[192];
+
 __device__ __forceinline__ double product_cell(const GuideView& g, const ProductLayer& L, int k) {
-  const double mean = __ldg(L.bs + k) / L.mm;
-  const double* ud = g.upper_dirs + 3 * k;
-  double cosf = __ldg(ud) * L.nsx + __ldg(ud + 1) * L.nsy + __ldg(ud + 2) * L.nsz;
+  // block_sums / (m m) (K:1008): m m is a power of two, so the product with
+  // its exact reciprocal is the same rounding of the same real number
+  const double mean = __dmul_rn(__ldg(L.bs + k), L.inv_mm);
+  const double* ud = c_upper_dirs + 3 * k;
+  double cosf = ud[0] * L.nsx + ud[1] * L.nsy + ud[2] * L.nsz;
   if (cosf < 0.0) cosf = 0.0;
   double val = mean * L.lum_pi * cosf;
   if (val < g.eps) val = g.eps;
@@ -207,6 +215,7 @@ __device__ __forceinline__ void product_layer(const GuideView& g, int slot, doub
   L->nsz = nsz;
   L->lum_pi = (0.2126 * alx + 0.7152 * aly + 0.0722 * alz) / WFPG_PI;
   L->mm = (double)(g.m * g.m);
+  L->inv_mm = 1.0 / L->mm;
   double upsum = 0.0;
 #pragma unroll
   for (int bj = 0; bj < 8; ++bj) {

@@ -487,6 +487,16 @@ int launch_shade(const SceneView& s, const GuideView& g, const PathsView& P, int
                  const int32_t* hit_tri, const int32_t* bin_slot, bool rr, int rr_depth,
                  cudaStream_t st) {
   if (n_max <= 0) return WFPG_OK;
+  if (g.mode == 2) {
+    // power-of-two block area (exact reciprocal) and the upper-layer
+    // directions in constant memory (product_cell)
+    if (g.m < 1 || (g.m & (g.m - 1))) {
+      set_error("shade: product mode needs n / 8 to be a power of two (n = %d)", g.n);
+      return WFPG_ERR_ARG;
+    }
+    WFPG_CUDA(cudaMemcpyToSymbolAsync(c_upper_dirs, g.upper_dirs, sizeof(double) * 192, 0,
+                                      cudaMemcpyDeviceToDevice, st));
+  }
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_max, 256), kNumSMs * 8));
   const size_t smem = s.brute ? sizeof(TriRec) * s.n_tris : 0;
   if (s.brute)
