@@ -173,6 +173,7 @@ __global__ void k_count_to_i64(const int32_t* __restrict__ c, int64_t* __restric
 }
 
 int comm_settle(Comm* c) {
+  NvtxRange nvtx_("wfpg_comm_settle");
   if (!c || !c->pending.active) return WFPG_OK;
   DepositPending& p = c->pending;
   p.active = false;

@@ -906,6 +906,7 @@ extern "C" int wfpg_render_pass(const wfpg_scene* scene, wfpg_svo* svo, const wf
                                 const wfpg_pass_config* cfg, wfpg_paths* paths, double* frame,
                                 wfpg_pass_stats* stats, void* workspace, size_t ws_bytes,
                                 void* stream) {
+  NvtxRange nvtx_("wfpg_render_pass");
   if (!scene || !cam || !cfg || !paths || !frame || !cfg_ok(cfg)) {
     set_error("wfpg_render_pass: bad arguments");
     return WFPG_ERR_ARG;

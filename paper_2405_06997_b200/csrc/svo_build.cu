@@ -463,6 +463,7 @@ extern "C" int wfpg_svo_build_sorted(const void* workspace, int64_t n_fragments,
 extern "C" int wfpg_svo_build_structure(wfpg_svo* svo, const int32_t* frag_coords,
                                         int64_t n_fragments, void* workspace, size_t ws_bytes,
                                         void* stream) {
+  NvtxRange nvtx_("wfpg_svo_build_structure");
   if (!svo || n_fragments <= 0) {
     set_error("cannot build an octree from an empty fragment list");
     return WFPG_ERR_ARG;
@@ -782,6 +783,7 @@ extern "C" int wfpg_svo_build_top_index(wfpg_svo* svo, void* stream) {
 extern "C" int wfpg_svo_build_fill(wfpg_svo* svo, const int32_t* frag_tris,
                                    const double* tri_normals, int64_t n_fragments, uint64_t seed,
                                    void* workspace, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("wfpg_svo_build_fill");
   if (!svo || !svo->codes || !svo->parent || !svo->child_base || !svo->child_mask ||
       !svo->normal || !svo->node_desc) {
     set_error("svo build fill: missing node arrays");
