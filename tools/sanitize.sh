@@ -1,4 +1,6 @@
 #!/bin/bash
+# NOTE: compute-sanitizer is closed on the B200 pool this repo was developed on
+# (runs under it left GPUs needing a reset); kept for other machines.
 # compute-sanitizer over the device path at small sizes (one B200):
 # memcheck (out-of-bounds / misaligned / leaks), racecheck (shared-memory
 # hazards), synccheck (barrier misuse), initcheck (uninitialised global reads)
