@@ -157,15 +157,19 @@ class SvoCache:
 
     # -- device storage -----------------------------------------------------
 
-    def _alloc(self, n):
+    def _alloc(self, n, zero=True):
+        """Node arrays for n nodes; zero=False when the caller writes every
+        array (wfpg_svo_build_fill writes the structure and normals and
+        zeroes the accumulators, means and counters itself)."""
         d = {}
+        make = _dev.zeros if zero else _dev.empty
         for name, (_, ddt, comp) in _ARRAYS.items():
             shape = (n, comp) if comp > 1 else (n,)
-            d[name] = _dev.zeros(shape, ddt)
-        d["node_desc"] = _dev.zeros((n, 2), np.uint32)
+            d[name] = make(shape, ddt)
+        d["node_desc"] = make((n, 2), np.uint32)
         # dense index of the top levels: descents start there with one load
         self.top_level = top_level_for(self.depth)
-        d["top_index"] = _dev.zeros((1 << (3 * self.top_level), 2), np.uint32)
+        d["top_index"] = make((1 << (3 * self.top_level), 2), np.uint32)
         self._d = d
         self._abi = None
 
@@ -414,7 +418,7 @@ def _build(frag_coords, frag_tris, tri_normals, cube_lo, cube_size, resolution, 
     _lib.call("wfpg_svo_build_structure", _lib.C.byref(s), _lib.ptr(frag_coords), f,
               _lib.ptr(ws), ws.numel(), st)
     svo.level_off = np.array([s.level_off[i] for i in range(svo.depth + 2)], dtype=np.int64)
-    svo._alloc(svo.node_count)
+    svo._alloc(svo.node_count, zero=False)
     s = svo.abi()
     _lib.call("wfpg_svo_build_fill", _lib.C.byref(s), _lib.ptr(frag_tris), _lib.ptr(tri_normals),
               f, int(seed) & 0xFFFFFFFFFFFFFFFF, _lib.ptr(ws), ws.numel(), st)
