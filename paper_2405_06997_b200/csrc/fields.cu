@@ -246,8 +246,15 @@ __device__ __forceinline__ void ph_mark(int k) {
 #endif
 
 // PRODUCT: block sums (+ block row sums) for the product sampler; a separate
-// instantiation so the plain kernel carries none of its registers
-template <int N, bool PRODUCT>
+// instantiation so the plain kernel carries none of its registers.
+// TRACE: the scene's nearest-hit path — kTraceBrute (triangle records in
+// shared memory, warp-culled), kTracePacket (warp-cooperative BVH walk over
+// the padded fp32 node boxes), kTraceLane (per-lane fp64 BVH walk, scenes
+// without fp32 boxes) — one instantiation each so every path keeps its
+// register budget.
+enum { kTraceBrute = 0, kTracePacket = 1, kTraceLane = 2 };
+
+template <int N, bool PRODUCT, int TRACE>
 __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks)
     k_fields(SceneView s, SvoView v, const double* __restrict__ origins,
              const double* __restrict__ jitters, int64_t nb_max, const int32_t* __restrict__ nb_dev,
@@ -273,7 +280,7 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
   // once the cone tracing is done), off the critical path.
   auto setup = [&](int64_t bb) {
     const double sx = origins[3 * bb], sy = origins[3 * bb + 1], sz = origins[3 * bb + 2];
-    const int n_tb = s.brute ? 3 * s.n_tris : 0;
+    const int n_tb = TRACE == kTraceBrute ? 3 * s.n_tris : 0;
     for (int k = threadIdx.x; k < 2 * N + n_tb; k += blockDim.x) {
       if (k < 2 * N) {
         const int i = k < N ? k : k - N;
@@ -313,9 +320,12 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
       double rgb[3] = {0.0, 0.0, 0.0};
       double bt;
       int32_t bid;
-      if (s.brute)
+      if (TRACE == kTraceBrute)
         warp_nearest_bin<(N <= WFPG_LANE_TEST_MAX_N)>(tb, s.n_tris, dx, dy, dz, s.ray_eps, &bt,
                                                        &bid);
+      else if (TRACE == kTracePacket)
+        warp_bvh_nearest(s, reinterpret_cast<int2*>(tb) + warp * kWarpBvhStack, ox, oy, oz, dx,
+                         dy, dz, s.ray_eps, &bt, &bid);
       else
         bvh_nearest(s, ox, oy, oz, dx, dy, dz, s.ray_eps, &bt, &bid);
       if (bid >= 0) cone_shade_hit(v, ox, oy, oz, dx, dy, dz, bt, omega, rgb);
@@ -454,28 +464,30 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
   }
 }
 
-template <int N, bool PRODUCT>
+template <int N, bool PRODUCT, int TRACE>
 static int launch_fields_n_(const SceneView& s, const SvoView& v, const double* origins,
                            const double* jitters, int64_t nb_max, const int32_t* nb_dev,
                            const BlurParams& bp, const FieldOut& out, cudaStream_t st) {
   constexpr int T = FieldCfg<N>::kThreads;
   size_t smem = sizeof(double) * (N * FieldCfg<N>::kStride + 3 * N) +
-                (s.brute ? sizeof(TriBin) * s.n_tris : 0);
+                (TRACE == kTraceBrute ? sizeof(TriBin) * s.n_tris
+                 : TRACE == kTracePacket ? sizeof(int2) * kWarpBvhStack * (T / 32)  // warp stacks
+                                         : 0);
   static size_t configured = 0;
   if (smem > configured) {
-    WFPG_CUDA(cudaFuncSetAttribute(k_fields<N, PRODUCT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    WFPG_CUDA(cudaFuncSetAttribute(k_fields<N, PRODUCT, TRACE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
     configured = smem;
   }
   int per_sm = 0;
-  WFPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fields<N, PRODUCT>, T, smem));
+  WFPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fields<N, PRODUCT, TRACE>, T, smem));
   if (per_sm < 1) {
     set_error("fields: kernel does not fit (smem %zu)", smem);
     return WFPG_ERR_ARG;
   }
   int64_t grid = std::min<int64_t>(nb_max, (int64_t)kNumSMs * per_sm);
   if (grid < 1) return WFPG_OK;
-  k_fields<N, PRODUCT><<<(unsigned)grid, T, smem, st>>>(s, v, origins, jitters, nb_max, nb_dev, bp, out);
+  k_fields<N, PRODUCT, TRACE><<<(unsigned)grid, T, smem, st>>>(s, v, origins, jitters, nb_max, nb_dev, bp, out);
   WFPG_CHECK_LAUNCH("k_fields");
   return WFPG_OK;
 }
@@ -484,9 +496,12 @@ template <int N>
 static int launch_fields_n(const SceneView& s, const SvoView& v, const double* origins,
                            const double* jitters, int64_t nb_max, const int32_t* nb_dev,
                            const BlurParams& bp, const FieldOut& out, cudaStream_t st) {
-  return out.block_sums
-             ? launch_fields_n_<N, true>(s, v, origins, jitters, nb_max, nb_dev, bp, out, st)
-             : launch_fields_n_<N, false>(s, v, origins, jitters, nb_max, nb_dev, bp, out, st);
+#define WFPG_FIELDS_(P, T) launch_fields_n_<N, P, T>(s, v, origins, jitters, nb_max, nb_dev, bp, out, st)
+  const bool prod = out.block_sums != nullptr;
+  if (s.brute) return prod ? WFPG_FIELDS_(true, kTraceBrute) : WFPG_FIELDS_(false, kTraceBrute);
+  if (s.bbox32) return prod ? WFPG_FIELDS_(true, kTracePacket) : WFPG_FIELDS_(false, kTracePacket);
+  return prod ? WFPG_FIELDS_(true, kTraceLane) : WFPG_FIELDS_(false, kTraceLane);
+#undef WFPG_FIELDS_
 }
 
 int launch_fields(const SceneView& s, const SvoView& v, const double* origins,

@@ -73,9 +73,13 @@ struct TriRec {
   float blo[3], bhi[3];
 };
 
-// Per-ray fp32 slab setup for the box prefilter.
+// Per-ray fp32 slab setup for the box prefilter: reciprocal direction and
+// origin * reciprocal, so a slab distance (b - o) / d is one FFMA,
+// b * (1/d) - o * (1/d).  Its rounding (a few ulp of o / d) stays far inside
+// the box padding (4e-7 of the largest coordinate), as the subtract-multiply
+// form's did.
 struct RaySlab {
-  float ox, oy, oz, ix, iy, iz;
+  float ix, iy, iz, oix, oiy, oiz;
 };
 
 __device__ __forceinline__ RaySlab make_ray_slab(double ox, double oy, double oz, double dx,
@@ -85,20 +89,21 @@ __device__ __forceinline__ RaySlab make_ray_slab(double ox, double oy, double oz
     if (fabsf(f) < 1e-30f) f = copysignf(1e-30f, f);
     return 1.0f / f;
   };
-  return RaySlab{(float)ox, (float)oy, (float)oz, inv(dx), inv(dy), inv(dz)};
+  const float ix = inv(dx), iy = inv(dy), iz = inv(dz);
+  return RaySlab{ix, iy, iz, (float)ox * ix, (float)oy * iy, (float)oz * iz};
 }
 
 // may the ray meet the (padded) box at a parameter in [lo, hi]?
 __device__ __forceinline__ bool slab_maybe(const RaySlab& r, const float* blo, const float* bhi,
                                            float lo, float hi) {
-  float t0 = (blo[0] - r.ox) * r.ix, t1 = (bhi[0] - r.ox) * r.ix;
+  float t0 = fmaf(blo[0], r.ix, -r.oix), t1 = fmaf(bhi[0], r.ix, -r.oix);
   float tn = fminf(t0, t1), tf = fmaxf(t0, t1);
-  t0 = (blo[1] - r.oy) * r.iy;
-  t1 = (bhi[1] - r.oy) * r.iy;
+  t0 = fmaf(blo[1], r.iy, -r.oiy);
+  t1 = fmaf(bhi[1], r.iy, -r.oiy);
   tn = fmaxf(tn, fminf(t0, t1));
   tf = fminf(tf, fmaxf(t0, t1));
-  t0 = (blo[2] - r.oz) * r.iz;
-  t1 = (bhi[2] - r.oz) * r.iz;
+  t0 = fmaf(blo[2], r.iz, -r.oiz);
+  t1 = fmaf(bhi[2], r.iz, -r.oiz);
   tn = fmaxf(tn, fminf(t0, t1));
   tf = fminf(tf, fmaxf(t0, t1));
   return (tn <= tf) & (tn <= hi) & (tf >= lo);
@@ -197,6 +202,34 @@ __device__ __forceinline__ double tri_hit(const double* v0, const double* e1, co
   return -1.0;
 }
 
+// tri_hit with every early return folded into one acceptance test (the
+// same conditions on the same values: us <= ad follows from us + vs <= ad
+// with vs >= 0 under monotone rounding), so the lanes of a packet stay
+// converged; the division runs on accepting lanes only.
+__device__ __forceinline__ double tri_hit_nb(const double* v0, const double* e1,
+                                             const double* e2, double ox, double oy, double oz,
+                                             double dx, double dy, double dz, double tmin,
+                                             double tmax) {
+  const double e2x = __ldg(e2), e2y = __ldg(e2 + 1), e2z = __ldg(e2 + 2);
+  const double e1x = __ldg(e1), e1y = __ldg(e1 + 1), e1z = __ldg(e1 + 2);
+  const double tx = ox - __ldg(v0), ty = oy - __ldg(v0 + 1), tz = oz - __ldg(v0 + 2);
+  double px = dy * e2z - dz * e2y;
+  double py = dz * e2x - dx * e2z;
+  double pz = dx * e2y - dy * e2x;
+  double det = e1x * px + e1y * py + e1z * pz;
+  double ad = fabs(det);
+  double s = det > 0.0 ? 1.0 : -1.0;
+  double us = (tx * px + ty * py + tz * pz) * s;
+  double qx = ty * e1z - tz * e1y;
+  double qy = tz * e1x - tx * e1z;
+  double qz = tx * e1y - ty * e1x;
+  double vs = (dx * qx + dy * qy + dz * qz) * s;
+  double ts = (e2x * qx + e2y * qy + e2z * qz) * s;
+  const bool ok = (ad > 1e-300) & (us >= 0.0) & (vs >= 0.0) & (us + vs <= ad) &
+                  (ts > tmin * ad) & (ts < tmax * ad);
+  return ok ? ts / ad : -1.0;
+}
+
 __device__ __forceinline__ void slab(const double* lo, const double* hi, double ox, double oy,
                                      double oz, double ix, double iy, double iz, double* tn,
                                      double* tf) {
@@ -219,14 +252,14 @@ __device__ __forceinline__ void slab(const double* lo, const double* hi, double 
 __device__ __forceinline__ void slab32(const float4* box, const RaySlab& r, float* tn,
                                        float* tf) {
   const float4 lo = __ldg(box), hi = __ldg(box + 1);
-  float t0 = (lo.x - r.ox) * r.ix, t1 = (hi.x - r.ox) * r.ix;
+  float t0 = fmaf(lo.x, r.ix, -r.oix), t1 = fmaf(hi.x, r.ix, -r.oix);
   float n = fminf(t0, t1), f = fmaxf(t0, t1);
-  t0 = (lo.y - r.oy) * r.iy;
-  t1 = (hi.y - r.oy) * r.iy;
+  t0 = fmaf(lo.y, r.iy, -r.oiy);
+  t1 = fmaf(hi.y, r.iy, -r.oiy);
   n = fmaxf(n, fminf(t0, t1));
   f = fminf(f, fmaxf(t0, t1));
-  t0 = (lo.z - r.oz) * r.iz;
-  t1 = (hi.z - r.oz) * r.iz;
+  t0 = fmaf(lo.z, r.iz, -r.oiz);
+  t1 = fmaf(hi.z, r.iz, -r.oiz);
   n = fmaxf(n, fminf(t0, t1));
   f = fminf(f, fmaxf(t0, t1));
   *tn = n;
@@ -575,6 +608,105 @@ __device__ __forceinline__ bool brute_occluded(const TriRec* __restrict__ tris, 
       return true;
   }
   return false;
+}
+
+// Warp-cooperative nearest hit over the BVH for the 32 rays of a warp that
+// share one origin (a field tile, `bvh_nearest` of _kernels.pyx:398-445 for
+// each lane).  The warp walks the tree as one packet: node ids, child order
+// and the stack are warp-uniform, the stack (node, lane mask) lives in this
+// warp's slice of shared memory, each lane slab-tests its own ray against the
+// padded fp32 child boxes and the warp descends into a child when any lane
+// reaches it before that lane's current best t.  A lane mask travels with
+// every stack entry (lanes outside a node's padded box cannot hit anything
+// below it) and is re-tested against the updated best t when the entry is
+// popped.  Leaves run the reference's fp64 `tri_hit` per lane.  Every lane
+// ends with the minimum accepted t over all triangles — the value the
+// per-lane walk returns; only which of two triangles at a bit-identical t is
+// reported can differ, and the field tracer uses the hit distance alone.
+// Rays of a field tile span a few degrees, so the packet visits about the
+// nodes one ray visits, without the per-lane divergence of 32 separate walks.
+constexpr int kWarpBvhStack = 64;
+
+__device__ __forceinline__ bool slab32_reach(const float4* box, const RaySlab& r, float lo,
+                                             float hi) {
+  float n, f;
+  slab32(box, r, &n, &f);
+  f *= 1.0f + 1e-6f;
+  return (f >= n) & (n <= hi) & (f >= lo);
+}
+
+__device__ __forceinline__ void warp_bvh_nearest(const SceneView& b, int2* __restrict__ wstack,
+                                                 double ox, double oy, double oz, double dx,
+                                                 double dy, double dz, double tmin,
+                                                 double* best_t, int32_t* best_tri) {
+  const int lane = threadIdx.x & 31;
+  const unsigned me = 1u << lane;
+  const RaySlab rs = make_ray_slab(ox, oy, oz, dx, dy, dz);
+  const float lo = (float)tmin * (1.0f - 1e-6f);
+  double bt = 1e300;
+  float hi = __int_as_float(0x7f800000);  // fp32 bound of bt, rounded up
+  int32_t bid = -1;
+  int sp = 0;
+  int32_t node = 0;
+  unsigned mask = __ballot_sync(0xffffffffu, slab32_reach(b.bbox32, rs, lo, hi));
+  while (mask) {
+    const int32_t cnt = __ldg(&b.bcount[node]);
+    const int32_t c0 = __ldg(&b.bleft[node]);
+    if (cnt > 0) {
+      if (mask & me) {
+        for (int32_t k = c0; k < c0 + cnt; ++k) {
+          const int32_t tri = __ldg(&b.border[k]);
+          const double t = tri_hit_nb(b.v0 + 3 * tri, b.e1 + 3 * tri, b.e2 + 3 * tri, ox, oy, oz,
+                                      dx, dy, dz, tmin, bt);
+          if (t > 0.0) {
+            bt = t;
+            bid = tri;
+          }
+        }
+        hi = bt < 1e300 ? __double2float_ru(bt) * (1.0f + 1e-6f) : hi;
+      }
+      mask = 0;
+    } else {
+      const int32_t c1 = __ldg(&b.bright[node]);
+      float n0, f0, n1, f1;
+      slab32(b.bbox32 + 2 * c0, rs, &n0, &f0);
+      slab32(b.bbox32 + 2 * c1, rs, &n1, &f1);
+      f0 *= 1.0f + 1e-6f;
+      f1 *= 1.0f + 1e-6f;
+      const bool in = (mask & me) != 0;
+      const bool h0 = in & (f0 >= n0) & (n0 <= hi) & (f0 >= lo);
+      const bool h1 = in & (f1 >= n1) & (n1 <= hi) & (f1 >= lo);
+      const unsigned m0 = __ballot_sync(0xffffffffu, h0);
+      const unsigned m1 = __ballot_sync(0xffffffffu, h1);
+      if (m0 && m1) {
+        // nearer child first: the majority vote of the lanes reaching both
+        const unsigned both = m0 & m1;
+        const unsigned pref1 = __ballot_sync(0xffffffffu, h0 & h1 & (n1 < n0));
+        const bool first1 = 2 * __popc(pref1) > __popc(both);
+        if (sp < kWarpBvhStack) {
+          if (lane == 0) wstack[sp] = first1 ? make_int2(c0, (int)m0) : make_int2(c1, (int)m1);
+          ++sp;
+        }
+        node = first1 ? c1 : c0;
+        mask = first1 ? m1 : m0;
+      } else {
+        node = m0 ? c0 : c1;
+        mask = m0 ? m0 : m1;
+      }
+    }
+    while (!mask && sp > 0) {
+      __syncwarp();
+      --sp;
+      const int2 e = wstack[sp];
+      node = e.x;
+      const bool again =
+          ((unsigned)e.y & me) && slab32_reach(b.bbox32 + 2 * node, rs, lo, hi);
+      mask = __ballot_sync(0xffffffffu, again);
+    }
+  }
+  __syncwarp();
+  *best_t = bt;
+  *best_tri = bid;
 }
 
 // ray_nearest (_kernels.pyx:481-489): brute force for small scenes (tris in

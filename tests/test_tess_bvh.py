@@ -103,3 +103,34 @@ def test_device_bvh_paths(G, scene_path):
         assert same.mean() >= floor, (tag, same.mean())
         if tag == "p0":
             assert np.array_equal(tree.weight_a, G["p0_svo_weight_a"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [16, 128])
+def test_device_bvh_fields_match_oracle(G, scene_path, n):
+    """Field generation over the BVH (the warp-cooperative packet walk of the
+    field tracer, geometry.cuh warp_bvh_nearest) against the oracle's per-ray
+    BVH traversal (_kernels.pyx:398-445 restated) on the same SVO state:
+    guiding.py:231-251 with the reference's tolerance bar."""
+    from paper_2405_06997_b200 import guiding, svo
+
+    c = _cfg(G)
+    sc = _scene(scene_path, c)
+    tree = svo.build_from_scene(sc, c["R"], seed=c["svo_seed"])
+    for k in ("sum_a", "sum_b", "weight_a", "weight_b"):
+        setattr(tree, k, G["p0_svo_" + k])
+    tree.propagate_up()
+    osvo = OR.Svo.from_scene(sc, c["R"], c["svo_seed"])
+    osvo.mean_a = np.ascontiguousarray(tree.mean_a)
+    osvo.mean_b = np.ascontiguousarray(tree.mean_b)
+    # origins: surface points seen by the reference's test rays (on walls,
+    # inside the box), jitters from a fixed stream
+    hit = G["isect_tri"] >= 0
+    o = G["isect_o"][hit] + G["isect_t"][hit, None] * G["isect_d"][hit]
+    o = o[:: max(1, len(o) // 24)][:24]
+    jit = np.random.default_rng(7).random((len(o), 2))
+    got = guiding.generate_fields_batch(tree, sc, o, n, jit, blur_sigma=1.0)
+    ref = OR.fields(OR.Scene(sc), osvo, o, jit, n)
+    rel = np.abs(got - ref) / np.maximum(np.abs(ref), 1e-300)
+    assert np.mean(rel < 1e-9) >= 0.99, np.mean(rel < 1e-9)
+    np.testing.assert_allclose(got.sum(axis=(1, 2)), ref.sum(axis=(1, 2)), rtol=1e-3)
