@@ -387,6 +387,8 @@ int wfpg_voxelize_emit(const wfpg_scene* scene, const double* cube_lo, double si
 size_t wfpg_svo_build_workspace_bytes(int64_t n_fragments, int32_t depth);
 int wfpg_svo_build_structure(wfpg_svo* svo, const int32_t* frag_coords, int64_t n_fragments,
                              void* workspace, size_t ws_bytes, void* stream);
+/* frag_tris NULL: one normal per fragment (tri_normals is (F,3), fragment i's
+ * normal at row i — SVOs over surface points / path vertices). */
 int wfpg_svo_build_fill(wfpg_svo* svo, const int32_t* frag_tris, const double* tri_normals,
                         int64_t n_fragments, uint64_t seed,
                         void* workspace, size_t ws_bytes, void* stream);

@@ -97,136 +97,165 @@ int scan_u32(const uint32_t* in, uint32_t* out, int64_t n_max, const int32_t* n_
 }
 
 // ---------------------------------------------------------------------------
-// stable LSD radix sort, 8-bit digits
+// stable LSD radix sort over a few large chunks: per pass, a histogram kernel
+// counts each chunk's digits (one block per chunk), one block per digit scans
+// that digit's chunk counts, and the scatter kernel walks its chunk tile by
+// tile with running digit offsets in shared memory — no look-back and a
+// chunk-count table of radix x chunks entries.  Digits are up to 9 bits
+// (passes = ceil(bits / 9), equal widths), so 36-bit Morton codes sort in 4
+// passes.  Within a tile every warp ranks its 32-item chunks by match_any
+// (stable), the tile is reordered by digit in shared memory and each digit's
+// run is stored by consecutive threads.
 // ---------------------------------------------------------------------------
-constexpr int kSortWarps = 8;
-constexpr int kSortBlock = kSortWarps * 32;
-constexpr int kSortIpt = 8;  // 32-item chunks per warp
-constexpr int kSortTile = kSortBlock * kSortIpt;
+constexpr int kCsWarps = 16;
+constexpr int kCsBlock = kCsWarps * 32;
+constexpr int kCsIpt = 8;                    // 32-item chunks per warp
+constexpr int kCsTile = kCsBlock * kCsIpt;   // 4096 items per tile
+constexpr int kCsMaxBits = 9;
+constexpr int kCsMaxRadix = 1 << kCsMaxBits;
+constexpr int kCsChunks = kNumSMs * 2;       // scatter blocks resident at once
 
-template <typename KT>
-__global__ void __launch_bounds__(kSortBlock) k_sort_hist(const KT* __restrict__ keys,
-                                                          int64_t n_max,
-                                                          const int32_t* __restrict__ n_dev,
-                                                          int shift, int64_t nblocks,
-                                                          uint32_t* __restrict__ hist) {
-  __shared__ uint32_t cnt[256];
-  const int64_t n = dev_count(n_max, n_dev);
-  cnt[threadIdx.x] = 0;
-  __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * kSortTile;
-  for (int k = 0; k < kSortIpt; ++k) {
-    int64_t i = base + (int64_t)k * kSortBlock + threadIdx.x;
-    if (i < n) atomicAdd(&cnt[(keys[i] >> shift) & 255u], 1u);
-  }
-  __syncthreads();
-  // digit-major (stride = worst-case tile count): each digit's tile counts
-  // are contiguous for the per-digit scan
-  if (base < n) hist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = cnt[threadIdx.x];
+struct CsPlan {
+  int passes, bits;
+};
+static CsPlan cs_plan(int key_bits) {
+  CsPlan p;
+  p.passes = (key_bits + kCsMaxBits - 1) / kCsMaxBits;
+  if (p.passes < 1) p.passes = 1;
+  p.bits = (key_bits + p.passes - 1) / p.passes;
+  return p;
 }
 
-// Digit offsets: one block per digit scans that digit's counts over the
-// active tiles (ceil(n / tile), n from the device) in place and writes the
-// digit total; the scatter blocks turn the 256 totals into digit bases.
-constexpr int kOffThreads = 256;
-__global__ void __launch_bounds__(kOffThreads) k_sort_offsets(uint32_t* __restrict__ hist,
-                                                              int64_t n_max,
-                                                              const int32_t* __restrict__ n_dev,
-                                                              int64_t nblocks,
-                                                              uint32_t* __restrict__ dtot) {
-  __shared__ uint32_t sw[kOffThreads / 32 + 1];
+// chunk c covers [c * len, (c + 1) * len) of the live count, len a tile multiple
+__device__ __forceinline__ int64_t cs_chunk_len(int64_t n) {
+  const int64_t tiles = (n + kCsTile - 1) / kCsTile;
+  return ((tiles + kCsChunks - 1) / kCsChunks) * kCsTile;
+}
+
+template <typename KT>
+__global__ void __launch_bounds__(256) k_cs_hist(const KT* __restrict__ keys, int64_t n_max,
+                                                 const int32_t* __restrict__ n_dev, int shift,
+                                                 int bits, uint32_t* __restrict__ counts) {
+  __shared__ uint32_t h[kCsMaxRadix];
+  const int radix = 1 << bits;
+  const uint32_t dm = (uint32_t)radix - 1u;
+  for (int i = threadIdx.x; i < radix; i += blockDim.x) h[i] = 0;
+  __syncthreads();
   const int64_t n = dev_count(n_max, n_dev);
-  const int64_t nb = (n + kSortTile - 1) / kSortTile;
-  uint32_t* h = hist + (int64_t)blockIdx.x * nblocks;
-  const int64_t per = (nb + kOffThreads - 1) / kOffThreads;
-  const int64_t b0 = (int64_t)threadIdx.x * per, b1 = b0 + per < nb ? b0 + per : nb;
-  uint32_t s = 0;
-  for (int64_t b = b0; b < b1; ++b) s += h[b];
+  const int64_t len = cs_chunk_len(n);
+  const int64_t b0 = (int64_t)blockIdx.x * len;
+  const int64_t b1 = b0 + len < n ? b0 + len : n;
+  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x)
+    atomicAdd(&h[(uint32_t)((keys[i] >> shift) & dm)], 1u);
+  __syncthreads();
+  for (int d = threadIdx.x; d < radix; d += blockDim.x)
+    counts[(int64_t)d * kCsChunks + blockIdx.x] = h[d];
+}
+
+// one block per digit: exclusive scan of the digit's chunk counts in place,
+// digit total to dtot
+constexpr int kCsOffThreads = ((kCsChunks + 31) / 32) * 32;
+__global__ void __launch_bounds__(kCsOffThreads) k_cs_offsets(uint32_t* __restrict__ counts,
+                                                              uint32_t* __restrict__ dtot) {
+  __shared__ uint32_t sw[kCsOffThreads / 32 + 1];
+  uint32_t* c = counts + (int64_t)blockIdx.x * kCsChunks;
+  const bool in = threadIdx.x < kCsChunks;
+  const uint32_t v = in ? c[threadIdx.x] : 0u;
   uint32_t total;
-  uint32_t run = block_exclusive_scan<kOffThreads>(s, sw, &total);
-  for (int64_t b = b0; b < b1; ++b) {
-    const uint32_t c = h[b];
-    h[b] = run;
-    run += c;
-  }
+  const uint32_t ex = block_exclusive_scan<kCsOffThreads>(v, sw, &total);
+  if (in) c[threadIdx.x] = ex;
   if (threadIdx.x == 0) dtot[blockIdx.x] = total;
 }
 
 template <typename KT>
-__global__ void __launch_bounds__(kSortBlock) k_sort_scatter(
+__global__ void __launch_bounds__(kCsBlock) k_cs_scatter(
     const KT* __restrict__ kin, const uint32_t* __restrict__ vin, KT* __restrict__ kout,
     uint32_t* __restrict__ vout, int64_t n_max, const int32_t* __restrict__ n_dev, int shift,
-    int64_t nblocks, const uint32_t* __restrict__ offs, const uint32_t* __restrict__ dbase) {
-  __shared__ uint32_t whist[kSortWarps][256];
-  __shared__ uint32_t goff[256];
-  __shared__ uint32_t dstart[256];
-  __shared__ uint32_t sw[kSortBlock / 32 + 1];
-  __shared__ KT sk[kSortTile];
-  __shared__ uint32_t sv[kSortTile];
+    int bits, const uint32_t* __restrict__ counts, const uint32_t* __restrict__ dtot) {
+  extern __shared__ __align__(16) unsigned char cs_smem[];
+  const int radix = 1 << bits;
+  const uint32_t dm = (uint32_t)radix - 1u;
+  KT* sk = reinterpret_cast<KT*>(cs_smem);
+  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + kCsTile);
+  uint32_t* whist = sv + kCsTile;              // [kCsWarps][radix]
+  uint32_t* run = whist + kCsWarps * radix;    // [radix] running global offsets
+  uint32_t* goff = run + radix;                // [radix]
+  uint32_t* dstart = goff + radix;             // [radix]
+  __shared__ uint32_t sw[kCsBlock / 32 + 1];
   const int64_t n = dev_count(n_max, n_dev);
-  if ((int64_t)blockIdx.x * kSortTile >= n) return;
+  const int64_t len = cs_chunk_len(n);
+  const int64_t c0 = (int64_t)blockIdx.x * len;
+  if (c0 >= n) return;
+  const int64_t c1 = c0 + len < n ? c0 + len : n;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < kSortWarps * 256; i += kSortBlock) (&whist[0][0])[i] = 0;
-  // digit base = exclusive prefix of the digit totals (thread t = digit t)
-  const uint32_t base_t = block_exclusive_scan<kSortBlock>(dbase[threadIdx.x], sw, nullptr);
-  goff[threadIdx.x] = base_t + offs[(int64_t)threadIdx.x * nblocks + blockIdx.x];
-  __syncthreads();
-
-  const int64_t wbase = (int64_t)blockIdx.x * kSortTile + (int64_t)warp * 32 * kSortIpt;
-  KT k[kSortIpt];
-  uint32_t v[kSortIpt];
-  uint32_t r[kSortIpt];
+  const int d = threadIdx.x;
+  {
+    // digit bases (exclusive scan of the digit totals) + this chunk's offset
+    const uint32_t t = d < radix ? dtot[d] : 0u;
+    const uint32_t base = block_exclusive_scan<kCsBlock>(t, sw, nullptr);
+    if (d < radix) run[d] = base + counts[(int64_t)d * kCsChunks + blockIdx.x];
+  }
   const uint32_t lt = lanemask_lt();
+  uint32_t* wh = whist + warp * radix;
+  for (int64_t tbase = c0; tbase < c1; tbase += kCsTile) {
+    for (int i = threadIdx.x; i < kCsWarps * radix; i += kCsBlock) whist[i] = 0;
+    __syncthreads();
+    const int64_t wbase = tbase + (int64_t)warp * 32 * kCsIpt;
+    KT k[kCsIpt];
+    uint32_t v[kCsIpt];
+    uint32_t r[kCsIpt];
 #pragma unroll
-  for (int c = 0; c < kSortIpt; ++c) {
-    int64_t i = wbase + c * 32 + lane;
-    bool valid = i < n;
-    k[c] = valid ? kin[i] : 0;
-    v[c] = valid ? vin[i] : 0;
-    uint32_t dig = valid ? (uint32_t)((k[c] >> shift) & 255u) : 256u + lane;
-    uint32_t vmask = __ballot_sync(0xffffffffu, valid);
-    uint32_t peers = __match_any_sync(0xffffffffu, dig) & vmask;
-    uint32_t pre = valid ? whist[warp][dig & 255u] : 0;
-    __syncwarp();
-    if (valid && (peers & lt) == 0) whist[warp][dig] = pre + __popc(peers);
-    __syncwarp();
-    r[c] = pre + __popc(peers & lt);
-  }
-  __syncthreads();
-  // per digit (thread t = digit t): warp-exclusive offsets within the digit,
-  // then the block-local start of each digit
-  uint32_t run = 0;
-  for (int w = 0; w < kSortWarps; ++w) {
-    uint32_t t = whist[w][threadIdx.x];
-    whist[w][threadIdx.x] = run;
-    run += t;
-  }
-  __syncthreads();  // sw is reused by the scan below
-  const uint32_t lstart = block_exclusive_scan<kSortBlock>(run, sw, nullptr);
-  dstart[threadIdx.x] = lstart;
-  goff[threadIdx.x] -= lstart;  // global position = goff[d] + block-local position
-  __syncthreads();
-  // reorder the tile in shared memory by digit (stable), then write each
-  // digit's run with consecutive threads: coalesced stores instead of 256-way
-  // scattered ones
-#pragma unroll
-  for (int c = 0; c < kSortIpt; ++c) {
-    int64_t i = wbase + c * 32 + lane;
-    if (i < n) {
-      uint32_t dig = (uint32_t)((k[c] >> shift) & 255u);
-      uint32_t lp = dstart[dig] + whist[warp][dig] + r[c];
-      sk[lp] = k[c];
-      sv[lp] = v[c];
+    for (int c = 0; c < kCsIpt; ++c) {
+      const int64_t i = wbase + c * 32 + lane;
+      const bool valid = i < c1;
+      k[c] = valid ? kin[i] : (KT)0;
+      v[c] = valid ? vin[i] : 0u;
+      const uint32_t dig = valid ? (uint32_t)((k[c] >> shift) & dm) : (uint32_t)radix + lane;
+      const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+      const uint32_t peers = __match_any_sync(0xffffffffu, dig) & vmask;
+      const uint32_t pre = valid ? wh[dig] : 0u;
+      __syncwarp();
+      if (valid && (peers & lt) == 0) wh[dig] = pre + __popc(peers);
+      __syncwarp();
+      r[c] = pre + __popc(peers & lt);
     }
-  }
-  __syncthreads();
-  const int64_t tbase = (int64_t)blockIdx.x * kSortTile;
-  const int valid = (int)(n - tbase < kSortTile ? n - tbase : kSortTile);
-  for (int e = threadIdx.x; e < valid; e += kSortBlock) {
-    const KT key = sk[e];
-    const uint32_t pos = goff[(uint32_t)((key >> shift) & 255u)] + (uint32_t)e;
-    kout[pos] = key;
-    vout[pos] = sv[e];
+    __syncthreads();
+    // thread d = digit d: warp-exclusive offsets within the digit, the tile's
+    // digit count, the tile-local digit starts
+    uint32_t cnt = 0;
+    if (d < radix) {
+      for (int w = 0; w < kCsWarps; ++w) {
+        const uint32_t t = whist[w * radix + d];
+        whist[w * radix + d] = cnt;
+        cnt += t;
+      }
+    }
+    const uint32_t lstart = block_exclusive_scan<kCsBlock>(cnt, sw, nullptr);
+    if (d < radix) {
+      dstart[d] = lstart;
+      goff[d] = run[d] - lstart;  // global position = goff + tile position
+      run[d] += cnt;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < kCsIpt; ++c) {
+      const int64_t i = wbase + c * 32 + lane;
+      if (i < c1) {
+        const uint32_t dig = (uint32_t)((k[c] >> shift) & dm);
+        const uint32_t lp = dstart[dig] + wh[dig] + r[c];
+        sk[lp] = k[c];
+        sv[lp] = v[c];
+      }
+    }
+    __syncthreads();
+    const int valid = (int)(c1 - tbase < kCsTile ? c1 - tbase : kCsTile);
+    for (int e = threadIdx.x; e < valid; e += kCsBlock) {
+      const KT key = sk[e];
+      const uint32_t pos = goff[(uint32_t)((key >> shift) & dm)] + (uint32_t)e;
+      kout[pos] = key;
+      vout[pos] = sv[e];
+    }
+    __syncthreads();  // sk / sv / whist are reused by the next tile
   }
 }
 
@@ -242,40 +271,63 @@ __global__ void k_copy_pairs(const KT* __restrict__ ks, const uint32_t* __restri
   }
 }
 
+template <typename KT>
+static size_t cs_smem_bytes(int bits) {
+  const int radix = 1 << bits;
+  return sizeof(KT) * kCsTile + sizeof(uint32_t) * kCsTile +
+         sizeof(uint32_t) * (size_t)(kCsWarps + 3) * radix;
+}
+
 size_t sort_ws_bytes(int64_t n_max) {
   int64_t n = n_max > 0 ? n_max : 1;
-  int64_t nb = ceil_div(n, kSortTile);
   return align_up(sizeof(uint64_t) * n) + align_up(sizeof(uint32_t) * n) +
-         align_up(sizeof(uint32_t) * 256 * nb) + align_up(sizeof(uint32_t) * 256) + 1024;
+         align_up(sizeof(uint32_t) * (size_t)kCsMaxRadix * kCsChunks) +
+         align_up(sizeof(uint32_t) * kCsMaxRadix) + 1024;
 }
 
 template <typename KT>
 static int sort_pairs_t(KT* keys, uint32_t* vals, int64_t n_max, const int32_t* n_dev, int key_bits,
                         Arena& ws, cudaStream_t st) {
   if (n_max <= 1) return WFPG_OK;
-  int64_t nb = ceil_div(n_max, kSortTile);
+  if (n_max >= (int64_t)UINT32_MAX) {
+    set_error("sort: %lld items exceed the 32-bit index range", (long long)n_max);
+    return WFPG_ERR_CAPACITY;
+  }
+  const CsPlan plan = cs_plan(key_bits);
+  const int radix = 1 << plan.bits;
   KT* k2 = ws.take<KT>(n_max);
   uint32_t* v2 = ws.take<uint32_t>(n_max);
-  uint32_t* hist = ws.take<uint32_t>(256 * nb);
-  uint32_t* dbase = ws.take<uint32_t>(256);
+  uint32_t* counts = ws.take<uint32_t>((int64_t)kCsMaxRadix * kCsChunks);
+  uint32_t* dtot = ws.take<uint32_t>(kCsMaxRadix);
   if (!ws.ok()) {
     set_error("sort: workspace too small");
     return WFPG_ERR_WORKSPACE;
   }
-  int passes = (key_bits + 7) / 8;
+  const size_t smem = cs_smem_bytes<KT>(plan.bits);
+  static bool configured = false;
+  if (!configured) {
+    WFPG_CUDA(cudaFuncSetAttribute(k_cs_scatter<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)cs_smem_bytes<KT>(kCsMaxBits)));
+    configured = true;
+  }
+  // fewer chunks than kCsChunks are live when n is small; the others return
+  const unsigned grid = (unsigned)std::min<int64_t>(kCsChunks, ceil_div(n_max, kCsTile));
   KT* ka = keys;
   uint32_t* va = vals;
   KT* kb = k2;
   uint32_t* vb = v2;
-  for (int p = 0; p < passes; ++p) {
-    int shift = 8 * p;
-    k_sort_hist<KT><<<(unsigned)nb, kSortBlock, 0, st>>>(ka, n_max, n_dev, shift, nb, hist);
-    WFPG_CHECK_LAUNCH("k_sort_hist");
-    k_sort_offsets<<<256, kOffThreads, 0, st>>>(hist, n_max, n_dev, nb, dbase);
-    WFPG_CHECK_LAUNCH("k_sort_offsets");
-    k_sort_scatter<KT><<<(unsigned)nb, kSortBlock, 0, st>>>(ka, va, kb, vb, n_max, n_dev, shift, nb,
-                                                         hist, dbase);
-    WFPG_CHECK_LAUNCH("k_sort_scatter");
+  for (int p = 0; p < plan.passes; ++p) {
+    const int shift = p * plan.bits;
+    // chunks past the live count must read as zero counts
+    if (grid < (unsigned)kCsChunks || n_dev)
+      WFPG_CUDA(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * (size_t)radix * kCsChunks, st));
+    k_cs_hist<KT><<<grid, 256, 0, st>>>(ka, n_max, n_dev, shift, plan.bits, counts);
+    WFPG_CHECK_LAUNCH("k_cs_hist");
+    k_cs_offsets<<<radix, kCsOffThreads, 0, st>>>(counts, dtot);
+    WFPG_CHECK_LAUNCH("k_cs_offsets");
+    k_cs_scatter<KT><<<grid, kCsBlock, smem, st>>>(ka, va, kb, vb, n_max, n_dev, shift,
+                                                   plan.bits, counts, dtot);
+    WFPG_CHECK_LAUNCH("k_cs_scatter");
     KT* tk = ka;
     ka = kb;
     kb = tk;
@@ -285,8 +337,8 @@ static int sort_pairs_t(KT* keys, uint32_t* vals, int64_t n_max, const int32_t* 
   }
   if (ka != keys) {
     // odd number of passes: copy the live prefix back
-    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_max, 256), kNumSMs * 8));
-    k_copy_pairs<KT><<<grid, 256, 0, st>>>(ka, va, keys, vals, n_max, n_dev);
+    int cgrid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_max, 256), kNumSMs * 8));
+    k_copy_pairs<KT><<<cgrid, 256, 0, st>>>(ka, va, keys, vals, n_max, n_dev);
     WFPG_CHECK_LAUNCH("k_copy_pairs");
   }
   return WFPG_OK;

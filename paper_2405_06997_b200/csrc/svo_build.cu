@@ -312,42 +312,42 @@ extern "C" int wfpg_voxelize_emit(const wfpg_scene* sc, const double* cube_lo, d
 // ---------------------------------------------------------------------------
 namespace wfpg {
 
+// Levels from the sorted fragment codes in two streaming passes (svo.py:
+// 416-500: np.unique per level, parents by searchsorted, children wired).
+// A node of level l is a distinct value of code >> 3 (depth - l); sorted
+// fragment i starts a new node at every level l >= lv(i), the coarsest
+// level at which its code differs from fragment i-1's (from the highest
+// differing bit; depth + 1 for a repeated code, 0 for i = 0).  So the node
+// index of fragment i at level l is (#{j <= i : lv(j) <= l}) - 1: pass 1
+// counts lv <= l per tile and level, a scan gives every tile's level
+// offsets, and pass 2 recomputes the in-tile ranks (ballots) and writes
+// every node once from the fragment that starts it — code, parent, first
+// child and a bit in the parent's child mask.  Same arrays as the level-by-
+// level build (levels in code order, root first).
+constexpr int kLvBlock = 256;
+constexpr int kLvWarps = kLvBlock / 32;
+constexpr int kLvChunks = 16;                       // 32-fragment chunks per warp
+constexpr int kLvTile = kLvBlock * kLvChunks;       // 4096 fragments per tile
+constexpr int kLvMaxLevels = 22;                    // depth <= 21
+
 struct BuildWs {
-  uint64_t* codes;    // (F,) sorted fragment codes
-  uint32_t* perm;     // (F,) stable sort permutation
-  uint32_t* flags;    // (F,)
-  uint32_t* scan;     // (F,)
-  uint64_t* lvl_codes;  // packed level codes, bottom-up, capacity cap_nodes
-  uint32_t* lvl_owner;  // owner (parent index within level) per entry
-  uint32_t* lvl_first;  // index of the first entry of each parent run ... (unused slot)
-  uint32_t* leaf_start; // (L+1,)
-  uint32_t* counts;     // (depth+1,) device level counts
-  int64_t* bases;       // (depth+2,) device offsets of the levels in lvl_codes
-  int64_t cap_nodes;
+  uint64_t* codes;       // (F,) sorted fragment codes
+  uint32_t* perm;        // (F,) stable sort permutation
+  uint32_t* tile_cnt;    // (depth+1, tiles) level-major counts, then offsets
+  uint32_t* counts;      // (depth+1,) level sizes
+  uint32_t* leaf_start;  // (L+1,) first sorted fragment of each leaf
+  double* sorted_n;      // (F,3) fragment normals in sorted-fragment order (phase B)
+  int64_t tiles;
 };
 
-static int64_t node_capacity(int64_t F, int depth) {
-  int64_t cap = F;
-  for (int l = 0; l < depth; ++l) {
-    int64_t full = (l < 21) ? ((int64_t)1 << (3 * l)) : INT64_MAX;
-    cap += std::min(F, full);
-  }
-  return cap;
-}
-
 static void carve(Arena& a, int64_t F, int depth, BuildWs& w) {
-  int64_t cap = node_capacity(F, depth);
   w.codes = a.take<uint64_t>(F);
   w.perm = a.take<uint32_t>(F);
-  w.flags = a.take<uint32_t>(F + 1);
-  w.scan = a.take<uint32_t>(F + 1);
-  w.lvl_codes = a.take<uint64_t>(cap);
-  w.lvl_owner = a.take<uint32_t>(cap);
-  w.lvl_first = a.take<uint32_t>(1);
-  w.leaf_start = a.take<uint32_t>(F + 1);
+  w.tiles = ceil_div(F > 0 ? F : 1, kLvTile);
+  w.tile_cnt = a.take<uint32_t>((int64_t)(depth + 1) * w.tiles);
   w.counts = a.take<uint32_t>(depth + 2);
-  w.bases = a.take<int64_t>(depth + 2);
-  w.cap_nodes = cap;
+  w.leaf_start = a.take<uint32_t>(F + 1);
+  w.sorted_n = a.take<double>(3 * F);
 }
 
 __global__ void k_frag_codes(const int32_t* __restrict__ coords, int64_t F,
@@ -360,84 +360,125 @@ __global__ void k_frag_codes(const int32_t* __restrict__ coords, int64_t F,
   }
 }
 
-// flags[i] = first of a run of equal (codes[i] >> shift)
-__global__ void k_run_flags(const uint64_t* __restrict__ codes, int64_t n_max,
-                            const uint32_t* __restrict__ n_dev, int shift,
-                            uint32_t* __restrict__ flags) {
-  int64_t n = n_dev ? (int64_t)*n_dev : n_max;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    flags[i] = (i == 0 || (codes[i] >> shift) != (codes[i - 1] >> shift)) ? 1u : 0u;
-  }
+// coarsest level at which fragment i starts a node
+__device__ __forceinline__ int start_level(const uint64_t* __restrict__ codes, int64_t i,
+                                           int depth) {
+  if (i == 0) return 0;
+  const uint64_t x = codes[i] ^ codes[i - 1];
+  if (x == 0) return depth + 1;
+  const int hb = 63 - __clzll((long long)x);
+  const int l = depth - hb / 3;
+  return l < 1 ? 1 : l;
 }
 
-// leaf level: unique codes + run starts (np.unique(return_index=True))
-__global__ void k_leaf_unique(const uint64_t* __restrict__ codes, int64_t F,
-                              const uint32_t* __restrict__ flags, const uint32_t* __restrict__ scan,
-                              uint64_t* __restrict__ leaf_codes, uint32_t* __restrict__ leaf_start,
-                              const uint32_t* __restrict__ n_leaves) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < F;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    if (flags[i]) {
-      leaf_codes[scan[i]] = codes[i];
-      leaf_start[scan[i]] = (uint32_t)i;
+// pass 1: per tile and level, the number of fragments with lv <= level
+__global__ void __launch_bounds__(kLvBlock) k_lv_count(const uint64_t* __restrict__ codes,
+                                                       int64_t F, int depth, int64_t tiles,
+                                                       uint32_t* __restrict__ tile_cnt) {
+  __shared__ uint32_t wc[kLvWarps][kLvMaxLevels];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t t0 = (int64_t)blockIdx.x * kLvTile;
+  uint32_t mine = 0;  // lane l: this warp's count for level l
+  for (int c = 0; c < kLvChunks; ++c) {
+    const int64_t i = t0 + ((int64_t)warp * kLvChunks + c) * 32 + lane;
+    const int lv = i < F ? start_level(codes, i, depth) : depth + 1;
+    for (int l = 0; l <= depth; ++l) {
+      const uint32_t b = __ballot_sync(0xffffffffu, lv <= l);
+      if (lane == l) mine += __popc(b);
     }
-    if (i == 0) leaf_start[*n_leaves] = (uint32_t)F;
+  }
+  if (lane <= depth) wc[warp][lane] = mine;
+  __syncthreads();
+  if (threadIdx.x <= depth) {
+    uint32_t s = 0;
+    for (int w = 0; w < kLvWarps; ++w) s += wc[w][threadIdx.x];
+    tile_cnt[(int64_t)threadIdx.x * tiles + blockIdx.x] = s;
   }
 }
 
-// parent level from a child level: owner[k] = index of (child>>3) in the
-// parent level (np.searchsorted on the unique parents, svo.py:463)
-__global__ void k_parent_level(const uint64_t* __restrict__ child, const uint32_t* __restrict__ n_c,
-                               const uint32_t* __restrict__ flags,
-                               const uint32_t* __restrict__ scan, uint32_t* __restrict__ owner,
-                               uint64_t* __restrict__ parent_codes) {
-  int64_t n = *n_c;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    // exclusive scan of run-start flags: owner = inclusive - 1
-    uint32_t o = scan[k] + flags[k] - 1u;
-    owner[k] = o;
-    if (flags[k]) parent_codes[o] = child[k] >> 3;
+// one block per level: exclusive scan of the level's tile counts in place,
+// level size to counts[level]
+__global__ void __launch_bounds__(1024) k_lv_offsets(uint32_t* __restrict__ tile_cnt,
+                                                     int64_t tiles,
+                                                     uint32_t* __restrict__ counts) {
+  __shared__ uint32_t sw[1024 / 32 + 1];
+  uint32_t* c = tile_cnt + (int64_t)blockIdx.x * tiles;
+  const int64_t per = (tiles + 1023) / 1024;
+  const int64_t b0 = (int64_t)threadIdx.x * per, b1 = b0 + per < tiles ? b0 + per : tiles;
+  uint32_t s = 0;
+  for (int64_t b = b0; b < b1; ++b) s += c[b];
+  uint32_t total;
+  uint32_t run = block_exclusive_scan<1024>(s, sw, &total);
+  for (int64_t b = b0; b < b1; ++b) {
+    const uint32_t v = c[b];
+    c[b] = run;
+    run += v;
   }
+  if (threadIdx.x == 0) counts[blockIdx.x] = total;
 }
 
-// Device-resident level bookkeeping of the structure phase: the levels are
-// packed bottom-up in lvl_codes, level l at bases[l] = bases[l+1] +
-// counts[l+1]; every per-level kernel reads its size and offsets from device
-// memory, so building the levels needs no host round trip (the capacity
-// node_capacity() bounds every level: count_l <= min(F, 8^l)).
-__global__ void k_level_base(const uint32_t* __restrict__ counts, int64_t* __restrict__ bases,
-                             int l) {
-  bases[l] = bases[l + 1] + (int64_t)counts[l + 1];
-}
+__global__ void k_set_u32(uint32_t* p, uint32_t v) { *p = v; }
 
-__global__ void k_run_flags_lvl(const uint64_t* __restrict__ lvl_codes,
-                                const int64_t* __restrict__ bases,
-                                const uint32_t* __restrict__ counts, int lvl, int shift,
-                                uint32_t* __restrict__ flags) {
-  const int64_t n = counts[lvl];
-  const uint64_t* codes = lvl_codes + bases[lvl];
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    flags[i] = (i == 0 || (codes[i] >> shift) != (codes[i - 1] >> shift)) ? 1u : 0u;
-}
+// pass 2: write every node from the fragment that starts it (internal
+// nodes' child masks are set by k_internal_normals from their children).
+struct LevelOffs {
+  int64_t off[kLvMaxLevels + 1];
+};
 
-__global__ void k_parent_level_lvl(uint64_t* __restrict__ lvl_codes,
-                                   uint32_t* __restrict__ lvl_owner,
-                                   const int64_t* __restrict__ bases,
-                                   const uint32_t* __restrict__ counts, int lvl,
-                                   const uint32_t* __restrict__ flags,
-                                   const uint32_t* __restrict__ scan) {
-  const int64_t n = counts[lvl];
-  const uint64_t* child = lvl_codes + bases[lvl];
-  uint32_t* owner = lvl_owner + bases[lvl];
-  uint64_t* parent_codes = lvl_codes + bases[lvl - 1];
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t o = scan[k] + flags[k] - 1u;  // inclusive scan - 1
-    owner[k] = o;
-    if (flags[k]) parent_codes[o] = child[k] >> 3;
+__global__ void __launch_bounds__(kLvBlock) k_lv_emit(
+    const uint64_t* __restrict__ codes, int64_t F, int depth, int64_t tiles,
+    const uint32_t* __restrict__ tile_off, LevelOffs lo, uint64_t* __restrict__ ncodes,
+    int32_t* __restrict__ parent, int32_t* __restrict__ child_base,
+    uint8_t* __restrict__ child_mask, uint32_t* __restrict__ leaf_start) {
+  __shared__ uint32_t wc[kLvWarps][kLvMaxLevels];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t t0 = (int64_t)blockIdx.x * kLvTile;
+  // warp counts per level, then each warp's exclusive offset within the tile
+  uint32_t mine = 0;
+  for (int c = 0; c < kLvChunks; ++c) {
+    const int64_t i = t0 + ((int64_t)warp * kLvChunks + c) * 32 + lane;
+    const int lv = i < F ? start_level(codes, i, depth) : depth + 1;
+    for (int l = 0; l <= depth; ++l) {
+      const uint32_t b = __ballot_sync(0xffffffffu, lv <= l);
+      if (lane == l) mine += __popc(b);
+    }
+  }
+  if (lane <= depth) wc[warp][lane] = mine;
+  __syncthreads();
+  // lane l: running count (fragments before this chunk with lv <= l), i.e.
+  // tile offset + earlier warps of the tile
+  uint32_t run = 0;
+  if (lane <= depth) {
+    run = tile_off[(int64_t)lane * tiles + blockIdx.x];
+    for (int w = 0; w < warp; ++w) run += wc[w][lane];
+  }
+  const uint32_t le = lanemask_lt() | (1u << lane);
+  for (int c = 0; c < kLvChunks; ++c) {
+    const int64_t i = t0 + ((int64_t)warp * kLvChunks + c) * 32 + lane;
+    const bool valid = i < F;
+    const int lv = valid ? start_level(codes, i, depth) : depth + 1;
+    const uint64_t code = valid ? codes[i] : 0;
+    // inclusive rank of fragment i at level l: run_l + popc(ballot_l & le)
+    uint32_t prev_rank = 0;  // rank at level l - 1
+    for (int l = 0; l <= depth; ++l) {
+      const uint32_t b = __ballot_sync(0xffffffffu, lv <= l);
+      const uint32_t rank = __shfl_sync(0xffffffffu, run, l) + __popc(b & le);
+      if (lane == l) run += __popc(b);
+      if (valid && lv <= l) {
+        const int64_t node = lo.off[l] + rank - 1;
+        const uint64_t key = code >> (3 * (depth - l));
+        ncodes[node] = key;
+        parent[node] = l == 0 ? -1 : (int32_t)(lo.off[l - 1] + prev_rank - 1);
+        if (l == depth) {
+          child_base[node] = -1;
+          child_mask[node] = 0;
+          leaf_start[rank - 1] = (uint32_t)i;
+        }
+        // a node's first child is started by the same fragment
+        if (l > 0 && lv <= l - 1) child_base[lo.off[l - 1] + prev_rank - 1] = (int32_t)node;
+      }
+      prev_rank = rank;
+    }
   }
 }
 
@@ -447,7 +488,7 @@ extern "C" size_t wfpg_svo_build_workspace_bytes(int64_t n_fragments, int32_t de
   Arena a(nullptr, 0);
   BuildWs w;
   carve(a, n_fragments, depth, w);
-  return a.off + std::max(sort_ws_bytes(n_fragments), scan_ws_bytes(n_fragments + 1)) + 4096;
+  return a.off + sort_ws_bytes(n_fragments) + 4096;
 }
 
 extern "C" int wfpg_svo_build_sorted(const void* workspace, int64_t n_fragments,
@@ -473,6 +514,10 @@ extern "C" int wfpg_svo_build_structure(wfpg_svo* svo, const int32_t* frag_coord
     return WFPG_ERR_CAPACITY;
   }
   const int depth = svo->depth;
+  if (depth < 0 || depth >= kLvMaxLevels) {
+    set_error("svo build: depth %d outside [0, %d]", depth, kLvMaxLevels - 1);
+    return WFPG_ERR_ARG;
+  }
   cudaStream_t st = as_stream(stream);
   Arena a(workspace, ws_bytes);
   BuildWs w;
@@ -490,37 +535,10 @@ extern "C" int wfpg_svo_build_structure(wfpg_svo* svo, const int32_t* frag_coord
     WFPG_TRY(sort_pairs(w.codes, w.perm, F, nullptr, std::max(1, 3 * depth), a, st));
     a.off = mark;
   }
-  // leaves
-  k_run_flags<<<grid, 256, 0, st>>>(w.codes, F, nullptr, 0, w.flags);
-  WFPG_CHECK_LAUNCH("k_run_flags");
-  uint32_t* cnt_leaf = w.counts + depth;
-  {
-    size_t mark = a.off;
-    WFPG_TRY(scan_u32(w.flags, w.scan, F, nullptr, cnt_leaf, a, st));
-    a.off = mark;
-  }
-  // level buffers are packed bottom-up: leaves at offset 0; sizes and
-  // offsets stay on the device until the single read-back below
-  WFPG_CUDA(cudaMemsetAsync(w.bases, 0, sizeof(int64_t) * (depth + 2), st));
-  k_leaf_unique<<<grid, 256, 0, st>>>(w.codes, F, w.flags, w.scan, w.lvl_codes, w.leaf_start,
-                                      cnt_leaf);
-  WFPG_CHECK_LAUNCH("k_leaf_unique");
-  for (int l = depth - 1; l >= 0; --l) {
-    k_level_base<<<1, 1, 0, st>>>(w.counts, w.bases, l);
-    WFPG_CHECK_LAUNCH("k_level_base");
-    // level l + 1 holds at most min(F, 8^(l+1)) codes
-    const int64_t bound = l + 1 < 21 ? std::min<int64_t>(F, (int64_t)1 << (3 * (l + 1))) : F;
-    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(bound, 256), (int64_t)kNumSMs * 8));
-    k_run_flags_lvl<<<g, 256, 0, st>>>(w.lvl_codes, w.bases, w.counts, l + 1, 3, w.flags);
-    WFPG_CHECK_LAUNCH("k_run_flags_lvl");
-    size_t mark = a.off;
-    WFPG_TRY(scan_u32(w.flags, w.scan, bound, reinterpret_cast<const int32_t*>(w.counts + l + 1),
-                      w.counts + l, a, st));
-    a.off = mark;
-    k_parent_level_lvl<<<g, 256, 0, st>>>(w.lvl_codes, w.lvl_owner, w.bases, w.counts, l + 1,
-                                          w.flags, w.scan);
-    WFPG_CHECK_LAUNCH("k_parent_level_lvl");
-  }
+  k_lv_count<<<(unsigned)w.tiles, kLvBlock, 0, st>>>(w.codes, F, depth, w.tiles, w.tile_cnt);
+  WFPG_CHECK_LAUNCH("k_lv_count");
+  k_lv_offsets<<<depth + 1, 1024, 0, st>>>(w.tile_cnt, w.tiles, w.counts);
+  WFPG_CHECK_LAUNCH("k_lv_offsets");
   std::vector<uint32_t> lvl_count(depth + 1);
   WFPG_CUDA(cudaMemcpyAsync(lvl_count.data(), w.counts, sizeof(uint32_t) * (depth + 1),
                             cudaMemcpyDeviceToHost, st));
@@ -541,17 +559,35 @@ namespace wfpg {
 // dual-normal k-means, svo.py:139-173, exact op order
 // ---------------------------------------------------------------------------
 struct LeafNormals {  // fragment normals of one leaf, sorted-fragment order
-  const double* tri_n;
-  const int32_t* frag_tris;
-  const uint32_t* perm;
-  int64_t start;
+  const double* sorted_n;  // gathered once by k_gather_normals: the k-means
+  int64_t start;           // passes re-read a leaf's rows from L1, not HBM
   __device__ __forceinline__ void get(int i, double* n) const {
-    int t = frag_tris[perm[start + i]];
-    n[0] = tri_n[3 * t];
-    n[1] = tri_n[3 * t + 1];
-    n[2] = tri_n[3 * t + 2];
+    const double* p = sorted_n + 3 * (start + i);
+    n[0] = p[0];
+    n[1] = p[1];
+    n[2] = p[2];
   }
 };
+
+// sorted_n[i] = normal of sorted fragment i: tri_n[frag_tris[perm[i]]], or
+// tri_n[perm[i]] for per-fragment normals (frag_tris NULL: surface points).
+// One random gather per fragment instead of one per k-means read.
+__global__ void k_gather_normals(const uint32_t* __restrict__ perm,
+                                 const int32_t* __restrict__ frag_tris,
+                                 const double* __restrict__ tri_n, int64_t F,
+                                 double* __restrict__ sorted_n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < F;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = perm[i];
+    const int64_t t = frag_tris ? (int64_t)frag_tris[f] : f;
+    const double* q = tri_n + 3 * t;
+    const double x = __ldg(q), y = __ldg(q + 1), z = __ldg(q + 2);
+    double* o = sorted_n + 3 * i;
+    o[0] = x;
+    o[1] = y;
+    o[2] = z;
+  }
+}
 
 struct KidNormals {  // [kid_n; -kid_n]
   const double* normal;
@@ -632,52 +668,13 @@ __device__ void cluster_normals(const Src& s, int K, uint64_t key, double* out) 
   out[2] = ma[2];
 }
 
-// Phase B: place levels top-down, wire parents / children / masks.
-__global__ void k_place_level(const uint64_t* __restrict__ lvl_codes, const uint32_t* __restrict__ lvl_owner,
-                              int64_t src, int64_t n, int64_t dst, int64_t parent_dst,
-                              int is_root, uint64_t* __restrict__ codes,
-                              int32_t* __restrict__ parent, int32_t* __restrict__ child_base,
-                              uint8_t* __restrict__ child_mask) {
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t c = lvl_codes[src + k];
-    codes[dst + k] = c;
-    child_base[dst + k] = -1;  // overwritten by the child level if any
-    child_mask[dst + k] = 0;
-    if (is_root) {
-      parent[dst + k] = -1;
-    } else {
-      uint32_t o = lvl_owner[src + k];
-      parent[dst + k] = (int32_t)(parent_dst + o);
-    }
-  }
-}
-
-__global__ void k_wire_children(const uint64_t* __restrict__ lvl_codes,
-                                const uint32_t* __restrict__ lvl_owner, int64_t src, int64_t n,
-                                int64_t dst, int64_t parent_dst, int32_t* __restrict__ child_base,
-                                uint8_t* __restrict__ child_mask) {
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t o = lvl_owner[src + k];
-    if (k > 0 && lvl_owner[src + k - 1] == o) continue;  // not the first child
-    uint32_t mask = 0;
-    for (int64_t j = k; j < n && j < k + 8 && lvl_owner[src + j] == o; ++j)
-      mask |= 1u << (uint32_t)(lvl_codes[src + j] & 7u);
-    child_base[parent_dst + o] = (int32_t)(dst + k);
-    child_mask[parent_dst + o] = (uint8_t)mask;
-  }
-}
-
 __global__ void k_leaf_normals(const uint64_t* __restrict__ codes, int64_t leaf_off, int64_t L,
                                const uint32_t* __restrict__ leaf_start,
-                               const uint32_t* __restrict__ perm,
-                               const int32_t* __restrict__ frag_tris,
-                               const double* __restrict__ tri_n, uint64_t seed,
+                               const double* __restrict__ sorted_n, uint64_t seed,
                                double* __restrict__ normal) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L;
        i += (int64_t)gridDim.x * blockDim.x) {
-    LeafNormals s{tri_n, frag_tris, perm, (int64_t)leaf_start[i]};
+    LeafNormals s{sorted_n, (int64_t)leaf_start[i]};
     int K = (int)(leaf_start[i + 1] - leaf_start[i]);
     double n0[3];
     s.get(0, n0);
@@ -701,13 +698,23 @@ __global__ void k_leaf_normals(const uint64_t* __restrict__ codes, int64_t leaf_
 
 __global__ void k_internal_normals(const uint64_t* __restrict__ codes, int64_t off, int64_t n,
                                    int level, const int32_t* __restrict__ child_base,
-                                   const uint8_t* __restrict__ child_mask, uint64_t seed,
+                                   const int32_t* __restrict__ parent, int64_t kid_end,
+                                   uint8_t* __restrict__ child_mask, uint64_t seed,
                                    double* __restrict__ normal) {
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
     int64_t node = off + k;
     int64_t base = child_base[node];
-    int cnt = __popc((uint32_t)child_mask[node]);
+    // children: the run of next-level nodes from child_base whose parent is
+    // this node (at most 8, ending at the next level's end); the child mask
+    // is their octants (svo.py:470-478)
+    int cnt = 0;
+    uint32_t mask = 0;
+    while (cnt < 8 && base + cnt < kid_end && parent[base + cnt] == (int32_t)node) {
+      mask |= 1u << (uint32_t)(codes[base + cnt] & 7u);
+      ++cnt;
+    }
+    child_mask[node] = (uint8_t)mask;
     const double* kid = normal + 3 * base;
     double a0 = fabs(kid[0]), a1 = fabs(kid[1]), a2 = fabs(kid[2]);
     bool same = true;
@@ -798,50 +805,59 @@ extern "C" int wfpg_svo_build_fill(wfpg_svo* svo, const int32_t* frag_tris,
     set_error("svo build: workspace too small");
     return WFPG_ERR_WORKSPACE;
   }
-  // packed bottom-up level bases (same as phase A)
-  std::vector<int64_t> base(depth + 1), cnt(depth + 1);
-  for (int l = 0; l <= depth; ++l) cnt[l] = svo->level_off[l + 1] - svo->level_off[l];
-  base[depth] = 0;
-  for (int l = depth - 1; l >= 0; --l) base[l] = base[l + 1] + cnt[l + 1];
   const int64_t n = svo->n_nodes;
   auto grid_for = [](int64_t m) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 256), (int64_t)kNumSMs * 8));
   };
-  for (int l = 0; l <= depth; ++l) {
-    int64_t dst = svo->level_off[l];
-    int64_t pdst = l > 0 ? svo->level_off[l - 1] : 0;
-    k_place_level<<<grid_for(cnt[l]), 256, 0, st>>>(w.lvl_codes, w.lvl_owner, base[l], cnt[l], dst,
-                                                   pdst, l == 0, svo->codes, svo->parent,
-                                                   svo->child_base, svo->child_mask);
-    WFPG_CHECK_LAUNCH("k_place_level");
+  std::vector<int64_t> cnt(depth + 1);
+  for (int l = 0; l <= depth; ++l) cnt[l] = svo->level_off[l + 1] - svo->level_off[l];
+  LevelOffs lo;
+  for (int l = 0; l <= depth + 1 && l <= kLvMaxLevels; ++l) lo.off[l] = svo->level_off[l];
+  // structure: every node written once by the fragment that starts it
+  k_lv_emit<<<(unsigned)w.tiles, kLvBlock, 0, st>>>(w.codes, n_fragments, depth, w.tiles,
+                                                    w.tile_cnt, lo, svo->codes, svo->parent,
+                                                    svo->child_base, svo->child_mask,
+                                                    w.leaf_start);
+  WFPG_CHECK_LAUNCH("k_lv_emit");
+  k_set_u32<<<1, 1, 0, st>>>(w.leaf_start + cnt[depth], (uint32_t)n_fragments);
+  WFPG_CHECK_LAUNCH("k_set_u32");
+  // zeroed accumulators / means / counters (svo.py:448-455): 116 B per node,
+  // written on a side stream while the normals are fitted (the gather and
+  // k-means are latency-bound), joined before returning
+  static cudaStream_t side = nullptr;
+  static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  if (!side) {
+    WFPG_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    WFPG_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    WFPG_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
   }
-  for (int l = 1; l <= depth; ++l) {
-    k_wire_children<<<grid_for(cnt[l]), 256, 0, st>>>(w.lvl_codes, w.lvl_owner, base[l], cnt[l],
-                                                     svo->level_off[l], svo->level_off[l - 1],
-                                                     svo->child_base, svo->child_mask);
-    WFPG_CHECK_LAUNCH("k_wire_children");
-  }
-  // zeroed accumulators / means / counters (svo.py:448-455)
-  if (svo->sum_a) WFPG_CUDA(cudaMemsetAsync(svo->sum_a, 0, 24 * n, st));
-  if (svo->sum_b) WFPG_CUDA(cudaMemsetAsync(svo->sum_b, 0, 24 * n, st));
-  if (svo->weight_a) WFPG_CUDA(cudaMemsetAsync(svo->weight_a, 0, 8 * n, st));
-  if (svo->weight_b) WFPG_CUDA(cudaMemsetAsync(svo->weight_b, 0, 8 * n, st));
-  if (svo->mean_a) WFPG_CUDA(cudaMemsetAsync(svo->mean_a, 0, 24 * n, st));
-  if (svo->mean_b) WFPG_CUDA(cudaMemsetAsync(svo->mean_b, 0, 24 * n, st));
-  if (svo->counter) WFPG_CUDA(cudaMemsetAsync(svo->counter, 0, 4 * n, st));
+  WFPG_CUDA(cudaEventRecord(ev_fork, st));
+  WFPG_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+  if (svo->sum_a) WFPG_CUDA(cudaMemsetAsync(svo->sum_a, 0, 24 * n, side));
+  if (svo->sum_b) WFPG_CUDA(cudaMemsetAsync(svo->sum_b, 0, 24 * n, side));
+  if (svo->weight_a) WFPG_CUDA(cudaMemsetAsync(svo->weight_a, 0, 8 * n, side));
+  if (svo->weight_b) WFPG_CUDA(cudaMemsetAsync(svo->weight_b, 0, 8 * n, side));
+  if (svo->mean_a) WFPG_CUDA(cudaMemsetAsync(svo->mean_a, 0, 24 * n, side));
+  if (svo->mean_b) WFPG_CUDA(cudaMemsetAsync(svo->mean_b, 0, 24 * n, side));
+  if (svo->counter) WFPG_CUDA(cudaMemsetAsync(svo->counter, 0, 4 * n, side));
+  WFPG_CUDA(cudaEventRecord(ev_join, side));
   // normals: leaves, then internal levels bottom-up
   int64_t L = cnt[depth];
+  k_gather_normals<<<grid_for(n_fragments), 256, 0, st>>>(w.perm, frag_tris, tri_normals,
+                                                          n_fragments, w.sorted_n);
+  WFPG_CHECK_LAUNCH("k_gather_normals");
   k_leaf_normals<<<grid_for(L), 128, 0, st>>>(svo->codes, svo->level_off[depth], L, w.leaf_start,
-                                              w.perm, frag_tris, tri_normals, seed, svo->normal);
+                                              w.sorted_n, seed, svo->normal);
   WFPG_CHECK_LAUNCH("k_leaf_normals");
   for (int l = depth - 1; l >= 0; --l) {
-    k_internal_normals<<<grid_for(cnt[l]), 128, 0, st>>>(svo->codes, svo->level_off[l], cnt[l], l,
-                                                         svo->child_base, svo->child_mask, seed,
-                                                         svo->normal);
+    k_internal_normals<<<grid_for(cnt[l]), 128, 0, st>>>(
+        svo->codes, svo->level_off[l], cnt[l], l, svo->child_base, svo->parent,
+        svo->level_off[l + 2], svo->child_mask, seed, svo->normal);
     WFPG_CHECK_LAUNCH("k_internal_normals");
   }
   k_node_desc<<<grid_for(n), 256, 0, st>>>(svo->child_base, svo->child_mask, n,
                                            reinterpret_cast<uint2*>(svo->node_desc));
   WFPG_CHECK_LAUNCH("k_node_desc");
+  WFPG_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
   return build_top_index(svo, st);
 }

@@ -479,8 +479,8 @@ def build_from_points(points, normals, cube_lo, cube_size, resolution, seed=0):
     if n == 0:
         raise ValueError("cannot build an octree from an empty fragment list")
     coords = quantise_points(points, cube_lo, cube_size, resolution)
-    idx = _dev.torch().arange(n, dtype=_dev.torch().int32, device=coords.device)
-    return _build(coords, idx, normals, cube_lo, cube_size, resolution, seed)
+    # frag_tris NULL: fragment i's normal is normals[i]
+    return _build(coords, None, normals, cube_lo, cube_size, resolution, seed)
 
 
 def build_from_scene(scene, resolution, seed=0):
