@@ -243,6 +243,18 @@ __device__ __forceinline__ void ph_mark(int k) {
   if (k > 0) atomicAdd(&g_field_phase[k - 1], (unsigned long long)(now - last));
   last = now;
 }
+}  // namespace wfpg
+// read (and optionally reset) the phase counters: tools/field_phases.py
+extern "C" int wfpg_debug_field_phases(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, wfpg::g_field_phase, sizeof(unsigned long long) * 8) != cudaSuccess)
+    return -1;
+  if (reset) {
+    static const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (cudaMemcpyToSymbol(wfpg::g_field_phase, z, sizeof(z)) != cudaSuccess) return -1;
+  }
+  return 0;
+}
+namespace wfpg {
 #endif
 
 // PRODUCT: block sums (+ block row sums) for the product sampler; a separate

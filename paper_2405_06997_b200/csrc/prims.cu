@@ -204,12 +204,18 @@ __global__ void __launch_bounds__(kCsBlock) k_cs_scatter(
     KT k[kCsIpt];
     uint32_t v[kCsIpt];
     uint32_t r[kCsIpt];
+    // all of the tile's loads in flight before the first ranking step
 #pragma unroll
     for (int c = 0; c < kCsIpt; ++c) {
       const int64_t i = wbase + c * 32 + lane;
       const bool valid = i < c1;
       k[c] = valid ? kin[i] : (KT)0;
       v[c] = valid ? vin[i] : 0u;
+    }
+#pragma unroll
+    for (int c = 0; c < kCsIpt; ++c) {
+      const int64_t i = wbase + c * 32 + lane;
+      const bool valid = i < c1;
       const uint32_t dig = valid ? (uint32_t)((k[c] >> shift) & dm) : (uint32_t)radix + lane;
       const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
       const uint32_t peers = __match_any_sync(0xffffffffu, dig) & vmask;

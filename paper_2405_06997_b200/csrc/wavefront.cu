@@ -133,7 +133,7 @@ __global__ void k_occluded(SceneView s, const double* __restrict__ orig,
 // BRUTE: shadow rays by brute force over the shared-memory triangles (small
 // scenes), else BVH traversal; separate instantiations keep the BVH
 // traversal's registers and stack out of the small-scene kernel
-template <bool BRUTE>
+template <bool BRUTE, int MODE>
 __device__ __forceinline__ void shade_path(int64_t p, int depth, const SceneView& sa,
                                            const GuideView& g, const PathsView& P,
                                            const double* hit_t, const int32_t* hit_tri,
@@ -219,7 +219,7 @@ __device__ __forceinline__ void shade_path(int64_t p, int depth, const SceneView
   const double alx = mrgb[0], aly = mrgb[1], alz = mrgb[2];
   const uint64_t kk = P.key[p];
   uint64_t c = P.ctr[p];
-  const int slot = (g.mode > 0 && bin_slot) ? bin_slot[p] : -1;
+  const int slot = (MODE > 0 && bin_slot) ? bin_slot[p] : -1;
   const bool guided = slot >= 0;
 
   // product layer (_kernels.pyx:1003-1019): built after the shadow ray (a
@@ -260,7 +260,7 @@ __device__ __forceinline__ void shade_path(int64_t p, int depth, const SceneView
         // the guide-table entry of the light direction (plain guiding) is
         // requested before the shadow ray so its DRAM latency overlaps it
         int nci = 0, ncj = 0;
-        if (guided && g.mode == 1) {
+        if (MODE == 1 && guided) {
           cell_of(g.n, lx, ly, lz, &nci, &ncj);
           prefetch_l2(g.vals + ((int64_t)slot * g.n + ncj) * g.n + nci);
         }
@@ -273,11 +273,11 @@ __device__ __forceinline__ void shade_path(int64_t p, int depth, const SceneView
         if (!blocked) {
           double p_cont;
           if (guided) {
-            if (g.mode == 2) {
+            if (MODE == 2) {
               product_layer(g, slot, nsx, nsy, nsz, alx, aly, alz, &layer);
               have_layer = true;
             }
-            double pg = g.mode == 1 ? pdf_plain_cell(g, slot, nci, ncj)
+            double pg = MODE == 1 ? pdf_plain_cell(g, slot, nci, ncj)
                                     : pdf_product(g, slot, layer, lx, ly, lz);
             p_cont = 0.5 * pg + 0.5 * (cos_s / WFPG_PI);
           } else {
@@ -312,13 +312,13 @@ __device__ __forceinline__ void shade_path(int64_t p, int depth, const SceneView
 
   // ---- continuation ----
   double wx = 0.0, wy = 0.0, wz = 1.0, cos_rel, pdf_mix;
-  if (guided && g.mode == 2 && !have_layer)
+  if (MODE == 2 && guided && !have_layer)
     product_layer(g, slot, nsx, nsy, nsz, alx, aly, alz, &layer);
   if (guided) {
     double coin = u01(kk, c);
     c += 1;
     if (coin < 0.5) {
-      if (g.mode == 1) {
+      if (MODE == 1) {
         double s1 = u01(kk, c), s2 = u01(kk, c + 1);
         c += 2;
         sample_plain(g, slot, s1, s2, &wx, &wy, &wz);
@@ -333,7 +333,7 @@ __device__ __forceinline__ void shade_path(int64_t p, int depth, const SceneView
       cosine_dir(nsx, nsy, nsz, s1, s2, &wx, &wy, &wz);
     }
     cos_rel = wx * nsx + wy * nsy + wz * nsz;
-    double pg = g.mode == 1 ? pdf_plain(g, slot, wx, wy, wz)
+    double pg = MODE == 1 ? pdf_plain(g, slot, wx, wy, wz)
                             : pdf_product(g, slot, layer, wx, wy, wz);
     double pb = fmax(cos_rel, 0.0) / WFPG_PI;
     pdf_mix = 0.5 * pg + 0.5 * pb;
@@ -365,7 +365,9 @@ __device__ __forceinline__ void shade_path(int64_t p, int depth, const SceneView
   P.ctr[p] = c;
 }
 
-template <bool BRUTE>
+// MODE: 0 unguided, 1 plain guiding, 2 product guiding (GuideView.mode) — one
+// instantiation each, so the plain kernel carries no product-layer registers
+template <bool BRUTE, int MODE>
 __global__ void __launch_bounds__(256, 3) k_shade(SceneView s, GuideView g, PathsView P, int depth,
                                                const int32_t* __restrict__ active, int64_t n_max,
                                                const int32_t* __restrict__ n_dev,
@@ -380,8 +382,8 @@ __global__ void __launch_bounds__(256, 3) k_shade(SceneView s, GuideView g, Path
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int64_t p = active ? active[i] : i;
-    shade_path<BRUTE>(p, depth, s, g, P, hit_t, hit_tri, bin_slot, rr != 0, rr_depth,
-                      smt_shade);
+    shade_path<BRUTE, MODE>(p, depth, s, g, P, hit_t, hit_tri, bin_slot, rr != 0, rr_depth,
+                            smt_shade);
   }
 }
 
@@ -499,12 +501,20 @@ int launch_shade(const SceneView& s, const GuideView& g, const PathsView& P, int
   }
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_max, 256), kNumSMs * 8));
   const size_t smem = s.brute ? sizeof(TriRec) * s.n_tris : 0;
-  if (s.brute)
-    k_shade<true><<<grid, 256, smem, st>>>(s, g, P, depth, active, n_max, n_dev, hit_t, hit_tri,
-                                           bin_slot, rr ? 1 : 0, rr_depth);
-  else
-    k_shade<false><<<grid, 256, smem, st>>>(s, g, P, depth, active, n_max, n_dev, hit_t, hit_tri,
-                                            bin_slot, rr ? 1 : 0, rr_depth);
+#define WFPG_SHADE_(B, M)                                                                   \
+  k_shade<B, M><<<grid, 256, smem, st>>>(s, g, P, depth, active, n_max, n_dev, hit_t, hit_tri, \
+                                         bin_slot, rr ? 1 : 0, rr_depth)
+  const int mode = g.mode == 1 ? 1 : (g.mode == 2 ? 2 : 0);
+  if (s.brute) {
+    if (mode == 1) WFPG_SHADE_(true, 1);
+    else if (mode == 2) WFPG_SHADE_(true, 2);
+    else WFPG_SHADE_(true, 0);
+  } else {
+    if (mode == 1) WFPG_SHADE_(false, 1);
+    else if (mode == 2) WFPG_SHADE_(false, 2);
+    else WFPG_SHADE_(false, 0);
+  }
+#undef WFPG_SHADE_
   WFPG_CHECK_LAUNCH("k_shade");
   return WFPG_OK;
 }
