@@ -139,9 +139,20 @@ __device__ __forceinline__ double norm_axis(double x, double y, double z) {
   return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
 }
 
+// fp64 constants of the hot device functions in constant memory: an fp64
+// literal costs two register moves per use (no 64-bit immediates), a
+// constant-bank operand costs nothing (DFMA R, R, c[bank][off], R)
+static __constant__ double c_k[24] = {
+    0.2126, 0.7152, 0.0722,                                           // 0-2 LUMA_WEIGHTS
+    1.0 / 355687428096000.0, 1.0 / 1307674368000.0, 1.0 / 6227020800.0,  // 3-5 sin
+    1.0 / 39916800.0, 1.0 / 362880.0, 1.0 / 5040.0, 1.0 / 120.0, 1.0 / 6.0,  // 6-10
+    1.0 / 6402373705728000.0, 1.0 / 20922789888000.0, 1.0 / 87178291200.0,  // 11-13 cos
+    1.0 / 479001600.0, 1.0 / 3628800.0, 1.0 / 40320.0, 1.0 / 720.0, 1.0 / 24.0,  // 14-18
+    0.5, WFPG_PI / 4.0, 0.70710678118654752440, 0.0, 0.0};             // 19-21
+
 // luminance of an (M,3) RGB array: core.py:18-19 (rgb @ LUMA_WEIGHTS, dgemv)
 __device__ __forceinline__ double luminance_rows(double r, double g, double b) {
-  return dot_gemv(r, g, b, 0.2126, 0.7152, 0.0722);
+  return dot_gemv(r, g, b, c_k[0], c_k[1], c_k[2]);
 }
 
 // ---------------------------------------------------------------------------
@@ -206,28 +217,28 @@ __device__ __forceinline__ double fast_sqrt(double x) {  // x > 0
 // About 25 fp64 operations against ~60 instructions for sincospi, within
 // 2 ulp of the exact values.
 __device__ __forceinline__ void sincos_quarter_turn(double t, double* so, double* co) {
-  const double x = (t - 1.0) * (WFPG_PI / 4.0);
+  const double x = (t - 1.0) * c_k[20];  // pi / 4
   const double x2 = x * x;
-  double sp = 1.0 / 355687428096000.0;                 // 1/17!
-  sp = fma(sp, -x2, 1.0 / 1307674368000.0);            // 1/15!
-  sp = fma(sp, -x2, 1.0 / 6227020800.0);               // 1/13!
-  sp = fma(sp, -x2, 1.0 / 39916800.0);                 // 1/11!
-  sp = fma(sp, -x2, 1.0 / 362880.0);                   // 1/9!
-  sp = fma(sp, -x2, 1.0 / 5040.0);                     // 1/7!
-  sp = fma(sp, -x2, 1.0 / 120.0);
-  sp = fma(sp, -x2, 1.0 / 6.0);
+  double sp = c_k[3];                  // 1/17!
+  sp = fma(sp, -x2, c_k[4]);           // 1/15!
+  sp = fma(sp, -x2, c_k[5]);           // 1/13!
+  sp = fma(sp, -x2, c_k[6]);           // 1/11!
+  sp = fma(sp, -x2, c_k[7]);           // 1/9!
+  sp = fma(sp, -x2, c_k[8]);           // 1/7!
+  sp = fma(sp, -x2, c_k[9]);           // 1/5!
+  sp = fma(sp, -x2, c_k[10]);          // 1/3!
   const double sx = fma(-x * x2, sp, x);
-  double cp = 1.0 / 6402373705728000.0;                // 1/18!
-  cp = fma(cp, -x2, 1.0 / 20922789888000.0);           // 1/16!
-  cp = fma(cp, -x2, 1.0 / 87178291200.0);              // 1/14!
-  cp = fma(cp, -x2, 1.0 / 479001600.0);                // 1/12!
-  cp = fma(cp, -x2, 1.0 / 3628800.0);                  // 1/10!
-  cp = fma(cp, -x2, 1.0 / 40320.0);                    // 1/8!
-  cp = fma(cp, -x2, 1.0 / 720.0);
-  cp = fma(cp, -x2, 1.0 / 24.0);
-  cp = fma(cp, -x2, 0.5);
+  double cp = c_k[11];                 // 1/18!
+  cp = fma(cp, -x2, c_k[12]);          // 1/16!
+  cp = fma(cp, -x2, c_k[13]);          // 1/14!
+  cp = fma(cp, -x2, c_k[14]);          // 1/12!
+  cp = fma(cp, -x2, c_k[15]);          // 1/10!
+  cp = fma(cp, -x2, c_k[16]);          // 1/8!
+  cp = fma(cp, -x2, c_k[17]);          // 1/6!
+  cp = fma(cp, -x2, c_k[18]);          // 1/4!
+  cp = fma(cp, -x2, c_k[19]);          // 1/2
   const double cx = fma(-x2, cp, 1.0);
-  const double r2 = 0.70710678118654752440;
+  const double r2 = c_k[21];           // sqrt(1/2)
   *so = (sx + cx) * r2;
   *co = (cx - sx) * r2;
 }
