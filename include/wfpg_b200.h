@@ -138,8 +138,8 @@ typedef struct wfpg_paths {
   uint64_t* ctr;             /* (P,) */
   uint8_t* alive;            /* (P,) */
   double* prev_pdf;          /* (P,) */
-  double* rec_pos;           /* (P,D+1,3) */
-  double* rec_T;             /* (P,D+1,3) */
+  double* rec_pos;           /* (P,D+1,3), or (D+1,P,3): rec_depth_major */
+  double* rec_T;             /* (P,D+1,3), or (D+1,P,3): rec_depth_major */
   double* emit_le;           /* (P,3) */
   int32_t* emit_depth;       /* (P,) */
   /* Optional (P,) deepest record slot written (0 = camera only).  When set,
@@ -147,6 +147,11 @@ typedef struct wfpg_paths {
    * slots above n_rec hold stale values, which readers mask (the exitance
    * update only reads slots <= emit_depth <= n_rec).  NULL: zeroed slots. */
   uint8_t* n_rec;
+  /* Record layout: 0 = (P, D+1, 3), the reference's PathState layout;
+   * 1 = (D+1, P, 3) depth-major — one depth's records of consecutive paths
+   * are contiguous, so the shade kernel's record stores fill whole sectors
+   * (the package's own PathState uses it). */
+  int32_t rec_depth_major;
 } wfpg_paths;
 
 /* Per-depth guide tables: guiding.py:254-309 (GuideTables).  The B200 layout

@@ -61,7 +61,7 @@ class Paths(C.Structure):
         ("ray_o", c_vp), ("ray_d", c_vp), ("beta", c_vp), ("radiance", c_vp),
         ("key", c_vp), ("ctr", c_vp), ("alive", c_vp), ("prev_pdf", c_vp),
         ("rec_pos", c_vp), ("rec_T", c_vp), ("emit_le", c_vp), ("emit_depth", c_vp),
-        ("n_rec", c_vp),
+        ("n_rec", c_vp), ("rec_depth_major", c_i32),
     ]
 
 

@@ -8,21 +8,21 @@
 
 namespace wfpg {
 
-__device__ __forceinline__ bool deposit_ok(const double* rt, int k) {
-  return rt[3 * k] > 0.0 && rt[3 * k + 1] > 0.0 && rt[3 * k + 2] > 0.0;
+__device__ __forceinline__ bool deposit_ok(const double* rt, int k, int64_t sd) {
+  return rt[k * sd] > 0.0 && rt[k * sd + 1] > 0.0 && rt[k * sd + 2] > 0.0;
 }
 
 __global__ void k_dep_count(const int32_t* __restrict__ emit_depth,
                             const double* __restrict__ emit_le, const double* __restrict__ rec_T,
-                            int rec_depths, int64_t n, uint32_t* __restrict__ counts) {
+                            RecLayout rl, int64_t n, uint32_t* __restrict__ counts) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x) {
     int nd = emit_depth[p];
     const double* le = emit_le + 3 * p;
     uint32_t c = 0;
     if (nd >= 2 && (le[0] + le[1] + le[2]) > 0.0) {
-      const double* rt = rec_T + (int64_t)p * rec_depths * 3;
-      for (int k = 1; k < nd; ++k) c += deposit_ok(rt, k) ? 1u : 0u;
+      const double* rt = rec_T + p * rl.sp;
+      for (int k = 1; k < nd; ++k) c += deposit_ok(rt, k, rl.sd) ? 1u : 0u;
     }
     counts[p] = c;
   }
@@ -30,7 +30,7 @@ __global__ void k_dep_count(const int32_t* __restrict__ emit_depth,
 
 __global__ void k_dep_emit(SvoView v, const int32_t* __restrict__ emit_depth,
                            const double* __restrict__ emit_le, const double* __restrict__ rec_T,
-                           const double* __restrict__ rec_pos, int rec_depths, int64_t n,
+                           const double* __restrict__ rec_pos, RecLayout rl, int64_t n,
                            const uint32_t* __restrict__ counts, const uint32_t* __restrict__ offs,
                            int32_t* __restrict__ leaf, double* __restrict__ dirs,
                            double* __restrict__ rad) {
@@ -41,18 +41,18 @@ __global__ void k_dep_emit(SvoView v, const int32_t* __restrict__ emit_depth,
        p += (int64_t)gridDim.x * blockDim.x) {
     if (counts[p] == 0) continue;
     int nd = emit_depth[p];
-    const double* rt = rec_T + (int64_t)p * rec_depths * 3;
-    const double* rp = rec_pos + (int64_t)p * rec_depths * 3;
+    const double* rt = rec_T + p * rl.sp;
+    const double* rp = rec_pos + p * rl.sp;
     const double* le = emit_le + 3 * p;
-    const double* tn = rt + 3 * nd;
+    const double* tn = rt + nd * rl.sd;
     uint32_t o = offs[p];
     for (int k = 1; k < nd; ++k) {
-      if (!deposit_ok(rt, k)) continue;
-      const double* tk = rt + 3 * k;
+      if (!deposit_ok(rt, k, rl.sd)) continue;
+      const double* tk = rt + k * rl.sd;
       double* r = rad + 3 * (int64_t)o;
       for (int c = 0; c < 3; ++c) r[c] = __dmul_rn(__ddiv_rn(tn[c], tk[c]), le[c]);
-      const double* pos = rp + 3 * k;
-      const double* prev = rp + 3 * (k - 1);
+      const double* pos = rp + k * rl.sd;
+      const double* prev = rp + (k - 1) * rl.sd;
       double d[3];
       for (int c = 0; c < 3; ++c) d[c] = __dsub_rn(prev[c], pos[c]);
       double nrm = norm_axis(d[0], d[1], d[2]);
@@ -84,11 +84,11 @@ size_t update_exitance_ws_bytes(int64_t n_paths, int max_depth) {
 }
 
 int update_exitance(wfpg_svo* svo, const int32_t* emit_depth, const double* emit_le,
-                    const double* rec_T, const double* rec_pos, int rec_depths, int64_t n_paths,
+                    const double* rec_T, const double* rec_pos, RecLayout rl, int64_t n_paths,
                     int deterministic, int32_t* n_dep_out, Arena& ws, cudaStream_t st,
                     int propagate, uint8_t* dirty, const DepositSink* sink) {
   if (n_paths <= 0) return WFPG_OK;
-  const int64_t m = n_paths * (int64_t)(rec_depths - 1 > 0 ? rec_depths - 1 : 1);
+  const int64_t m = n_paths * (int64_t)(rl.depths - 1 > 0 ? rl.depths - 1 : 1);
   if (sink && (sink->capacity < m || !sink->leaf || !sink->dir || !sink->rad || !sink->count)) {
     set_error("update_exitance: deposit sink needs capacity >= n_paths * max_depth (%lld)",
               (long long)m);
@@ -106,14 +106,14 @@ int update_exitance(wfpg_svo* svo, const int32_t* emit_depth, const double* emit
   }
   SvoView v = make_view(svo);
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_paths, 256), kNumSMs * 8));
-  k_dep_count<<<grid, 256, 0, st>>>(emit_depth, emit_le, rec_T, rec_depths, n_paths, counts);
+  k_dep_count<<<grid, 256, 0, st>>>(emit_depth, emit_le, rec_T, rl, n_paths, counts);
   WFPG_CHECK_LAUNCH("k_dep_count");
   {
     size_t mark = ws.off;
     WFPG_TRY(scan_u32(counts, offs, n_paths, nullptr, total, ws, st));
     ws.off = mark;
   }
-  k_dep_emit<<<grid, 256, 0, st>>>(v, emit_depth, emit_le, rec_T, rec_pos, rec_depths, n_paths,
+  k_dep_emit<<<grid, 256, 0, st>>>(v, emit_depth, emit_le, rec_T, rec_pos, rl, n_paths,
                                    counts, offs, leaf, dirs, rad);
   WFPG_CHECK_LAUNCH("k_dep_emit");
   const int32_t* n_dev = reinterpret_cast<const int32_t*>(total);
@@ -149,6 +149,6 @@ extern "C" int wfpg_update_exitance(wfpg_svo* svo, const wfpg_paths* paths, int3
   }
   Arena ws(workspace, ws_bytes);
   return update_exitance(svo, paths->emit_depth, paths->emit_le, paths->rec_T, paths->rec_pos,
-                         paths->max_depth + 1, paths->n, deterministic, n_deposits_dev, ws,
+                         rec_layout(paths), paths->n, deterministic, n_deposits_dev, ws,
                          as_stream(stream), 1, nullptr);
 }

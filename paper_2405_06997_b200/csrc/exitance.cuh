@@ -14,8 +14,20 @@ struct DepositSink {
   int32_t* count;   // device count
   int64_t capacity;
 };
+// record layout of rec_T / rec_pos: slot k of path p at p * sp + k * sd doubles
+struct RecLayout {
+  int depths;
+  int64_t sp, sd;
+};
+inline RecLayout rec_layout(const wfpg_paths* p) {
+  RecLayout r;
+  r.depths = p->max_depth + 1;
+  r.sp = p->rec_depth_major ? 3 : 3 * (int64_t)r.depths;
+  r.sd = p->rec_depth_major ? 3 * p->n : 3;
+  return r;
+}
 int update_exitance(wfpg_svo* svo, const int32_t* emit_depth, const double* emit_le,
-                    const double* rec_T, const double* rec_pos, int rec_depths, int64_t n_paths,
+                    const double* rec_T, const double* rec_pos, RecLayout rl, int64_t n_paths,
                     int deterministic, int32_t* n_dep_out, Arena& ws, cudaStream_t st,
                     int propagate = 1, uint8_t* dirty = nullptr,  // 0 none, 1 full, 2 dirty-only
                     const DepositSink* sink = nullptr);

@@ -792,7 +792,7 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
     DepositSink sink{L.dep_leaf, L.dep_dir, L.dep_rad, L.dep_count,
                      P * (int64_t)std::max(1, cfg->max_depth)};
     WFPG_TRY(update_exitance(svo, paths->emit_depth, paths->emit_le, paths->rec_T,
-                             paths->rec_pos, cfg->max_depth + 1, P, cfg->deterministic,
+                             paths->rec_pos, rec_layout(paths), P, cfg->deterministic,
                              &L.stats->deposits, scratch, st, 0, nullptr, &sink));
     const int wgrid =
         (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(L.wire_cap, 256), kNumSMs * 4));
@@ -822,21 +822,21 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
     DepositSink sink{cfg->dep_leaf, cfg->dep_dir, cfg->dep_rad, cfg->dep_count,
                      cfg->dep_capacity};
     WFPG_TRY(update_exitance(svo, paths->emit_depth, paths->emit_le, paths->rec_T,
-                             paths->rec_pos, cfg->max_depth + 1, P, cfg->deterministic,
+                             paths->rec_pos, rec_layout(paths), P, cfg->deterministic,
                              &L.stats->deposits, scratch, st, 0, nullptr, &sink));
   } else if (svo && cfg->leaf_acc) {
     int64_t nleaf = svo->level_off[svo->depth + 1] - svo->level_off[svo->depth];
     WFPG_CUDA(cudaMemsetAsync(cfg->leaf_acc, 0, sizeof(double) * 8 * nleaf, st));
     wfpg_svo acc_view = leaf_acc_view(svo, cfg->leaf_acc);
     WFPG_TRY(update_exitance(&acc_view, paths->emit_depth, paths->emit_le, paths->rec_T,
-                             paths->rec_pos, cfg->max_depth + 1, P, cfg->deterministic,
+                             paths->rec_pos, rec_layout(paths), P, cfg->deterministic,
                              &L.stats->deposits, scratch, st, 0));
   } else if (svo) {
     // the SVO means are consistent at pass start, so only the deposited
     // subtrees need refreshing (bitwise equal to the full recompute)
     WFPG_CUDA(cudaMemsetAsync(L.dirty, 0, (size_t)svo->n_nodes, st));
     WFPG_TRY(update_exitance(svo, paths->emit_depth, paths->emit_le, paths->rec_T,
-                             paths->rec_pos, cfg->max_depth + 1, P, cfg->deterministic,
+                             paths->rec_pos, rec_layout(paths), P, cfg->deterministic,
                              &L.stats->deposits, scratch, st, 2, L.dirty));
   }
   if (svo) WFPG_TRY(rec_ev(cfg->ev_rec_svo));

@@ -351,6 +351,7 @@ struct PathsView {
   int32_t* emit_depth;
   uint8_t* n_rec;  // optional: deepest record slot written
   int32_t rec_depths;
+  int64_t rec_sp, rec_sd;  // record strides (doubles) per path and per depth
 };
 
 // shade_one (_kernels.pyx:905-1161) for path p.

@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(kInitTile) k_init_paths(CameraView c, PathsVie
       P.prev_pdf[p] = -1.0;
       P.emit_depth[p] = 0;
       if (P.n_rec) P.n_rec[p] = 0;
-      double* rp = P.rec_pos + (int64_t)p * P.rec_depths * 3;  // zeroed by the launcher unless n_rec
+      double* rp = P.rec_pos + p * P.rec_sp;  // slot 0; zeroed by the launcher unless n_rec
       rp[0] = c.pos[0];
       rp[1] = c.pos[1];
       rp[2] = c.pos[2];
@@ -152,7 +152,7 @@ __device__ __forceinline__ void shade_path(int64_t p, int depth, const SceneView
   const double dx = rd[0], dy = rd[1], dz = rd[2];
   const double px = ro[0] + t * dx, py = ro[1] + t * dy, pz = ro[2] + t * dz;
   {
-    int64_t rb = ((int64_t)p * P.rec_depths + depth) * 3;
+    int64_t rb = p * P.rec_sp + depth * P.rec_sd;
     P.rec_pos[rb] = px;
     P.rec_pos[rb + 1] = py;
     P.rec_pos[rb + 2] = pz;
@@ -437,7 +437,10 @@ int launch_camera_init(const CameraView& c, const PathsView& P, int64_t n_paths,
                        int64_t n_img, int64_t pix0, const int64_t* sample0,
                        const int64_t* sample_list, uint64_t seed, cudaStream_t st) {
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_paths, 256), kNumSMs * 8));
-  size_t rec_bytes = sizeof(double) * 3 * (size_t)P.rec_depths * (size_t)n_paths;
+  // depth-major records span the whole (D+1, P, 3) array
+  size_t rec_bytes = P.rec_sp == 3 && P.rec_depths > 1
+                         ? sizeof(double) * (size_t)P.rec_depths * (size_t)P.rec_sd
+                         : sizeof(double) * 3 * (size_t)P.rec_depths * (size_t)n_paths;
   if (!P.n_rec) {  // with n_rec, slots above it are masked by the readers
     WFPG_CUDA(cudaMemsetAsync(P.rec_pos, 0, rec_bytes, st));
     WFPG_CUDA(cudaMemsetAsync(P.rec_T, 0, rec_bytes, st));
@@ -535,6 +538,8 @@ PathsView make_paths_view(const wfpg_paths* p) {
   v.emit_le = p->emit_le;
   v.emit_depth = p->emit_depth;
   v.rec_depths = p->max_depth + 1;
+  v.rec_sp = p->rec_depth_major ? 3 : 3 * (int64_t)v.rec_depths;
+  v.rec_sd = p->rec_depth_major ? 3 * p->n : 3;
   return v;
 }
 

@@ -57,12 +57,17 @@ _STATE = {
     "beta": (np.float64, lambda d: (3,)), "radiance": (np.float64, lambda d: (3,)),
     "key": (np.uint64, lambda d: ()), "ctr": (np.uint64, lambda d: ()),
     "alive": (np.uint8, lambda d: ()), "prev_pdf": (np.float64, lambda d: ()),
+    # records: (D+1, P, 3) on the device (depth-major: one depth's records of
+    # consecutive paths are contiguous); read back as the reference's (P, D+1, 3)
     "rec_pos": (np.float64, lambda d: (d + 1, 3)), "rec_T": (np.float64, lambda d: (d + 1, 3)),
     "emit_le": (np.float64, lambda d: (3,)), "emit_depth": (np.int32, lambda d: ()),
     # deepest record slot written this pass: slots above it are stale on the
     # device (the pass does not re-zero them) and read back as zeros
     "n_rec": (np.uint8, lambda d: ()),
 }
+
+
+_RECORDS = ("rec_pos", "rec_T")
 
 
 class PathState:
@@ -74,12 +79,15 @@ class PathState:
         self.max_depth = int(max_depth)
         self.dev = {}
         for name, (dt, shp) in _STATE.items():
+            if name in _RECORDS:
+                self.dev[name] = _dev.zeros((self.max_depth + 1, self.n, 3), dt)
+                continue
             self.dev[name] = _dev.zeros((self.n,) + shp(self.max_depth), dt)
         self.dev["beta"].fill_(1.0)
         self.dev["alive"].fill_(1)
         self.dev["prev_pdf"].fill_(-1.0)
         cp = np.asarray(camera_pos, dtype=np.float64)
-        self.dev["rec_pos"][:, 0] = _dev.upload(cp)
+        self.dev["rec_pos"][0, :] = _dev.upload(cp)
         self.pixel = np.arange(self.n, dtype=np.int64)
 
     def abi(self):
@@ -88,12 +96,21 @@ class PathState:
         p.max_depth = self.max_depth
         for name in _STATE:
             setattr(p, name, self.dev[name].data_ptr())
+        p.rec_depth_major = 1
         return p
+
+    def set(self, name, host):
+        """Upload a host array in the reference's layout ((P, D+1, 3) for the
+        records)."""
+        a = np.asarray(host, dtype=_STATE[name][0])
+        t = _dev.upload(np.ascontiguousarray(a.transpose(1, 0, 2)) if name in _RECORDS else a)
+        self.dev[name].copy_(t.reshape(self.dev[name].shape))
 
     def __getattr__(self, name):
         if name in _STATE and "dev" in self.__dict__:
             a = _dev.download(self.dev[name])
-            if name in ("rec_pos", "rec_T"):
+            if name in _RECORDS:
+                a = np.ascontiguousarray(a.transpose(1, 0, 2))
                 n_rec = _dev.download(self.dev["n_rec"]).astype(np.int64)
                 a[np.arange(a.shape[1])[None, :] > n_rec[:, None]] = 0.0
             return a.astype(bool) if name == "alive" else a

@@ -115,8 +115,8 @@ def test_eq5_deposit_and_running_mean():
     rt = np.zeros((1, 4, 3))
     rt[0, 1] = 0.5
     rt[0, 2] = 0.125
-    st.dev["rec_pos"].copy_(st.dev["rec_pos"].new_tensor(rp))
-    st.dev["rec_T"].copy_(st.dev["rec_T"].new_tensor(rt))
+    st.set("rec_pos", rp)
+    st.set("rec_T", rt)
     st.dev["emit_le"].fill_(8.0)
     st.dev["emit_depth"].fill_(2)
     dirty = wavefront.update_exitance(st, tree)
