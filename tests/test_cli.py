@@ -113,6 +113,9 @@ def test_accumulation_buffer_bitwise():
     bad[1, 1, 1] = np.nan
     with pytest.raises(ValueError, match="non-finite"):
         buf.add_sample(bad)
+    # the rejected frame left the running sums untouched (the reference raises
+    # before touching weighted_sum)
+    assert np.array_equal(buf.resolve().view(np.uint64), (ws / w).view(np.uint64))
 
 
 @pytest.mark.gpu
