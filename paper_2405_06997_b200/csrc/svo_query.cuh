@@ -21,8 +21,14 @@ __device__ __forceinline__ int best_cone_level(double size, int depth, double ar
   // ties), which is what the level-by-level scan from the leaf level returns.
   const double s0 = size * size;
   const float x = 0.5f * (__log2f((float)s0) - __log2f((float)area));
-  const int c = (int)floorf(fminf(fmaxf(x, -4.0f), 64.0f));
-  const int lo = min(max(c - 1, 0), depth), hi = min(max(c + 2, 0), depth);
+  const float xc = fminf(fmaxf(x, -4.0f), 64.0f);
+  const int c = (int)floorf(xc);
+  // the integer optimum is floor or ceil of the exact x; the estimate is
+  // within ~1e-5 of it (fp32 conversions + __log2f), so away from integers
+  // floor(estimate) = floor(x) and two candidates suffice
+  const float fr = xc - (float)c;
+  const bool safe = fr > 1e-4f && fr < 1.0f - 1e-4f;
+  const int lo = min(max(safe ? c : c - 1, 0), depth), hi = min(max(safe ? c + 1 : c + 2, 0), depth);
   // exact power-of-two scaling: s0 * 2^(-2 lv)
   int best = hi;
   double bd = fabs(__dmul_rn(s0, __longlong_as_double((long long)(1023 - 2 * hi) << 52)) - area);
