@@ -33,6 +33,16 @@ def main():
     ncu = subprocess.run([sys.executable, os.path.join(REPO, "tools", "ncu_raw_summary.py"),
                           "f128=" + os.path.join(P, "round2_ncu_f128_raw.csv")],
                          capture_output=True, text=True).stdout
+    shade = subprocess.run([sys.executable, os.path.join(REPO, "tools", "ncu_raw_summary.py"),
+                            "shade=" + os.path.join(P, "round2_ncu_shade_raw.csv")],
+                           capture_output=True, text=True).stdout
+    import csv as _csv
+    _rows = list(_csv.reader(open(os.path.join(P, "round2_ncu_shade_raw.csv"))))
+    _h = next(i for i, r in enumerate(_rows) if r and r[0] == "ID")
+    _d, _u = dict(zip(_rows[_h], _rows[_h + 2])), dict(zip(_rows[_h], _rows[_h + 1]))
+    _sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    shade_r = float(_d["dram__bytes_read.sum"].replace(",", "")) * _sc[_u["dram__bytes_read.sum"]] / 2073600
+    shade_w = float(_d["dram__bytes_write.sum"].replace(",", "")) * _sc[_u["dram__bytes_write.sum"]] / 2073600
     lines = subprocess.run([sys.executable, os.path.join(REPO, "tools", "ncu_lines.py"),
                             os.path.join(P, "round2_ncu_f128_source.csv"), "25"],
                            capture_output=True, text=True).stdout
@@ -47,7 +57,7 @@ All numbers: `tools/round_measure.sh` on one B200 (files `profiles/round2_*`).
 * **C3** (`--scene c3`, round2_bench_c3.json): occluded-light two-room interior, SVO R=2048 — **{M(c3):.1f} M/s** ({c3['ms_per_step']:.2f} ms), e2e {c3['e2e']['value'] / 1e6:.1f} M/s.
 * **Product guiding** (`--product`): **{M(pr):.1f} M/s** ({pr['ms_per_step']:.2f} ms), {100 * (1 - pr['value'] / c2['value']):.0f}% below plain (round 1: 19%).
 * **4K on one GPU** (`--width 3840 --height 2160`): {M(k4):.1f} M/s ({k4['ms_per_step']:.1f} ms per pass).
-* **BVH paths** (`--scene tess`, 2,304 triangles): {M(ts):.1f} M/s ({ts['ms_per_step']:.1f} ms); field tracer {ts['roofline']['gcones_per_s']:.1f} G cones/s (per-lane BVH traversal).
+* **BVH paths** (`--scene tess`, 2,304 triangles): {M(ts):.1f} M/s ({ts['ms_per_step']:.1f} ms); field tracer {ts["roofline"]["gcones_per_s"]:.1f} G cones/s (warp-cooperative packet walk, shared-memory stacks).
 
 ## Dominant kernel: `k_fields<128, plain>` (depth-1 fields), ncu --set full
 
@@ -55,6 +65,15 @@ All numbers: `tools/round_measure.sh` on one B200 (files `profiles/round2_*`).
 Top source lines by warp-stall samples (`tools/ncu_lines.py`):
 
 {lines}
+## `k_shade<brute, plain>` (first guided depth-1 launch), ncu --set full
+
+{shade}
+Per live path at depth 1 (2.07 M paths): {shade_r:.0f} B read + {shade_w:.0f} B written from DRAM against SURVEY §8(d)'s 172 B algorithmic — the rest is the guide-table probes of the samplers (1.26 GB of depth-1 tables, far beyond L2; ~10 dependent probes per guided path).  Round 1: 747 MB read / 219 MB written for the same launch; the depth-major path records (full-sector record stores) removed most of the difference.
+
+## C5 microbenchmark
+
+`profiles/round2_c5.md` (SVO build + cone trace, 1 M – 64 M points, depth 8 – 12).
+
 ## Launch list (C2)
 
 `ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e` (round2_launches_c2.csv; C3 round2_launches_c3.csv).  ncu serialises kernels with cold caches: compare shares, not absolutes.

@@ -23,3 +23,8 @@ ncu -i /tmp/f128.ncu-rep --page raw --csv > $O/ncu_f128_raw.csv 2>/dev/null
 ncu -i /tmp/f128.ncu-rep --page source --csv --print-source cuda,sass > $O/ncu_f128_source.csv 2>/dev/null
 python bench.py --impl reference > $O/bench_reference_c2.json 2> $O/bench_reference_c2.err
 ls -la $O
+python tools/bench_c5.py --check-n 1100000 > $O/c5.jsonl 2> $O/c5.err
+ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
+    -k "regex:k_shade" -s 4 -c 1 -f -o /tmp/shade python bench.py --no-cpu-baseline --no-e2e \
+    --steps 1 --warmup 3 > $O/ncu_shade.log 2>&1
+ncu -i /tmp/shade.ncu-rep --page raw --csv > $O/ncu_shade_raw.csv 2>/dev/null
