@@ -105,7 +105,8 @@ typedef struct wfpg_svo {
   int64_t level_off[32];     /* host: depth+2 entries used */
   uint64_t* codes;           /* (n,) morton code at the node's level */
   int32_t* child_base;       /* (n,) first child, -1 for leaves */
-  uint8_t* child_mask;       /* (n,) */
+  uint8_t* child_mask;       /* (n,); wfpg_svo_build_fill needs it 4-byte aligned
+                                and padded to whole 32-bit words (word atomics) */
   int32_t* parent;           /* (n,) -1 for the root */
   uint32_t* node_desc;       /* (n,2) packed {child_base, child_mask} for descents */
   double* normal;            /* (n,3) normal_a (normal_b = -normal_a) */
@@ -397,6 +398,13 @@ int wfpg_svo_build_structure(wfpg_svo* svo, const int32_t* frag_coords, int64_t 
 int wfpg_svo_build_fill(wfpg_svo* svo, const int32_t* frag_tris, const double* tri_normals,
                         int64_t n_fragments, uint64_t seed,
                         void* workspace, size_t ws_bytes, void* stream);
+/* Phase A from fp64 points (n,3) (surface points / path vertices): leaf
+ * coordinates by the compiled quantisation against svo->lo / size /
+ * resolution (_kernels.pyx:593-606), identical to wfpg_quantise_points +
+ * wfpg_svo_build_structure without the coordinate array.  Phase B is
+ * wfpg_svo_build_fill with frag_tris NULL (normals (n,3) per point). */
+int wfpg_svo_build_structure_points(wfpg_svo* svo, const double* points, int64_t n,
+                                    void* workspace, size_t ws_bytes, void* stream);
 /* Debug/golden access to phase-A intermediates kept in the workspace. */
 int wfpg_svo_build_sorted(const void* workspace, int64_t n_fragments,
                           const uint64_t** sorted_codes, const uint32_t** sort_perm);

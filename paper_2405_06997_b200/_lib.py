@@ -145,6 +145,7 @@ _SIGS = {
                                    P(c_i64), c_vp, c_size, c_vp]),
     "wfpg_svo_build_workspace_bytes": (c_size, [c_i64, c_i32]),
     "wfpg_svo_build_structure": (c_i32, [P(Svo), c_vp, c_i64, c_vp, c_size, c_vp]),
+    "wfpg_svo_build_structure_points": (c_i32, [P(Svo), c_vp, c_i64, c_vp, c_size, c_vp]),
     "wfpg_svo_build_fill": (c_i32, [P(Svo), c_vp, c_vp, c_i64, c_u64, c_vp, c_size, c_vp]),
     "wfpg_svo_build_sorted": (c_i32, [c_vp, c_i64, P(c_vp), P(c_vp)]),
     "wfpg_descend": (c_i32, [P(Svo), c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]),

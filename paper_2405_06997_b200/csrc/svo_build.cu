@@ -360,6 +360,21 @@ __global__ void k_frag_codes(const int32_t* __restrict__ coords, int64_t F,
   }
 }
 
+// Morton codes straight from fp64 points (the compiled quantisation,
+// _kernels.pyx:593-606, then morton3): no int32 coordinate array
+__global__ void k_point_codes(const double* __restrict__ pts, int64_t n, double lox, double loy,
+                              double loz, double scale, int32_t res, uint64_t* __restrict__ codes,
+                              uint32_t* __restrict__ perm) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = (uint32_t)quantise(pts[3 * i], lox, scale, res);
+    const uint32_t y = (uint32_t)quantise(pts[3 * i + 1], loy, scale, res);
+    const uint32_t z = (uint32_t)quantise(pts[3 * i + 2], loz, scale, res);
+    codes[i] = morton3(x, y, z);
+    perm[i] = (uint32_t)i;
+  }
+}
+
 // coarsest level at which fragment i starts a node
 __device__ __forceinline__ int start_level(const uint64_t* __restrict__ codes, int64_t i,
                                            int depth) {
@@ -419,8 +434,10 @@ __global__ void __launch_bounds__(1024) k_lv_offsets(uint32_t* __restrict__ tile
 
 __global__ void k_set_u32(uint32_t* p, uint32_t v) { *p = v; }
 
-// pass 2: write every node from the fragment that starts it (internal
-// nodes' child masks are set by k_internal_normals from their children).
+// pass 2: write every node from the fragment that starts it; each node sets
+// its octant bit in its parent's child mask with a 32-bit atomicOr on the
+// word holding the parent's byte (child_mask zeroed, 4-byte aligned, padded
+// to whole words).
 struct LevelOffs {
   int64_t off[kLvMaxLevels + 1];
 };
@@ -471,11 +488,15 @@ __global__ void __launch_bounds__(kLvBlock) k_lv_emit(
         parent[node] = l == 0 ? -1 : (int32_t)(lo.off[l - 1] + prev_rank - 1);
         if (l == depth) {
           child_base[node] = -1;
-          child_mask[node] = 0;
           leaf_start[rank - 1] = (uint32_t)i;
         }
-        // a node's first child is started by the same fragment
-        if (l > 0 && lv <= l - 1) child_base[lo.off[l - 1] + prev_rank - 1] = (int32_t)node;
+        if (l > 0) {
+          const int64_t p = lo.off[l - 1] + prev_rank - 1;
+          atomicOr(reinterpret_cast<unsigned int*>(child_mask) + (p >> 2),
+                   1u << (8 * (int)(p & 3) + (int)(key & 7u)));
+          // a node's first child is started by the same fragment
+          if (lv <= l - 1) child_base[p] = (int32_t)node;
+        }
       }
       prev_rank = rank;
     }
@@ -501,35 +522,10 @@ extern "C" int wfpg_svo_build_sorted(const void* workspace, int64_t n_fragments,
   return WFPG_OK;
 }
 
-extern "C" int wfpg_svo_build_structure(wfpg_svo* svo, const int32_t* frag_coords,
-                                        int64_t n_fragments, void* workspace, size_t ws_bytes,
-                                        void* stream) {
-  NvtxRange nvtx_("wfpg_svo_build_structure");
-  if (!svo || n_fragments <= 0) {
-    set_error("cannot build an octree from an empty fragment list");
-    return WFPG_ERR_ARG;
-  }
-  if (n_fragments >= (int64_t)INT32_MAX) {
-    set_error("too many fragments");
-    return WFPG_ERR_CAPACITY;
-  }
+// codes (F,) in w.codes, identity in w.perm -> sorted codes, levels, level
+// sizes (the one host read-back)
+static int structure_from_codes(wfpg_svo* svo, int64_t F, BuildWs& w, Arena& a, cudaStream_t st) {
   const int depth = svo->depth;
-  if (depth < 0 || depth >= kLvMaxLevels) {
-    set_error("svo build: depth %d outside [0, %d]", depth, kLvMaxLevels - 1);
-    return WFPG_ERR_ARG;
-  }
-  cudaStream_t st = as_stream(stream);
-  Arena a(workspace, ws_bytes);
-  BuildWs w;
-  carve(a, n_fragments, depth, w);
-  if (!a.ok()) {
-    set_error("svo build: workspace too small");
-    return WFPG_ERR_WORKSPACE;
-  }
-  const int64_t F = n_fragments;
-  const int grid = (int)std::min<int64_t>(ceil_div(F, 256), (int64_t)kNumSMs * 8);
-  k_frag_codes<<<grid, 256, 0, st>>>(frag_coords, F, w.codes, w.perm);
-  WFPG_CHECK_LAUNCH("k_frag_codes");
   {
     size_t mark = a.off;
     WFPG_TRY(sort_pairs(w.codes, w.perm, F, nullptr, std::max(1, 3 * depth), a, st));
@@ -551,6 +547,66 @@ extern "C" int wfpg_svo_build_structure(wfpg_svo* svo, const int32_t* frag_coord
   svo->level_off[depth + 1] = off;
   svo->n_nodes = off;
   return WFPG_OK;
+}
+
+static int structure_args(const wfpg_svo* svo, int64_t n_fragments) {
+  if (!svo || n_fragments <= 0) {
+    set_error("cannot build an octree from an empty fragment list");
+    return WFPG_ERR_ARG;
+  }
+  if (n_fragments >= (int64_t)INT32_MAX) {
+    set_error("too many fragments");
+    return WFPG_ERR_CAPACITY;
+  }
+  if (svo->depth < 0 || svo->depth >= kLvMaxLevels) {
+    set_error("svo build: depth %d outside [0, %d]", svo->depth, kLvMaxLevels - 1);
+    return WFPG_ERR_ARG;
+  }
+  return WFPG_OK;
+}
+
+extern "C" int wfpg_svo_build_structure(wfpg_svo* svo, const int32_t* frag_coords,
+                                        int64_t n_fragments, void* workspace, size_t ws_bytes,
+                                        void* stream) {
+  NvtxRange nvtx_("wfpg_svo_build_structure");
+  WFPG_TRY(structure_args(svo, n_fragments));
+  cudaStream_t st = as_stream(stream);
+  Arena a(workspace, ws_bytes);
+  BuildWs w;
+  carve(a, n_fragments, svo->depth, w);
+  if (!a.ok()) {
+    set_error("svo build: workspace too small");
+    return WFPG_ERR_WORKSPACE;
+  }
+  const int64_t F = n_fragments;
+  const int grid = (int)std::min<int64_t>(ceil_div(F, 256), (int64_t)kNumSMs * 8);
+  k_frag_codes<<<grid, 256, 0, st>>>(frag_coords, F, w.codes, w.perm);
+  WFPG_CHECK_LAUNCH("k_frag_codes");
+  return structure_from_codes(svo, F, w, a, st);
+}
+
+extern "C" int wfpg_svo_build_structure_points(wfpg_svo* svo, const double* points, int64_t n,
+                                               void* workspace, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("wfpg_svo_build_structure_points");
+  WFPG_TRY(structure_args(svo, n));
+  if (!points || svo->resolution != (1 << svo->depth) || !(svo->size > 0.0)) {
+    set_error("wfpg_svo_build_structure_points: bad arguments");
+    return WFPG_ERR_ARG;
+  }
+  cudaStream_t st = as_stream(stream);
+  Arena a(workspace, ws_bytes);
+  BuildWs w;
+  carve(a, n, svo->depth, w);
+  if (!a.ok()) {
+    set_error("svo build: workspace too small");
+    return WFPG_ERR_WORKSPACE;
+  }
+  const double scale = (double)svo->resolution / svo->size;
+  const int grid = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)kNumSMs * 8);
+  k_point_codes<<<grid, 256, 0, st>>>(points, n, svo->lo[0], svo->lo[1], svo->lo[2], scale,
+                                      svo->resolution, w.codes, w.perm);
+  WFPG_CHECK_LAUNCH("k_point_codes");
+  return structure_from_codes(svo, n, w, a, st);
 }
 
 namespace wfpg {
@@ -698,23 +754,13 @@ __global__ void k_leaf_normals(const uint64_t* __restrict__ codes, int64_t leaf_
 
 __global__ void k_internal_normals(const uint64_t* __restrict__ codes, int64_t off, int64_t n,
                                    int level, const int32_t* __restrict__ child_base,
-                                   const int32_t* __restrict__ parent, int64_t kid_end,
-                                   uint8_t* __restrict__ child_mask, uint64_t seed,
+                                   const uint8_t* __restrict__ child_mask, uint64_t seed,
                                    double* __restrict__ normal) {
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
     int64_t node = off + k;
     int64_t base = child_base[node];
-    // children: the run of next-level nodes from child_base whose parent is
-    // this node (at most 8, ending at the next level's end); the child mask
-    // is their octants (svo.py:470-478)
-    int cnt = 0;
-    uint32_t mask = 0;
-    while (cnt < 8 && base + cnt < kid_end && parent[base + cnt] == (int32_t)node) {
-      mask |= 1u << (uint32_t)(codes[base + cnt] & 7u);
-      ++cnt;
-    }
-    child_mask[node] = (uint8_t)mask;
+    const int cnt = __popc((uint32_t)child_mask[node]);
     const double* kid = normal + 3 * base;
     double a0 = fabs(kid[0]), a1 = fabs(kid[1]), a2 = fabs(kid[2]);
     bool same = true;
@@ -814,6 +860,7 @@ extern "C" int wfpg_svo_build_fill(wfpg_svo* svo, const int32_t* frag_tris,
   LevelOffs lo;
   for (int l = 0; l <= depth + 1 && l <= kLvMaxLevels; ++l) lo.off[l] = svo->level_off[l];
   // structure: every node written once by the fragment that starts it
+  WFPG_CUDA(cudaMemsetAsync(svo->child_mask, 0, (size_t)((n + 3) & ~(int64_t)3), st));
   k_lv_emit<<<(unsigned)w.tiles, kLvBlock, 0, st>>>(w.codes, n_fragments, depth, w.tiles,
                                                     w.tile_cnt, lo, svo->codes, svo->parent,
                                                     svo->child_base, svo->child_mask,
@@ -850,9 +897,9 @@ extern "C" int wfpg_svo_build_fill(wfpg_svo* svo, const int32_t* frag_tris,
                                               w.sorted_n, seed, svo->normal);
   WFPG_CHECK_LAUNCH("k_leaf_normals");
   for (int l = depth - 1; l >= 0; --l) {
-    k_internal_normals<<<grid_for(cnt[l]), 128, 0, st>>>(
-        svo->codes, svo->level_off[l], cnt[l], l, svo->child_base, svo->parent,
-        svo->level_off[l + 2], svo->child_mask, seed, svo->normal);
+    k_internal_normals<<<grid_for(cnt[l]), 128, 0, st>>>(svo->codes, svo->level_off[l], cnt[l], l,
+                                                         svo->child_base, svo->child_mask, seed,
+                                                         svo->normal);
     WFPG_CHECK_LAUNCH("k_internal_normals");
   }
   k_node_desc<<<grid_for(n), 256, 0, st>>>(svo->child_base, svo->child_mask, n,

@@ -165,6 +165,10 @@ class SvoCache:
         make = _dev.zeros if zero else _dev.empty
         for name, (_, ddt, comp) in _ARRAYS.items():
             shape = (n, comp) if comp > 1 else (n,)
+            if name == "child_mask":
+                # whole 32-bit words: the build sets mask bits with word atomics
+                d[name] = make((-(-n // 4) * 4,), ddt)[:n]
+                continue
             d[name] = make(shape, ddt)
         d["node_desc"] = make((n, 2), np.uint32)
         # dense index of the top levels: descents start there with one load
@@ -403,11 +407,13 @@ class SvoCache:
         return svo
 
 
-def _build(frag_coords, frag_tris, tri_normals, cube_lo, cube_size, resolution, seed):
+def _build(frag_coords, frag_tris, tri_normals, cube_lo, cube_size, resolution, seed,
+           points=None):
     """Device build from device fragment arrays (int32 coords (F,3), int32
-    tri index (F,), fp64 normals indexed by tri)."""
+    tri index (F,), fp64 normals indexed by tri), or from fp64 points (F,3)
+    quantised on the fly (``points``, frag_coords None)."""
     resolution = _check_resolution(resolution)
-    f = int(frag_coords.shape[0])
+    f = int((frag_coords if points is None else points).shape[0])
     if f == 0:
         raise ValueError("cannot build an octree from an empty fragment list")
     svo = SvoCache(resolution, cube_lo, cube_size)
@@ -415,8 +421,12 @@ def _build(frag_coords, frag_tris, tri_normals, cube_lo, cube_size, resolution, 
     ws = _dev.workspace(lib.wfpg_svo_build_workspace_bytes(f, svo.depth))
     st = _dev.stream()
     s = svo.abi()
-    _lib.call("wfpg_svo_build_structure", _lib.C.byref(s), _lib.ptr(frag_coords), f,
-              _lib.ptr(ws), ws.numel(), st)
+    if points is None:
+        _lib.call("wfpg_svo_build_structure", _lib.C.byref(s), _lib.ptr(frag_coords), f,
+                  _lib.ptr(ws), ws.numel(), st)
+    else:
+        _lib.call("wfpg_svo_build_structure_points", _lib.C.byref(s), _lib.ptr(points), f,
+                  _lib.ptr(ws), ws.numel(), st)
     svo.level_off = np.array([s.level_off[i] for i in range(svo.depth + 2)], dtype=np.int64)
     svo._alloc(svo.node_count, zero=False)
     s = svo.abi()
@@ -478,9 +488,10 @@ def build_from_points(points, normals, cube_lo, cube_size, resolution, seed=0):
     n = int(points.shape[0])
     if n == 0:
         raise ValueError("cannot build an octree from an empty fragment list")
-    coords = quantise_points(points, cube_lo, cube_size, resolution)
+    # codes straight from the points (the quantisation of quantise_points);
     # frag_tris NULL: fragment i's normal is normals[i]
-    return _build(coords, None, normals, cube_lo, cube_size, resolution, seed)
+    return _build(None, None, normals, cube_lo, cube_size, resolution, seed,
+                  points=points.contiguous())
 
 
 def build_from_scene(scene, resolution, seed=0):
