@@ -232,29 +232,97 @@ __device__ void blur_cols_r(double* F, const BlurParams& bp) {
   }
 }
 
+// Sliding-window variants (radius 3, N >= 64): one thread per (mirror pair,
+// 8-output segment), so a segment's 14 inputs per line are loaded once
+// instead of 7 loads per output (the shared-memory pipe was the blur's
+// limiter).  Every thread first reads its window head and right halo (the
+// only positions other threads write), a barrier, then slides in place over
+// its own segment.  Lanes map to consecutive lines (row pass) or columns
+// (column pass), so the padded-row layout keeps every access conflict free.
+// Same taps, same order, same rounding as blur_rows_r / blur_cols_r.
+template <int N>
+__device__ __forceinline__ void blur_rows_sw(double* F, const BlurParams& bp) {
+  constexpr int S = FieldCfg<N>::kStride, L = 8, NP = N / 2;
+  static_assert(NP * (N / L) == FieldCfg<N>::kThreads, "one thread per (pair, segment)");
+  const int t = threadIdx.x;
+  const int j = t % NP, c0 = (t / NP) * L;
+  double* A = F + j * S;
+  double* B = F + (N - 1 - j) * S;
+  double xa[14], xb[14];  // virtual positions c0 - 3 + k
+#pragma unroll
+  for (int k = 0; k < 14; ++k) {
+    if (k >= 7 && k <= 10) continue;  // inside the segment: read after the barrier
+    bool f;
+    const int c = fold_once(c0 - 3 + k, N, &f);
+    xa[k] = f ? B[c] : A[c];
+    xb[k] = f ? A[c] : B[c];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < L; ++q) {
+    if (q >= 1 && q <= 4) {
+      xa[6 + q] = A[c0 + 3 + q];
+      xb[6 + q] = B[c0 + 3 + q];
+    }
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+      a = __dadd_rn(a, __dmul_rn(bp.w[k], xa[q + k]));
+      b = __dadd_rn(b, __dmul_rn(bp.w[k], xb[q + k]));
+    }
+    A[c0 + q] = a;
+    B[c0 + q] = b;
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void blur_cols_sw(double* F, const BlurParams& bp) {
+  constexpr int S = FieldCfg<N>::kStride, L = 8, NP = N / 2;
+  static_assert(NP * (N / L) == FieldCfg<N>::kThreads, "one thread per (pair, segment)");
+  const int t = threadIdx.x;
+  const int i = t % NP, ip = N - 1 - i, r0 = (t / NP) * L;
+  double xa[14], xb[14];  // virtual rows r0 - 3 + k
+#pragma unroll
+  for (int k = 0; k < 14; ++k) {
+    if (k >= 7 && k <= 10) continue;
+    bool f;
+    const int rr = fold_once(r0 - 3 + k, N, &f);
+    const double* row = F + rr * S;
+    xa[k] = f ? row[ip] : row[i];
+    xb[k] = f ? row[i] : row[ip];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < L; ++q) {
+    if (q >= 1 && q <= 4) {
+      const double* row = F + (r0 + 3 + q) * S;
+      xa[6 + q] = row[i];
+      xb[6 + q] = row[ip];
+    }
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+      a = __dadd_rn(a, __dmul_rn(bp.w[k], xa[q + k]));
+      b = __dadd_rn(b, __dmul_rn(bp.w[k], xb[q + k]));
+    }
+    F[(r0 + q) * S + i] = a;
+    F[(r0 + q) * S + ip] = b;
+  }
+}
+
 #ifdef WFPG_FIELD_PHASES
 // phase profiling build: cycles between the phase boundaries of thread 0,
 // summed over bins and CTAs (phase 0 = setup, 1 trace, 2 blur, 3 floor +
 // values, 4 row sums + marginal, 5 prefix sums + stores)
-__device__ unsigned long long g_field_phase[8];
+__device__ unsigned long long g_field_phase[40];  // [log2(N) - 3][phase]
+template <int N>
 __device__ __forceinline__ void ph_mark(int k) {
   static __shared__ long long last;
+  constexpr int row = N == 8 ? 0 : (N == 16 ? 1 : (N == 32 ? 2 : (N == 64 ? 3 : 4)));
   long long now = clock64();
-  if (k > 0) atomicAdd(&g_field_phase[k - 1], (unsigned long long)(now - last));
+  if (k > 0) atomicAdd(&g_field_phase[row * 8 + k - 1], (unsigned long long)(now - last));
   last = now;
 }
-}  // namespace wfpg
-// read (and optionally reset) the phase counters: tools/field_phases.py
-extern "C" int wfpg_debug_field_phases(unsigned long long* out, int reset) {
-  if (cudaMemcpyFromSymbol(out, wfpg::g_field_phase, sizeof(unsigned long long) * 8) != cudaSuccess)
-    return -1;
-  if (reset) {
-    static const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (cudaMemcpyToSymbol(wfpg::g_field_phase, z, sizeof(z)) != cudaSuccess) return -1;
-  }
-  return 0;
-}
-namespace wfpg {
 #endif
 
 // PRODUCT: block sums (+ block row sums) for the product sampler; a separate
@@ -314,12 +382,12 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
   for (; b >= 0;) {
     const double ox = origins[3 * b], oy = origins[3 * b + 1], oz = origins[3 * b + 2];
 #ifdef WFPG_FIELD_PHASES
-    if (threadIdx.x == 0) ph_mark(0);
+    if (threadIdx.x == 0) ph_mark<N>(0);
 #endif
     if (threadIdx.x == 0) tile_ctr = nwarps;
     __syncthreads();
 #ifdef WFPG_FIELD_PHASES
-    if (threadIdx.x == 0) ph_mark(1);
+    if (threadIdx.x == 0) ph_mark<N>(1);
 #endif
     // 1. cone-trace every cell; tiles are handed out dynamically (cull
     // candidates and hit depths vary per tile, static striping left warps
@@ -356,10 +424,21 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
     const int64_t b_next = next_bin;
     if (b_next >= 0) setup(b_next);  // overlaps the blur below
 #ifdef WFPG_FIELD_PHASES
-    if (threadIdx.x == 0) ph_mark(2);
+    if (threadIdx.x == 0) ph_mark<N>(2);
 #endif
     // 2. fold-aware separable blur, horizontal then vertical (core.py:185-195)
-    if (bp.radius == 3 && N > 8) {
+    bool blurred = false;
+    if constexpr (N >= 64) {
+      if (bp.radius == 3) {
+        blur_rows_sw<N>(F, bp);
+        __syncthreads();
+        blur_cols_sw<N>(F, bp);
+        __syncthreads();
+        blurred = true;
+      }
+    }
+    if (blurred) {
+    } else if (bp.radius == 3 && N > 8) {
       blur_rows_r<N, 3>(F, bp);
       __syncthreads();
       blur_cols_r<N, 3>(F, bp);
@@ -371,7 +450,7 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
       __syncthreads();
     }
 #ifdef WFPG_FIELD_PHASES
-    if (threadIdx.x == 0) ph_mark(3);
+    if (threadIdx.x == 0) ph_mark<N>(3);
 #endif
     // 3. epsilon floor + store values (coalesced 16-byte stores)
     double2* gv = reinterpret_cast<double2*>(out.vals + b * (int64_t)N * N);
@@ -386,7 +465,7 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
     }
     __syncthreads();
 #ifdef WFPG_FIELD_PHASES
-    if (threadIdx.x == 0) ph_mark(4);
+    if (threadIdx.x == 0) ph_mark<N>(4);
 #endif
     // 4. row sums (0 + numpy pairwise: 8 strided accumulators combined as
     // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), exact for N in 8..128), 8 lanes
@@ -457,7 +536,7 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
     }
     __syncthreads();
 #ifdef WFPG_FIELD_PHASES
-    if (threadIdx.x == 0) ph_mark(5);
+    if (threadIdx.x == 0) ph_mark<N>(5);
 #endif
     // 5. marginal CDF divisions and the prefix-sum table stores, in parallel
     for (int j = threadIdx.x; j < N; j += blockDim.x) out.marg[b * N + j] = __ddiv_rn(rs[j], tot_sh);
@@ -469,7 +548,7 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
       }
     }
 #ifdef WFPG_FIELD_PHASES
-    if (threadIdx.x == 0) ph_mark(6);
+    if (threadIdx.x == 0) ph_mark<N>(6);
 #endif
     __syncthreads();
     b = b_next;
@@ -769,9 +848,9 @@ extern "C" int wfpg_guide_expand(const wfpg_guide* guide, int64_t n_bins, double
 #ifdef WFPG_FIELD_PHASES
 extern "C" int wfpg_field_phases(unsigned long long* out, int reset) {
   WFPG_CUDA(cudaDeviceSynchronize());
-  WFPG_CUDA(cudaMemcpyFromSymbol(out, wfpg::g_field_phase, sizeof(unsigned long long) * 8));
+  WFPG_CUDA(cudaMemcpyFromSymbol(out, wfpg::g_field_phase, sizeof(unsigned long long) * 40));
   if (reset) {
-    unsigned long long z[8] = {0};
+    unsigned long long z[40] = {0};
     WFPG_CUDA(cudaMemcpyToSymbol(wfpg::g_field_phase, z, sizeof(z)));
   }
   return 0;
