@@ -232,8 +232,8 @@ __device__ void blur_cols_r(double* F, const BlurParams& bp) {
   }
 }
 
-// Sliding-window variants (radius 3, N >= 64): one thread per (mirror pair,
-// 8-output segment), so a segment's 14 inputs per line are loaded once
+// Sliding-window variants (radius 3, N >= 16): one thread per (mirror pair,
+// segment of N^2 / (2 threads) outputs: 8 at N = 64, 128), so a segment's 14 inputs per line are loaded once
 // instead of 7 loads per output (the shared-memory pipe was the blur's
 // limiter).  Every thread first reads its window head and right halo (the
 // only positions other threads write), a barrier, then slides in place over
@@ -242,16 +242,17 @@ __device__ void blur_cols_r(double* F, const BlurParams& bp) {
 // Same taps, same order, same rounding as blur_rows_r / blur_cols_r.
 template <int N>
 __device__ __forceinline__ void blur_rows_sw(double* F, const BlurParams& bp) {
-  constexpr int S = FieldCfg<N>::kStride, L = 8, NP = N / 2;
-  static_assert(NP * (N / L) == FieldCfg<N>::kThreads, "one thread per (pair, segment)");
+  constexpr int S = FieldCfg<N>::kStride, NP = N / 2;
+  constexpr int L = N * NP / FieldCfg<N>::kThreads;  // outputs per thread and line
+  static_assert(NP * (N / L) == FieldCfg<N>::kThreads && L >= 2, "one thread per (pair, segment)");
   const int t = threadIdx.x;
   const int j = t % NP, c0 = (t / NP) * L;
   double* A = F + j * S;
   double* B = F + (N - 1 - j) * S;
-  double xa[14], xb[14];  // virtual positions c0 - 3 + k
+  double xa[L + 6], xb[L + 6];  // virtual positions c0 - 3 + k
 #pragma unroll
-  for (int k = 0; k < 14; ++k) {
-    if (k >= 7 && k <= 10) continue;  // inside the segment: read after the barrier
+  for (int k = 0; k < L + 6; ++k) {
+    if (k >= 7 && k <= L + 2) continue;  // inside the segment: read after the barrier
     bool f;
     const int c = fold_once(c0 - 3 + k, N, &f);
     xa[k] = f ? B[c] : A[c];
@@ -260,7 +261,7 @@ __device__ __forceinline__ void blur_rows_sw(double* F, const BlurParams& bp) {
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < L; ++q) {
-    if (q >= 1 && q <= 4) {
+    if (q >= 1 && q <= L - 4) {
       xa[6 + q] = A[c0 + 3 + q];
       xb[6 + q] = B[c0 + 3 + q];
     }
@@ -277,14 +278,15 @@ __device__ __forceinline__ void blur_rows_sw(double* F, const BlurParams& bp) {
 
 template <int N>
 __device__ __forceinline__ void blur_cols_sw(double* F, const BlurParams& bp) {
-  constexpr int S = FieldCfg<N>::kStride, L = 8, NP = N / 2;
-  static_assert(NP * (N / L) == FieldCfg<N>::kThreads, "one thread per (pair, segment)");
+  constexpr int S = FieldCfg<N>::kStride, NP = N / 2;
+  constexpr int L = N * NP / FieldCfg<N>::kThreads;
+  static_assert(NP * (N / L) == FieldCfg<N>::kThreads && L >= 2, "one thread per (pair, segment)");
   const int t = threadIdx.x;
   const int i = t % NP, ip = N - 1 - i, r0 = (t / NP) * L;
-  double xa[14], xb[14];  // virtual rows r0 - 3 + k
+  double xa[L + 6], xb[L + 6];  // virtual rows r0 - 3 + k
 #pragma unroll
-  for (int k = 0; k < 14; ++k) {
-    if (k >= 7 && k <= 10) continue;
+  for (int k = 0; k < L + 6; ++k) {
+    if (k >= 7 && k <= L + 2) continue;
     bool f;
     const int rr = fold_once(r0 - 3 + k, N, &f);
     const double* row = F + rr * S;
@@ -294,7 +296,7 @@ __device__ __forceinline__ void blur_cols_sw(double* F, const BlurParams& bp) {
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < L; ++q) {
-    if (q >= 1 && q <= 4) {
+    if (q >= 1 && q <= L - 4) {
       const double* row = F + (r0 + 3 + q) * S;
       xa[6 + q] = row[i];
       xb[6 + q] = row[ip];
@@ -428,7 +430,7 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
 #endif
     // 2. fold-aware separable blur, horizontal then vertical (core.py:185-195)
     bool blurred = false;
-    if constexpr (N >= 64) {
+    if constexpr (N >= 16) {
       if (bp.radius == 3) {
         blur_rows_sw<N>(F, bp);
         __syncthreads();
