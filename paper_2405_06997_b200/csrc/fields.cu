@@ -276,8 +276,12 @@ __device__ __forceinline__ void blur_rows_sw(double* F, const BlurParams& bp) {
   }
 }
 
+// The column pass is the blur's last step: it applies the epsilon floor
+// (guiding.py:249) as it writes each output and stores the floored value to
+// the bin's global table row (lanes on consecutive columns: coalesced).
 template <int N>
-__device__ __forceinline__ void blur_cols_sw(double* F, const BlurParams& bp) {
+__device__ __forceinline__ void blur_cols_sw(double* F, const BlurParams& bp, double eps,
+                                             double* __restrict__ gvals) {
   constexpr int S = FieldCfg<N>::kStride, NP = N / 2;
   constexpr int L = N * NP / FieldCfg<N>::kThreads;
   static_assert(NP * (N / L) == FieldCfg<N>::kThreads && L >= 2, "one thread per (pair, segment)");
@@ -307,8 +311,12 @@ __device__ __forceinline__ void blur_cols_sw(double* F, const BlurParams& bp) {
       a = __dadd_rn(a, __dmul_rn(bp.w[k], xa[q + k]));
       b = __dadd_rn(b, __dmul_rn(bp.w[k], xb[q + k]));
     }
+    a = a < eps ? eps : a;
+    b = b < eps ? eps : b;
     F[(r0 + q) * S + i] = a;
     F[(r0 + q) * S + ip] = b;
+    gvals[(r0 + q) * N + i] = a;
+    gvals[(r0 + q) * N + ip] = b;
   }
 }
 
@@ -434,7 +442,7 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
       if (bp.radius == 3) {
         blur_rows_sw<N>(F, bp);
         __syncthreads();
-        blur_cols_sw<N>(F, bp);
+        blur_cols_sw<N>(F, bp, out.eps, out.vals + b * (int64_t)N * N);
         __syncthreads();
         blurred = true;
       }
@@ -454,18 +462,19 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
 #ifdef WFPG_FIELD_PHASES
     if (threadIdx.x == 0) ph_mark<N>(3);
 #endif
-    // 3. epsilon floor + store values (coalesced 16-byte stores)
-    double2* gv = reinterpret_cast<double2*>(out.vals + b * (int64_t)N * N);
-    for (int c = threadIdx.x; c < N * N / 2; c += blockDim.x) {
-      const int j = (2 * c) / N, i = (2 * c) % N;
-      double x0 = F[j * S + i], x1 = F[j * S + i + 1];
-      x0 = x0 < out.eps ? out.eps : x0;
-      x1 = x1 < out.eps ? out.eps : x1;
-      F[j * S + i] = x0;
-      F[j * S + i + 1] = x1;
-      gv[c] = make_double2(x0, x1);
+    // 3. epsilon floor + store values (the sliding blur did both already);
+    // one element per lane: conflict-free on the padded rows
+    if (!blurred) {
+      double* gv = out.vals + b * (int64_t)N * N;
+      for (int e = threadIdx.x; e < N * N; e += blockDim.x) {
+        const int j = e / N, i = e % N;
+        double x = F[j * S + i];
+        x = x < out.eps ? out.eps : x;
+        F[j * S + i] = x;
+        gv[e] = x;
+      }
+      __syncthreads();
     }
-    __syncthreads();
 #ifdef WFPG_FIELD_PHASES
     if (threadIdx.x == 0) ph_mark<N>(4);
 #endif
@@ -473,7 +482,10 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
     // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), exact for N in 8..128), 8 lanes
     // per row, then total / marginal CDF (guiding.py:296-298)
     for (int t = threadIdx.x; t < 8 * N; t += blockDim.x) {
-      const int j = t >> 3, k = t & 7;
+      // 8 lanes per row; the two rows of a 16-lane shared-memory phase are 8
+      // apart (16 banks on the padded rows), so the loads never conflict
+      const int slot = t >> 3, k = t & 7;
+      const int j = N >= 32 ? (slot & ~31) + ((slot & 31) >> 2) + 8 * (slot & 3) : slot;
       const double* row = F + j * S;
       double r = row[k];
       for (int i = k + 8; i < N; i += 8) r = __dadd_rn(r, row[i]);
@@ -543,11 +555,8 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
     // 5. marginal CDF divisions and the prefix-sum table stores, in parallel
     for (int j = threadIdx.x; j < N; j += blockDim.x) out.marg[b * N + j] = __ddiv_rn(rs[j], tot_sh);
     if (out.cum) {
-      double2* gc = reinterpret_cast<double2*>(out.cum + b * (int64_t)N * N);
-      for (int c = threadIdx.x; c < N * N / 2; c += blockDim.x) {
-        const int j = (2 * c) / N, i = (2 * c) % N;
-        gc[c] = make_double2(F[j * S + i], F[j * S + i + 1]);
-      }
+      double* gc = out.cum + b * (int64_t)N * N;
+      for (int e = threadIdx.x; e < N * N; e += blockDim.x) gc[e] = F[(e / N) * S + e % N];
     }
 #ifdef WFPG_FIELD_PHASES
     if (threadIdx.x == 0) ph_mark<N>(6);
