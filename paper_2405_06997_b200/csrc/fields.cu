@@ -418,7 +418,12 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
                          dy, dz, s.ray_eps, &bt, &bid);
       else
         bvh_nearest(s, ox, oy, oz, dx, dy, dz, s.ray_eps, &bt, &bid);
-      if (bid >= 0) cone_shade_hit(v, ox, oy, oz, dx, dy, dz, bt, omega, rgb);
+      if (bid >= 0) {
+        // the origin re-read here (L1) rather than held in registers
+        // through the cull and the triangle tests
+        const double* o3 = origins + 3 * b;
+        cone_shade_hit(v, __ldg(o3), __ldg(o3 + 1), __ldg(o3 + 2), dx, dy, dz, bt, omega, rgb);
+      }
       F[j * S + i] = luminance_rows(rgb[0], rgb[1], rgb[2]);
       int next = 0;
       if (lane == 0) next = atomicAdd(&tile_ctr, 1);
