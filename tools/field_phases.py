@@ -53,18 +53,21 @@ def main():
     wavefront.render_pass(sc, tree, cfg0, [0])
     cfg = wavefront.GuidingConfig(max_depth=4, guided_depths=4, field_res=128, l_min=5,
                                   c_ray=512, seed=0)
-    fn = _lib.load().wfpg_debug_field_phases
-    buf = (ctypes.c_ulonglong * 8)()
+    fn = _lib.load().wfpg_field_phases
+    buf = (ctypes.c_ulonglong * 40)()
     wavefront.render_pass(sc, tree, cfg, [1])
     fn(buf, 1)
     for s in range(a.passes):
         wavefront.render_pass(sc, tree, cfg, [2 + s])
     fn(buf, 0)
-    v = np.array(list(buf)[:6], dtype=np.float64)
-    tot = v.sum()
-    print("| phase | share |\n|---|---|")
-    for n, x in zip(PHASES, v):
-        print(f"| {n} | {100 * x / tot:.1f}% |")
+    v = np.array(list(buf), dtype=np.float64).reshape(5, 8)[:, :6]
+    sizes = [8, 16, 32, 64, 128]
+    print("| phase | " + " | ".join(f"N={n}" for n in sizes) + " |\n|---|" + "---|" * 5)
+    for k, name in enumerate(PHASES):
+        print(f"| {name} | " + " | ".join(
+            f"{100 * v[r, k] / max(v[r].sum(), 1):.1f}%" for r in range(5)) + " |")
+    print("| total Mcycles (thread 0 of every CTA) | " + " | ".join(
+        f"{v[r].sum() / 1e6:.1f}" for r in range(5)) + " |")
 
 
 if __name__ == "__main__":
