@@ -744,13 +744,14 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
         const int32_t* work_n = global ? L.n_need : L.n_bins;
         fo.bin_list = global ? L.need_list : nullptr;
         WFPG_CUDA(cudaMemsetAsync(L.bin_ctr, 0, sizeof(int32_t), st));
-        if (prof) {
-          k_stamp_begin<<<1, 1, 0, st>>>(prof, depth);
-          WFPG_CHECK_LAUNCH("k_stamp_begin");
-        }
         if (!svo_waited) {  // the previous pass's exitance update is complete
           WFPG_TRY(wait_ev(cfg->ev_wait_svo));
           svo_waited = true;
+        }
+        // stamped after the wait, so the field timing is the kernel's alone
+        if (prof) {
+          k_stamp_begin<<<1, 1, 0, st>>>(prof, depth);
+          WFPG_CHECK_LAUNCH("k_stamp_begin");
         }
         WFPG_TRY(launch_fields(sv, vv, L.origins, L.jitters, L.cap, work_n, n, bp, fo, st));
         if (prof) {
