@@ -289,6 +289,12 @@ typedef struct wfpg_pass_config {
   void* ev_wait_svo;
   void* ev_rec_counters;
   void* ev_rec_svo;
+  /* 1: bin only the guided depths (and depth 1 for bin_image).  The
+   * reference bins every depth (wavefront.py:240-256), but the bins of
+   * non-guided depths only feed PassStats (bins / rays / material groups of
+   * those depths then read 0); frames and the SVO are identical either way.
+   * 0 (default): the reference's behaviour. */
+  int32_t skip_unguided_bins;
 } wfpg_pass_config;
 
 /* Per-pass statistics returned to the host: wavefront.py:81-85 (PassStats). */

@@ -96,7 +96,7 @@ class PassConfig(C.Structure):
         ("sample_list", c_vp),
         ("own_bins", c_i32 * 32),
         ("ev_wait_counters", c_vp), ("ev_wait_svo", c_vp),
-        ("ev_rec_counters", c_vp), ("ev_rec_svo", c_vp),
+        ("ev_rec_counters", c_vp), ("ev_rec_svo", c_vp), ("skip_unguided_bins", c_i32),
     ]
 
 

@@ -606,7 +606,12 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
     return WFPG_OK;
   };
   bool counters_waited = false, svo_waited = false;
-  if (!svo) WFPG_TRY(rec_ev(cfg->ev_rec_counters));
+  // the last depth that runs Alg. 2 (records "counters free" after it)
+  const int last_bin_depth =
+      !cfg->skip_unguided_bins
+          ? cfg->max_depth
+          : std::max(std::min(cfg->guided_depths, cfg->max_depth), cfg->bin_image ? 1 : 0);
+  if (!svo || last_bin_depth < 1) WFPG_TRY(rec_ev(cfg->ev_rec_counters));
 
   for (int depth = 1; depth <= cfg->max_depth; ++depth) {
     // live queue (np.nonzero(state.alive), wavefront.py:227)
@@ -631,7 +636,8 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
     GuideView gv{};
     gv.mode = 0;
     const int32_t* slots = nullptr;
-    if (svo) {
+    if (svo && depth <= last_bin_depth &&
+        (!cfg->skip_unguided_bins || depth <= cfg->guided_depths || (depth == 1 && cfg->bin_image))) {
       k_flags_lambert<<<grid, 256, 0, st>>>(sv, L.active, L.n_active, L.hit_tri, P, L.flags,
                                             L.stats->mats[depth]);
       WFPG_CHECK_LAUNCH("k_flags_lambert");
@@ -728,7 +734,7 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
         WFPG_CHECK_LAUNCH("k_bin_setup");
         scratch.off = mark;
       }
-      if (depth == cfg->max_depth) WFPG_TRY(rec_ev(cfg->ev_rec_counters));
+      if (depth == last_bin_depth) WFPG_TRY(rec_ev(cfg->ev_rec_counters));
       if (want_image) {
         int igrid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(L.n_pix, 256), kNumSMs * 8));
         k_bin_image<<<igrid, 256, 0, st>>>(L.bin_slot, L.bin_node, L.n_pix, P / L.n_pix,

@@ -195,7 +195,7 @@ class PassRunner:
 
     def __init__(self, scene, svo, cfg, n_samples=1, deterministic=True, pixel_offset=0,
                  n_pixels=None, leaf_acc=None, use_graph=True, collect_bin_image=False,
-                 comm=None, wire_capacity=0):
+                 comm=None, wire_capacity=0, skip_unguided_bins=False):
         cam = scene.camera
         self.scene = scene
         self.svo = svo
@@ -226,6 +226,9 @@ class PassRunner:
         self.leaf_acc = leaf_acc
         pc.leaf_acc = leaf_acc.data_ptr() if leaf_acc is not None else None
         pc.use_graph = 1 if use_graph else 0  # replay the pass as a CUDA graph
+        # the bins of non-guided depths only feed PassStats: callers that do
+        # not read those stats may skip their Alg. 2 passes (same frames / SVO)
+        pc.skip_unguided_bins = 1 if skip_unguided_bins else 0
         # depth-1 bin node per pixel (wavefront.py:221,254-256)
         self.bin_image = _dev.empty((self.n_pix,), np.int32) if collect_bin_image else None
         pc.bin_image = self.bin_image.data_ptr() if collect_bin_image else None

@@ -48,7 +48,7 @@ def _runners(scene, svo, conf, k=1):
             c = cli._pass_cfg(conf, g)
             if svo is not None:
                 c.l_min = conf.effective_lmin(svo.depth)
-            runners[g] = wavefront.PassRunner(scene, svo, c, k)
+            runners[g] = wavefront.PassRunner(scene, svo, c, k, skip_unguided_bins=True)
         return runners[g]
 
     return lambda i: runner(0 if (pt_first and i == 1) else guided)
@@ -116,6 +116,7 @@ def main():
     ap.add_argument("--ref-file", default=None,
                     help="reuse a reference frame written by --save-ref (same scene/size/depth)")
     ap.add_argument("--guided-depths", type=int, default=4)
+    ap.add_argument("--seed", type=int, default=7, help="seed of the guided and PT runs")
     ap.add_argument("--field-res", type=int, default=128)
     ap.add_argument("--skip-pt", action="store_true", help="guided curve only")
     ap.add_argument("--lmin", type=int, default=5)
@@ -148,10 +149,10 @@ def main():
             np.save(args.save_ref, ref)
     cps = {1 << k for k in range(0, 20)}
     g_conf = cli.RunConfig(path, mode=args.mode, spp=args.spp, depth=args.depth, svo_res=res,
-                           seed=7, guided_depths=min(args.guided_depths, args.depth),
+                           seed=args.seed, guided_depths=min(args.guided_depths, args.depth),
                            field_res=args.field_res, lmin=args.lmin, cray=args.c_ray)
     kpp = args.spp_per_pass
-    p_conf = cli.RunConfig(path, mode="pt", spp=1 << 30, depth=args.depth, seed=7)
+    p_conf = cli.RunConfig(path, mode="pt", spp=1 << 30, depth=args.depth, seed=args.seed)
     # steady-state costs: SVO build, guided pass (on a scratch SVO), PT pass
     cur = torch.cuda.current_stream()
     b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
