@@ -166,12 +166,30 @@ __device__ __forceinline__ void brute_nearest(const TriRec* __restrict__ tris, i
   const float lo = (float)tmin * 0.99999f;
   float hi = 3.0e38f;
   for (int t = 0; t < n; ++t) {
-    if (!slab_maybe(rs, tris[t].blo, tris[t].bhi, lo, hi)) continue;
-    double h = mt_brute(tris[t], ox, oy, oz, dx, dy, dz, tmin);
-    if (h > 0.0 && h < best) hi = __double2float_ru(h) * 1.00001f;
-    if (h > 0.0 && h < best) {  // accepted hits have ts/ad > tmin > 0
-      best = h;
-      id = t;
+    const TriRec& T = tris[t];
+    if (!slab_maybe(rs, T.blo, T.bhi, lo, hi)) continue;
+    // mt_brute's test; the division only on accepting lanes (it used to be
+    // evaluated for every candidate and selected away)
+    double px = dy * T.e2z - dz * T.e2y;
+    double py = dz * T.e2x - dx * T.e2z;
+    double pz = dx * T.e2y - dy * T.e2x;
+    double det = T.e1x * px + T.e1y * py + T.e1z * pz;
+    double sg = det > 0.0 ? 1.0 : -1.0;
+    double ad = det * sg;
+    double tx = ox - T.v0x, ty = oy - T.v0y, tz = oz - T.v0z;
+    double us = (tx * px + ty * py + tz * pz) * sg;
+    double qx = ty * T.e1z - tz * T.e1y;
+    double qy = tz * T.e1x - tx * T.e1z;
+    double qz = tx * T.e1y - ty * T.e1x;
+    double vs = (dx * qx + dy * qy + dz * qz) * sg;
+    double ts = (T.e2x * qx + T.e2y * qy + T.e2z * qz) * sg;
+    if ((ad > 1e-300) & (us >= 0.0) & (vs >= 0.0) & (us + vs <= ad) & (ts > tmin * ad)) {
+      const double h = ts / ad;  // > tmin > 0
+      if (h < best) {
+        best = h;
+        id = t;
+        hi = __double2float_ru(h) * 1.00001f;
+      }
     }
   }
   *bt = best;
