@@ -110,6 +110,7 @@ __device__ __forceinline__ bool slab_maybe(const RaySlab& r, const float* blo, c
 }
 
 constexpr int kMaxBruteTris = 512;
+constexpr int kBoxPrefilterMinTris = 48;
 
 // Cooperative load of the triangle pack into shared memory.
 __device__ __forceinline__ void load_tris_smem(const SceneView& s, TriRec* sm) {
@@ -167,7 +168,10 @@ __device__ __forceinline__ void brute_nearest(const TriRec* __restrict__ tris, i
   float hi = 3.0e38f;
   for (int t = 0; t < n; ++t) {
     const TriRec& T = tris[t];
-    if (!slab_maybe(rs, T.blo, T.bhi, lo, hi)) continue;
+    // the box prefilter pays off from a few dozen triangles on (measured:
+    // 68-triangle C3 +3.5 % with it, 36-triangle Cornell +0.4 % and random
+    // C5 cones +8 % without); same hits either way
+    if (n > kBoxPrefilterMinTris && !slab_maybe(rs, T.blo, T.bhi, lo, hi)) continue;
     // mt_brute's test; the division only on accepting lanes (it used to be
     // evaluated for every candidate and selected away)
     double px = dy * T.e2z - dz * T.e2y;
