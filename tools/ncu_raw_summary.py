@@ -18,15 +18,14 @@ METRICS = [
     ("dram__bytes_write.sum", "DRAM write"),
     ("lts__t_sector_hit_rate.pct", "L2 hit %"),
     ("l1tex__t_sector_hit_rate.pct", "L1 hit %"),
-    ("smsp__average_warp_latency_issue_stalled_long_scoreboard.ratio", "stall long_sb"),
-    ("smsp__average_warp_latency_issue_stalled_barrier.ratio", "stall barrier"),
-    ("smsp__average_warp_latency_issue_stalled_short_scoreboard.ratio", "stall short_sb"),
-    ("smsp__average_warp_latency_issue_stalled_wait.ratio", "stall wait"),
-    ("smsp__average_warp_latency_issue_stalled_math_pipe_throttle.ratio", "stall math"),
-    ("smsp__average_warp_latency_issue_stalled_not_selected.ratio", "stall not_selected"),
-    ("smsp__average_warp_latency_issue_stalled_mio_throttle.ratio", "stall mio"),
-    ("smsp__average_warp_latency_issue_stalled_lg_throttle.ratio", "stall lg"),
-]
+    # warps stalled per issued instruction (ncu 2025 names; older releases
+    # report smsp__average_warp_latency_issue_stalled_*.ratio instead)
+] + [(f"smsp__average_warps_issue_stalled_{k}_per_issue_active.ratio", f"stall {lab} / issue")
+     for k, lab in (("long_scoreboard", "long_sb"), ("short_scoreboard", "short_sb"),
+                    ("wait", "wait"), ("math_pipe_throttle", "math"),
+                    ("not_selected", "not_selected"), ("barrier", "barrier"),
+                    ("mio_throttle", "mio"), ("lg_throttle", "lg"),
+                    ("dispatch_stall", "dispatch"), ("branch_resolving", "branch"))]
 
 
 def load(path):
@@ -48,7 +47,11 @@ def main():
     for key, label in [("Kernel Name", "kernel")] + METRICS:
         cells = []
         for t in tags:
-            v, u = data[t].get(key, ("-", ""))
+            v, u = data[t].get(key, None) or data[t].get(
+                key.replace("average_warps_issue_stalled_", "average_warp_latency_issue_stalled_")
+                   .replace("_per_issue_active", ""), ("-", ""))
+            if "_stalled_" in key:
+                u = ""
             if key == "Kernel Name":
                 v = v.split("(")[0].replace("void wfpg::", "")
                 u = ""
