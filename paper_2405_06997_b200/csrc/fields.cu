@@ -33,6 +33,9 @@ __device__ __forceinline__ int fold_once(int raw, int n, bool* flip) {
   return lo ? -1 - raw : (hi ? 2 * n - 1 - raw : raw);
 }
 
+#ifndef WFPG_SUBCONE_MAX_N
+#define WFPG_SUBCONE_MAX_N 32  // quarter-tile cones in the warp cull (geometry.cuh)
+#endif
 #ifndef WFPG_LANE_TEST_MAX_N
 #define WFPG_LANE_TEST_MAX_N 64
 #endif
@@ -350,6 +353,8 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
              const double* __restrict__ jitters, int64_t nb_max, const int32_t* __restrict__ nb_dev,
              BlurParams bp, FieldOut out) {
   constexpr int S = FieldCfg<N>::kStride;
+  static_assert(N > WFPG_SUBCONE_MAX_N || FieldCfg<N>::kThreads / 32 <= kSubWarps,
+                "quarter-tile cones: one shared slot per warp");
   // warp tiles of 8 (u) x 4 (v) cells: the 32 cones of a warp are angularly
   // coherent, so whole-warp triangle culling is effective
   constexpr int TU = 8, TV = 4, TILES_U = N / TU, TILES = (N / TU) * (N / TV);
@@ -411,8 +416,8 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
       double bt;
       int32_t bid;
       if (TRACE == kTraceBrute)
-        warp_nearest_bin<(N <= WFPG_LANE_TEST_MAX_N)>(tb, s.n_tris, dx, dy, dz, s.ray_eps, &bt,
-                                                       &bid);
+        warp_nearest_bin<(N <= WFPG_LANE_TEST_MAX_N), (N <= WFPG_SUBCONE_MAX_N)>(
+            tb, s.n_tris, dx, dy, dz, s.ray_eps, &bt, &bid);
       else if (TRACE == kTracePacket)
         warp_bvh_nearest(s, reinterpret_cast<int2*>(tb) + warp * kWarpBvhStack, ox, oy, oz, dx,
                          dy, dz, s.ray_eps, &bt, &bid);

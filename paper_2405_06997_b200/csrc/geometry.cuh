@@ -522,11 +522,48 @@ __device__ __forceinline__ double warp_min_d(double x) {
 // triangle order with the strict '<' of the brute-force kernel, so the result
 // (minimum t, lowest id on ties) is brute force over all triangles (the 1e-6
 // slack dwarfs the rounding of both the cull and the hit test).
-template <bool LANE_TEST = false>
+//
+// SUB (small fields, where an 8x4-cell tile spans up to an eighth of the
+// sphere and one bounding cone culls almost nothing): the same test against
+// the four 4x2-cell quarter tiles' cones, a triangle being a candidate when
+// any quarter's cone can reach it (a quarter cone's radius is half the whole
+// tile's).  The quarter cones live in the warp's slot of a small shared
+// table (at most kSubWarps warps per CTA).
+constexpr int kSubWarps = 8;
+template <bool LANE_TEST = false, bool SUB = false>
 __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, int n, double dx,
                                                  double dy, double dz, double tmin, double* bt,
                                                  int32_t* bid) {
   const int lane = threadIdx.x & 31;
+  // quarter tile of a lane (i = lane % 8, j = lane / 8): (i >= 4) + 2 (j >= 2)
+  __shared__ float4 sub_cone[SUB ? kSubWarps : 1][4];  // axis, reach
+  __shared__ float sub_graze[SUB ? kSubWarps : 1][4];
+  if constexpr (SUB) {
+    const int w = threadIdx.x >> 5;
+    const int c = 10 | (lane & 0x14);  // (i, j) = (2, 1) of the lane's quarter
+    const float sx = __shfl_sync(0xffffffffu, (float)dx, c);
+    const float sy = __shfl_sync(0xffffffffu, (float)dy, c);
+    const float sz = __shfl_sync(0xffffffffu, (float)dz, c);
+    const float l2 = sx * sx + sy * sy + sz * sz;
+    const float il = rsqrtf(l2);
+    const float fl = l2 * il;
+    float cq = ((float)dx * sx + (float)dy * sy + (float)dz * sz) * il - 4e-6f;
+    cq = fminf(cq, __shfl_xor_sync(0xffffffffu, cq, 1));
+    cq = fminf(cq, __shfl_xor_sync(0xffffffffu, cq, 2));
+    cq = fminf(cq, __shfl_xor_sync(0xffffffffu, cq, 8));
+    const float s2 = fmaxf(1.0f - cq * cq, 1e-30f);
+    const float g2 = fmaxf(2.0f - 2.0f * cq, 1e-30f);
+    // a quarter that does not fit in a half-space reaches everything
+    const float rch = cq > 0.0f ? -(s2 * rsqrtf(s2) + 1e-5f) * fl : -INFINITY;
+    const float grz = cq > 0.0f ? (g2 * rsqrtf(g2) + 3e-5f) * fl : INFINITY;
+    __syncwarp();
+    if (lane == c) {
+      const int q = ((lane >> 2) & 1) | ((lane >> 3) & 2);
+      sub_cone[w][q] = make_float4(sx, sy, sz, rch);
+      sub_graze[w][q] = grz;
+    }
+    __syncwarp();
+  }
   // axis: the centre lane's direction, broadcast as floats (any common axis is
   // valid).  The tile bound and the plane tests are evaluated in fp32 and
   // widened by 4e-6 (cos) and 1e-5 (sin) — far above fp32 rounding (~1e-7)
@@ -557,7 +594,23 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
   for (int g = 0; g < n; g += 32) {
     const int t = g + lane;
     bool cand = t < n;
-    if (cand && cull) {
+    if (SUB && cand) {
+      const TriBin& B = tb[t];
+      const int w = threadIdx.x >> 5;
+      const bool planes = B.plane_ok[0] & B.plane_ok[1] & B.plane_ok[2];
+      bool any = false;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 A = sub_cone[w][q];
+        const float d0 = A.x * B.n0x + A.y * B.n0y + A.z * B.n0z;
+        const float d1 = A.x * B.n1x + A.y * B.n1y + A.z * B.n1z;
+        const float d2 = A.x * B.n2x + A.y * B.n2y + A.z * B.n2z;
+        const float dp = fabsf(A.x * B.pnx + A.y * B.pny + A.z * B.pnz);
+        const bool inside = (d0 >= A.w) & (d1 >= A.w) & (d2 >= A.w);
+        any |= planes ? inside : (!B.flat | (dp <= sub_graze[w][q]));
+      }
+      cand = any;
+    } else if (cand && cull) {
       // branch-free per lane (each lane holds a different triangle)
       const TriBin& B = tb[t];
       const float d0 = fax * B.n0x + fay * B.n0y + faz * B.n0z;
