@@ -412,8 +412,9 @@ struct __align__(16) TriBin {
   double nx, ny, nz, wx, wy, wz, qx, qy, qz, ts0;
   // unit normals of the three planes through o and an edge, oriented toward
   // the opposite vertex: the triangle's solid angle seen from o is the
-  // intersection of their positive half-spaces.  A degenerate plane (o on
-  // or near the triangle's plane / an edge line) disables the cull.
+  // intersection of their positive half-spaces, so each plane on its own
+  // bounds it.  A degenerate plane (o on or near the triangle's plane / an
+  // edge line) is stored as the zero vector, which every test passes.
   // (fp32: the cull carries a 1e-5 slack, far above their rounding)
   float n0x, n0y, n0z, n1x, n1y, n1z, n2x, n2y, n2z;
   // unit normal of the triangle's own plane; `flat` when o lies within
@@ -421,16 +422,14 @@ struct __align__(16) TriBin {
   // ray can then only hit the triangle beyond tmin if it is within 1e-5 of
   // parallel to the plane, so tiles that stay away from that band skip it
   float pnx, pny, pnz;
-  // per-plane validity, one byte per part so the three builders write
-  // without atomics; the warp culls only when all three are set
-  unsigned char plane_ok[3];
-  unsigned char flat;
+  // 0 when `flat`, +inf otherwise: the grazing-band test is
+  // |a.pn| <= graze + unflat
+  float unflat;
 };
 
 // One third of a triangle's record: part e computes the edge plane through o
 // and edge e (and, for e = 0, the Moeller-Trumbore terms), so three threads
-// build a record.  Degenerate edge planes clear their plane_ok byte; culling
-// applies only when all three are set.
+// build a record.  Degenerate edge planes are left as zero vectors.
 __device__ __forceinline__ void make_tri_bin_part(const SceneView& s, int t, int e, double ox,
                                                   double oy, double oz, TriBin& B) {
   const double* v0 = s.v0 + 3 * t;
@@ -455,7 +454,7 @@ __device__ __forceinline__ void make_tri_bin_part(const SceneView& s, int t, int
     B.pny = (float)(B.ny * inl);
     B.pnz = (float)(B.nz * inl);
     const double fl = 1e-5 * s.ray_eps;
-    B.flat = B.ts0 * B.ts0 < fl * fl * n2 ? 1 : 0;
+    B.unflat = B.ts0 * B.ts0 < fl * fl * n2 ? 0.0f : INFINITY;
   }
   // directions from o to the three vertices (unnormalised: the thresholds
   // below are the unit-vector tests |a^ x b^| > 1e-9 and |n^ . c^| >= 1e-9
@@ -470,7 +469,8 @@ __device__ __forceinline__ void make_tri_bin_part(const SceneView& s, int t, int
     l2[k] = w[k][0] * w[k][0] + w[k][1] * w[k][1] + w[k][2] * w[k][2];
     if (!(l2[k] > dl * dl)) degenerate = true;
   }
-  B.plane_ok[e] = 0;
+  float* nb = &B.n0x + 3 * e;
+  nb[0] = nb[1] = nb[2] = 0.0f;
   if (degenerate) return;
   // the plane through o and edge e, oriented toward the opposite vertex
   const int e1i = (e + 1) % 3, e2i = (e + 2) % 3;
@@ -488,11 +488,9 @@ __device__ __forceinline__ void make_tri_bin_part(const SceneView& s, int t, int
   nx *= inv;
   ny *= inv;
   nz *= inv;
-  float* nb = &B.n0x + 3 * e;
   nb[0] = (float)nx;
   nb[1] = (float)ny;
   nb[2] = (float)nz;
-  B.plane_ok[e] = 1;
 }
 
 // Whole record by one thread.
@@ -597,7 +595,6 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
     if (SUB && cand) {
       const TriBin& B = tb[t];
       const int w = threadIdx.x >> 5;
-      const bool planes = B.plane_ok[0] & B.plane_ok[1] & B.plane_ok[2];
       bool any = false;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -607,7 +604,7 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
         const float d2 = A.x * B.n2x + A.y * B.n2y + A.z * B.n2z;
         const float dp = fabsf(A.x * B.pnx + A.y * B.pny + A.z * B.pnz);
         const bool inside = (d0 >= A.w) & (d1 >= A.w) & (d2 >= A.w);
-        any |= planes ? inside : (!B.flat | (dp <= sub_graze[w][q]));
+        any |= inside & (dp <= sub_graze[w][q] + B.unflat);
       }
       cand = any;
     } else if (cand && cull) {
@@ -617,16 +614,15 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
       const float d1 = fax * B.n1x + fay * B.n1y + faz * B.n1z;
       const float d2 = fax * B.n2x + fay * B.n2y + faz * B.n2z;
       const float dp = fabsf(fax * B.pnx + fay * B.pny + faz * B.pnz);
-      const bool planes = B.plane_ok[0] & B.plane_ok[1] & B.plane_ok[2];
       const bool inside = (d0 >= reach) & (d1 >= reach) & (d2 >= reach);
-      cand = planes ? inside : (!B.flat | (dp <= graze));
+      cand = inside & (dp <= graze + B.unflat);
     }
     unsigned m = __ballot_sync(0xffffffffu, cand);
     while (m) {
       const int k = g + __ffs(m) - 1;
       m &= m - 1;
       const TriBin& B = tb[k];
-      if (LANE_TEST && (B.plane_ok[0] & B.plane_ok[1] & B.plane_ok[2])) {
+      if (LANE_TEST) {
         // each lane's own direction against the three edge planes (fp32,
         // 1e-5 slack): a ray outside the triangle's solid angle cannot hit
         // it, so the warp skips the exact test when no lane is inside
