@@ -53,14 +53,17 @@ __device__ __forceinline__ void cone_shade_hit(const SvoView& v, double ox, doub
   double qx = ox + r * dx - dx * nudge;
   double qy = oy + r * dy - dy * nudge;
   double qz = oz + r * dz - dz * nudge;
-  qx = fmin(fmax(qx, v.clo[0]), v.chi[0]);
-  qy = fmin(fmax(qy, v.clo[1]), v.chi[1]);
-  qz = fmin(fmax(qz, v.clo[2]), v.chi[2]);
-  // q is clamped into [lo + tiny, lo + size - tiny], so (q - lo) * scale lies
-  // in (0, R): the compiled (long) truncation is a plain round-toward-zero
-  int32_t ix = min(__double2int_rz(__dmul_rn(__dsub_rn(qx, v.lox), v.scale)), v.resolution - 1);
-  int32_t iy = min(__double2int_rz(__dmul_rn(__dsub_rn(qy, v.loy), v.scale)), v.resolution - 1);
-  int32_t iz = min(__double2int_rz(__dmul_rn(__dsub_rn(qz, v.loz), v.scale)), v.resolution - 1);
+  // The reference clamps q into [lo + tiny, lo + size - tiny] and truncates
+  // (q - lo) * scale, which lands in [0, R - 1] (tiny * scale = R 1e-12).
+  // Truncation is monotone, so clamping the cell index instead is the same
+  // cell for every q: below lo + tiny the index is <= 0, above
+  // lo + size - tiny it is >= R - 1 (saturating conversion; NaN -> 0, as the
+  // clamp's fmax(NaN, lo + tiny) gives cell 0).  Integer min / max instead
+  // of six fp64 min / max (no DMNMX: compare + two selects each).
+  const int32_t rm = v.resolution - 1;
+  int32_t ix = min(max(__double2int_rz(__dmul_rn(__dsub_rn(qx, v.lox), v.scale)), 0), rm);
+  int32_t iy = min(max(__double2int_rz(__dmul_rn(__dsub_rn(qy, v.loy), v.scale)), 0), rm);
+  int32_t iz = min(max(__double2int_rz(__dmul_rn(__dsub_rn(qz, v.loz), v.scale)), 0), rm);
   int target = best_cone_level(v.size, v.depth, r * r * omega);
   bool pres;
   int32_t lvl;
