@@ -258,7 +258,9 @@ __device__ __forceinline__ void octa_uv_to_dir_cell(double u, double v, double* 
   double r = __dsub_rn(1.0, fabs(sd));
   double t = (r == 0.0) ? 1.0 : fast_div(bp - ap, r) + 1.0;  // phi / (pi/4)
   double rr = __dmul_rn(r, r);
-  double rho = r * fast_sqrt(fmax(2.0 - rr, 1.0));  // 2 - r^2 is in [1, 2]
+  // r = 1 - |1 - (|a| + |b|)| is in [0, 1] for u, v in [0, 1], so
+  // 2 - r^2 is in [1, 2] (no clamp needed)
+  double rho = r * fast_sqrt(2.0 - rr);
   double s, c;
   sincos_quarter_turn(t, &s, &c);
   *ox = __dmul_rn(copysign(c, a), rho);
