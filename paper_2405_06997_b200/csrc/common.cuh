@@ -331,6 +331,7 @@ struct SvoView {
   double scale;        // resolution / size
   double nudge;        // (size / resolution) * 1e-3 (_kernels.pyx:676)
   double clo[3], chi[3];  // lo + size*1e-12, (lo + size) - size*1e-12 (:677-683)
+  float half_log2_s0;     // 0.5 log2(size^2): best_cone_level's estimate (fp32)
   int32_t resolution, depth;
 };
 
@@ -355,6 +356,7 @@ __host__ inline SvoView make_view(const wfpg_svo* s) {
     v.clo[a] = s->lo[a] + tiny;
     v.chi[a] = s->lo[a] + s->size - tiny;
   }
+  v.half_log2_s0 = 0.5f * log2f((float)(s->size * s->size));
   v.resolution = s->resolution;
   v.depth = s->depth;
   return v;

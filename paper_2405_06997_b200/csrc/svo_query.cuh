@@ -13,14 +13,20 @@ namespace wfpg {
 // (size / 2^lv)^2 == round(size * size) * 4^-lv exactly (power-of-two scaling
 // commutes with rounding), so the per-level squares come from one product and
 // exact multiplications by 4 — same bits as the reference's divisions.
-__device__ __forceinline__ int best_cone_level(double size, int depth, double area) {
+__device__ __forceinline__ int best_cone_level(double size, int depth, double area,
+                                               float half_log2_s0) {
   // The error |s0 * 4^-lv - area| falls while s0 * 4^-lv >= area and rises
   // after, so the integer optimum is floor or ceil of x = log4(s0 / area).
   // An fp32 estimate of x (error far below 1) brackets it; the candidates
   // are then compared exactly, deepest first with strict '<' (deeper wins
   // ties), which is what the level-by-level scan from the leaf level returns.
   const double s0 = size * size;
-  const float x = 0.5f * (__log2f((float)s0) - __log2f((float)area));
+  // 0.5 log2(s0) comes with the view; log2(area) by the flush-to-zero MUFU
+  // (area = t^2 omega with t > tmin is never subnormal; if it were, the
+  // estimate would clamp to the deepest level, which is then the answer)
+  float lg;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"((float)area));
+  const float x = half_log2_s0 - 0.5f * lg;
   const float xc = fminf(fmaxf(x, -4.0f), 64.0f);
   const int c = (int)floorf(xc);
   // the integer optimum is floor or ceil of the exact x; the estimate is
@@ -64,7 +70,7 @@ __device__ __forceinline__ void cone_shade_hit(const SvoView& v, double ox, doub
   int32_t ix = min(max(__double2int_rz(__dmul_rn(__dsub_rn(qx, v.lox), v.scale)), 0), rm);
   int32_t iy = min(max(__double2int_rz(__dmul_rn(__dsub_rn(qy, v.loy), v.scale)), 0), rm);
   int32_t iz = min(max(__double2int_rz(__dmul_rn(__dsub_rn(qz, v.loz), v.scale)), 0), rm);
-  int target = best_cone_level(v.size, v.depth, r * r * omega);
+  int target = best_cone_level(v.size, v.depth, r * r * omega, v.half_log2_s0);
   bool pres;
   int32_t lvl;
   int32_t node = descend_view(v, ix, iy, iz, target, &pres, &lvl);
