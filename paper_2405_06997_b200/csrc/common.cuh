@@ -251,8 +251,9 @@ __device__ __forceinline__ void sincos_quarter_turn(double t, double* so, double
 // one division instead of four and no general-argument sincos.
 __device__ __forceinline__ void octa_uv_to_dir_cell(double u, double v, double* ox, double* oy,
                                                     double* oz) {
-  double a = __dsub_rn(__dmul_rn(2.0, u), 1.0);
-  double b = __dsub_rn(__dmul_rn(2.0, v), 1.0);
+  // 2u is exact, so fma(2, u, -1) is the numpy 2u - 1 to the bit
+  double a = __fma_rn(2.0, u, -1.0);
+  double b = __fma_rn(2.0, v, -1.0);
   double ap = fabs(a), bp = fabs(b);
   double sd = __dsub_rn(1.0, __dadd_rn(ap, bp));
   double r = __dsub_rn(1.0, fabs(sd));

@@ -528,6 +528,14 @@ __device__ __forceinline__ double warp_min_d(double x) {
 // tile's).  The quarter cones live in the warp's slot of a small shared
 // table (at most kSubWarps warps per CTA).
 constexpr int kSubWarps = 8;
+// MUFU reciprocal square root without the subnormal-input fixup rsqrtf
+// carries (four extra instructions): every argument below is a normal float
+// (squared lengths of unit vectors, or clamped to >= 1e-30)
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 template <bool LANE_TEST = false, bool SUB = false>
 __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, int n, double dx,
                                                  double dy, double dz, double tmin, double* bt,
@@ -543,7 +551,7 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
     const float sy = __shfl_sync(0xffffffffu, (float)dy, c);
     const float sz = __shfl_sync(0xffffffffu, (float)dz, c);
     const float l2 = sx * sx + sy * sy + sz * sz;
-    const float il = rsqrtf(l2);
+    const float il = rsqrt_ftz(l2);
     const float fl = l2 * il;
     float cq = ((float)dx * sx + (float)dy * sy + (float)dz * sz) * il - 4e-6f;
     cq = fminf(cq, __shfl_xor_sync(0xffffffffu, cq, 1));
@@ -552,8 +560,8 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
     const float s2 = fmaxf(1.0f - cq * cq, 1e-30f);
     const float g2 = fmaxf(2.0f - 2.0f * cq, 1e-30f);
     // a quarter that does not fit in a half-space reaches everything
-    const float rch = cq > 0.0f ? -(s2 * rsqrtf(s2) + 1e-5f) * fl : -INFINITY;
-    const float grz = cq > 0.0f ? (g2 * rsqrtf(g2) + 3e-5f) * fl : INFINITY;
+    const float rch = cq > 0.0f ? -(s2 * rsqrt_ftz(s2) + 1e-5f) * fl : -INFINITY;
+    const float grz = cq > 0.0f ? (g2 * rsqrt_ftz(g2) + 3e-5f) * fl : INFINITY;
     __syncwarp();
     if (lane == c) {
       const int q = ((lane >> 2) & 1) | ((lane >> 3) & 2);
@@ -572,7 +580,7 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
   // (MUFU reciprocal square roots: their ~1e-7 relative error sits far
   // inside the slacks)
   const float fal2 = fax * fax + fay * fay + faz * faz;
-  const float inv_fal = rsqrtf(fal2);
+  const float inv_fal = rsqrt_ftz(fal2);
   const float fal = fal2 * inv_fal;
   float cm = ((float)dx * fax + (float)dy * fay + (float)dz * faz) * inv_fal - 4e-6f;
 #pragma unroll
@@ -581,12 +589,12 @@ __device__ __forceinline__ void warp_nearest_bin(const TriBin* __restrict__ tb, 
   // -|a| (sin(th) + slack): a ray within th of the axis cannot reach the
   // inner side of a plane whose normal n has a.n below this
   const float s2 = fmaxf(1.0f - cm * cm, 1e-30f);
-  const float reach = -(s2 * rsqrtf(s2) + 1e-5f) * fal;
+  const float reach = -(s2 * rsqrt_ftz(s2) + 1e-5f) * fal;
   // every ray of the tile is within 2 sin(th/2) = sqrt(2 - 2 cos th) of the
   // unit axis, so |d.n| >= |a.n| - that: tiles clear of a flat triangle's
   // grazing band (|d.n| <= 1e-5, plus fp32 slack) cannot hit it past tmin
   const float g2 = fmaxf(2.0f - 2.0f * cm, 1e-30f);
-  const float graze = (g2 * rsqrtf(g2) + 3e-5f) * fal;
+  const float graze = (g2 * rsqrt_ftz(g2) + 3e-5f) * fal;
   double best = 1e300;
   int32_t id = -1;
   for (int g = 0; g < n; g += 32) {
