@@ -36,11 +36,17 @@ __device__ __forceinline__ int best_cone_level(double size, int depth, double ar
   const bool safe = fr > 1e-4f && fr < 1.0f - 1e-4f;
   const int lo = min(max(safe ? c : c - 1, 0), depth), hi = min(max(safe ? c + 1 : c + 2, 0), depth);
   // exact power-of-two scaling: s0 * 2^(-2 lv)
+  auto err = [&](int lv) {
+    return fabs(__dmul_rn(s0, __longlong_as_double((long long)(1023 - 2 * lv) << 52)) - area);
+  };
   int best = hi;
-  double bd = fabs(__dmul_rn(s0, __longlong_as_double((long long)(1023 - 2 * hi) << 52)) - area);
+  double bd = err(hi);
+  if (safe) {  // hi - lo <= 1: one more candidate, no loop
+    if (lo < hi && err(lo) < bd) best = lo;
+    return best;
+  }
   for (int lv = hi - 1; lv >= lo; --lv) {
-    const double diff =
-        fabs(__dmul_rn(s0, __longlong_as_double((long long)(1023 - 2 * lv) << 52)) - area);
+    const double diff = err(lv);
     if (diff < bd) {
       bd = diff;
       best = lv;
