@@ -268,9 +268,11 @@ __device__ __forceinline__ void blur_rows_sw(double* F, const BlurParams& bp) {
       xa[6 + q] = A[c0 + 3 + q];
       xb[6 + q] = B[c0 + 3 + q];
     }
-    double a = 0.0, b = 0.0;
+    // numpy's 0 + w0 x0 + ... : the leading 0 + p is p itself (p >= +0:
+    // luminances and Gaussian taps are non-negative, so no -0 to normalise)
+    double a = __dmul_rn(bp.w[0], xa[q]), b = __dmul_rn(bp.w[0], xb[q]);
 #pragma unroll
-    for (int k = 0; k < 7; ++k) {
+    for (int k = 1; k < 7; ++k) {
       a = __dadd_rn(a, __dmul_rn(bp.w[k], xa[q + k]));
       b = __dadd_rn(b, __dmul_rn(bp.w[k], xb[q + k]));
     }
@@ -308,9 +310,11 @@ __device__ __forceinline__ void blur_cols_sw(double* F, const BlurParams& bp, do
       xa[6 + q] = row[i];
       xb[6 + q] = row[ip];
     }
-    double a = 0.0, b = 0.0;
+    // numpy's 0 + w0 x0 + ... : the leading 0 + p is p itself (p >= +0:
+    // luminances and Gaussian taps are non-negative, so no -0 to normalise)
+    double a = __dmul_rn(bp.w[0], xa[q]), b = __dmul_rn(bp.w[0], xb[q]);
 #pragma unroll
-    for (int k = 0; k < 7; ++k) {
+    for (int k = 1; k < 7; ++k) {
       a = __dadd_rn(a, __dmul_rn(bp.w[k], xa[q + k]));
       b = __dadd_rn(b, __dmul_rn(bp.w[k], xb[q + k]));
     }
