@@ -365,11 +365,11 @@ __host__ inline SvoView make_view(const wfpg_svo* s) {
 
 __device__ __forceinline__ int32_t quantise(double p, double lo, double scale, int32_t res) {
   double q = __dmul_rn(__dsub_rn(p, lo), scale);
-  // (long) truncation toward zero, then clamp (_kernels.pyx:594-606)
-  long long qi = (q >= 9.2e18) ? (long long)9.2e18 : (q <= -9.2e18 ? -(long long)9.2e18 : (long long)q);
-  if (qi < 0) qi = 0;
-  if (qi > res - 1) qi = res - 1;
-  return (int32_t)qi;
+  // (long) truncation toward zero, then clamp to [0, res - 1]
+  // (_kernels.pyx:594-606).  The saturating 32-bit conversion gives the same
+  // clamped cell for every q: out-of-range values saturate to the side they
+  // clamp to anyway, NaN converts to 0 as the 64-bit path did.
+  return min(max(__double2int_rz(q), 0), res - 1);
 }
 
 // Descend toward leaf coords (qx,qy,qz) through at most `max_level` levels.
