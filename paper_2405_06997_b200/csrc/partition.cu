@@ -190,7 +190,7 @@ size_t partition_ws_bytes(int64_t n) {
   int64_t m = n > 0 ? n : 1;
   return align_up(4 * m) + align_up(1 * m) + align_up(8 * m) + align_up(4 * m) +
          align_up(4 * (m + 1)) + align_up(4 * (m + 1)) + align_up(8) +
-         std::max(sort_ws_bytes(m), scan_ws_bytes(m + 1)) + 4096;
+         sort_ws_bytes(m) + scan_ws_bytes(m + 1) + 4096;  // the sorted pairs may live in the sort's workspace
 }
 
 int partition_spatial(const SvoView& v, int32_t* counter, const int32_t* parent,
@@ -235,11 +235,10 @@ int partition_spatial(const SvoView& v, int32_t* counter, const int32_t* parent,
     k_part_clear<<<grid, 256, 0, st>>>(counter, parent, start, lev, n_max, n_dev, l_min);
     WFPG_CHECK_LAUNCH("k_part_clear");
   }
-  {
-    size_t mark = ws.off;
-    WFPG_TRY(sort_pairs(keys, vals, n_max, n_dev, bits_for((uint64_t)n_nodes), ws, st));
-    ws.off = mark;
-  }
+  // the result stays where the last pass wrote it (no copy-back); that
+  // workspace is kept for the rest of the partition
+  WFPG_TRY(sort_pairs_nocopy(keys, vals, n_max, n_dev, bits_for((uint64_t)n_nodes), ws, st,
+                             &keys, &vals));
   k_part_flags<<<grid, 256, 0, st>>>(keys, n_max, n_dev, flags);
   WFPG_CHECK_LAUNCH("k_part_flags");
   {

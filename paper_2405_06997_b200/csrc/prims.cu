@@ -291,9 +291,15 @@ size_t sort_ws_bytes(int64_t n_max) {
          align_up(sizeof(uint32_t) * kCsMaxRadix) + 1024;
 }
 
+// kres / vres (optional): report the buffers that hold the result instead of
+// copying it back into keys / vals after an odd number of passes (the
+// caller then keeps the workspace taken here alive while it reads them)
 template <typename KT>
 static int sort_pairs_t(KT* keys, uint32_t* vals, int64_t n_max, const int32_t* n_dev, int key_bits,
-                        Arena& ws, cudaStream_t st) {
+                        Arena& ws, cudaStream_t st, KT** kres = nullptr,
+                        uint32_t** vres = nullptr) {
+  if (kres) *kres = keys;
+  if (vres) *vres = vals;
   if (n_max <= 1) return WFPG_OK;
   if (n_max >= (int64_t)UINT32_MAX) {
     set_error("sort: %lld items exceed the 32-bit index range", (long long)n_max);
@@ -341,7 +347,10 @@ static int sort_pairs_t(KT* keys, uint32_t* vals, int64_t n_max, const int32_t* 
     va = vb;
     vb = tv;
   }
-  if (ka != keys) {
+  if (kres && vres) {
+    *kres = ka;
+    *vres = va;
+  } else if (ka != keys) {
     // odd number of passes: copy the live prefix back
     int cgrid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_max, 256), kNumSMs * 8));
     k_copy_pairs<KT><<<cgrid, 256, 0, st>>>(ka, va, keys, vals, n_max, n_dev);
@@ -358,6 +367,12 @@ int sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n_max, const int32_t* n_d
 int sort_pairs(uint32_t* keys, uint32_t* vals, int64_t n_max, const int32_t* n_dev, int key_bits,
                Arena& ws, cudaStream_t st) {
   return sort_pairs_t(keys, vals, n_max, n_dev, key_bits < 32 ? key_bits : 32, ws, st);
+}
+int sort_pairs_nocopy(uint32_t* keys, uint32_t* vals, int64_t n_max, const int32_t* n_dev,
+                      int key_bits, Arena& ws, cudaStream_t st, uint32_t** kres,
+                      uint32_t** vres) {
+  return sort_pairs_t(keys, vals, n_max, n_dev, key_bits < 32 ? key_bits : 32, ws, st, kres,
+                      vres);
 }
 
 }  // namespace wfpg

@@ -16,6 +16,12 @@ int sort_pairs(uint64_t* keys, uint32_t* vals, int64_t n_max, const int32_t* n_d
                int key_bits, Arena& ws, cudaStream_t st);
 int sort_pairs(uint32_t* keys, uint32_t* vals, int64_t n_max, const int32_t* n_dev,
                int key_bits, Arena& ws, cudaStream_t st);
+// Same sort without the copy-back after an odd pass count: *kres / *vres
+// name the buffers holding the result (keys / vals or workspace taken from
+// ws, which the caller must not release while it reads them).
+int sort_pairs_nocopy(uint32_t* keys, uint32_t* vals, int64_t n_max, const int32_t* n_dev,
+                      int key_bits, Arena& ws, cudaStream_t st, uint32_t** kres,
+                      uint32_t** vres);
 
 inline int bits_for(uint64_t max_value) {
   int b = 0;
