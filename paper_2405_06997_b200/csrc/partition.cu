@@ -14,10 +14,15 @@
 
 namespace wfpg {
 
+// chain_out (optional, (n_chain, n_max)): row c holds the item's ancestor c
+// levels above its start node, for the levels above l_min (at most n_chain),
+// so the ascent loads them all at once instead of walking parent links one
+// dependent load at a time
 __global__ void k_part_count(SvoView v, int32_t* __restrict__ counter,
                              const double* __restrict__ pos, int64_t n_max,
                              const int32_t* __restrict__ n_dev, int l_min,
-                             int32_t* __restrict__ start, int8_t* __restrict__ start_lev) {
+                             int32_t* __restrict__ start, int8_t* __restrict__ start_lev,
+                             int32_t* __restrict__ chain_out, int n_chain) {
   const int64_t n = dev_count(n_max, n_dev);
   const int lane = threadIdx.x & 31;
   // whole warps iterate together so the counter updates can be aggregated:
@@ -57,6 +62,9 @@ __global__ void k_part_count(SvoView v, int32_t* __restrict__ counter,
       }
       start[i] = node;
       start_lev[i] = (int8_t)lvl;
+      if (chain_out)
+        for (int c = 0; c < n_chain && lvl - c > l_min; ++c)
+          chain_out[(int64_t)c * n_max + i] = chain[lvl - c];
     }
     int top = valid ? lvl : 0;
 #pragma unroll
@@ -93,6 +101,55 @@ __global__ void k_part_count_chain(int32_t* __restrict__ counter, const int32_t*
       if (a >= 0 && lane == __ffs(grp) - 1) atomicAdd(&counter[a], __popc(grp));
       if (a >= 0) cur = __ldg(&parent[a]);
     }
+  }
+}
+
+// k_part_ascend with the stored chains: the chain entries, then their
+// counters, each as independent loads; the deepest marked level wins as in
+// the walk (a level-l_min node is marked regardless: one parent link from
+// level l_min + 1, or the start node itself when it sits at l_min).
+constexpr int kAscendMax = 16;
+__global__ void k_part_ascend_chain(const int32_t* __restrict__ counter,
+                                    const int32_t* __restrict__ parent,
+                                    const int32_t* __restrict__ start,
+                                    const int8_t* __restrict__ start_lev,
+                                    const int32_t* __restrict__ chain, int n_chain,
+                                    int64_t n_max, const int32_t* __restrict__ n_dev, int l_min,
+                                    int c_ray, uint32_t* __restrict__ keys,
+                                    uint32_t* __restrict__ vals) {
+  const int64_t n = dev_count(n_max, n_dev);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int lev = start_lev[i];
+    const int m = min(lev - l_min, n_chain);  // stored levels lev .. lev - m + 1
+    int32_t node[kAscendMax];
+#pragma unroll
+    for (int c = 0; c < kAscendMax; ++c)
+      if (c < m) node[c] = __ldg(&chain[(int64_t)c * n_max + i]);
+    int32_t cnt[kAscendMax];
+#pragma unroll
+    for (int c = 0; c < kAscendMax; ++c)
+      if (c < m) cnt[c] = counter[node[c]];
+    int32_t a = start[i];
+    int l = lev;
+    bool found = lev <= l_min;
+#pragma unroll
+    for (int c = 0; c < kAscendMax; ++c)
+      if (!found && c < m) {
+        a = node[c];
+        l = lev - c;
+        found = cnt[c] >= c_ray;
+      }
+    if (!found) {
+      // past the stored levels (deeper than kAscendMax above l_min) or
+      // nothing marked above l_min: continue with the parent walk
+      while (l > l_min && counter[a] < c_ray) {
+        a = parent[a];
+        --l;
+      }
+    }
+    keys[i] = (uint32_t)a;
+    vals[i] = (uint32_t)i;
   }
 }
 
@@ -186,10 +243,12 @@ __global__ void k_part_counts(const int32_t* __restrict__ bin_start, const uint3
   }
 }
 
-size_t partition_ws_bytes(int64_t n) {
+size_t partition_ws_bytes(int64_t n, int chain_levels) {
   int64_t m = n > 0 ? n : 1;
+  const int k = std::max(0, std::min(chain_levels, kAscendMax));
   return align_up(4 * m) + align_up(1 * m) + align_up(8 * m) + align_up(4 * m) +
          align_up(4 * (m + 1)) + align_up(4 * (m + 1)) + align_up(8) +
+         (k ? align_up(4 * m * k) : 0) +
          sort_ws_bytes(m) + scan_ws_bytes(m + 1) + 4096;  // the sorted pairs may live in the sort's workspace
 }
 
@@ -213,6 +272,19 @@ int partition_spatial(const SvoView& v, int32_t* counter, const int32_t* parent,
     set_error("partition: workspace too small");
     return WFPG_ERR_WORKSPACE;
   }
+  // stored ancestor chains for the ascent, when the workspace has room for
+  // them next to the sort and the scan (else the parent walk)
+  int n_chain = given ? 0 : std::min(kAscendMax, v.depth - l_min);
+  int32_t* chain = nullptr;
+  if (n_chain > 0) {
+    const size_t mark = ws.off;
+    chain = ws.take<int32_t>((int64_t)n_chain * n_max);
+    if (ws.off + sort_ws_bytes(n_max) + scan_ws_bytes(n_max + 1) > ws.cap) {
+      ws.off = mark;
+      chain = nullptr;
+      n_chain = 0;
+    }
+  }
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_max, 256), kNumSMs * 8));
   if (given) {
     if (!start || !lev) {
@@ -222,12 +294,19 @@ int partition_spatial(const SvoView& v, int32_t* counter, const int32_t* parent,
     k_part_count_chain<<<grid, 256, 0, st>>>(counter, parent, start, lev, n_max, n_dev, l_min);
     WFPG_CHECK_LAUNCH("k_part_count_chain");
   } else {
-    k_part_count<<<grid, 256, 0, st>>>(v, counter, pos, n_max, n_dev, l_min, start, lev);
+    k_part_count<<<grid, 256, 0, st>>>(v, counter, pos, n_max, n_dev, l_min, start, lev, chain,
+                                       n_chain);
     WFPG_CHECK_LAUNCH("k_part_count");
   }
-  k_part_ascend<<<grid, 256, 0, st>>>(counter, parent, start, lev, n_max, n_dev, l_min, c_ray,
-                                      keys, vals);
-  WFPG_CHECK_LAUNCH("k_part_ascend");
+  if (chain) {
+    k_part_ascend_chain<<<grid, 256, 0, st>>>(counter, parent, start, lev, chain, n_chain, n_max,
+                                              n_dev, l_min, c_ray, keys, vals);
+    WFPG_CHECK_LAUNCH("k_part_ascend_chain");
+  } else {
+    k_part_ascend<<<grid, 256, 0, st>>>(counter, parent, start, lev, n_max, n_dev, l_min, c_ray,
+                                        keys, vals);
+    WFPG_CHECK_LAUNCH("k_part_ascend");
+  }
   if (out.clear_from >= 0 && out.clear_from <= n_nodes) {
     WFPG_CUDA(cudaMemsetAsync(counter + out.clear_from, 0,
                               sizeof(int32_t) * (size_t)(n_nodes - out.clear_from), st));

@@ -27,7 +27,9 @@ struct PartitionOut {
   int32_t* need = nullptr;
 };
 
-size_t partition_ws_bytes(int64_t n);
+// chain_levels: ancestor levels above l_min stored for the ascent (the SVO
+// depth minus l_min; capped at 16 inside)
+size_t partition_ws_bytes(int64_t n, int chain_levels = 16);
 int partition_spatial(const SvoView& v, int32_t* counter, const int32_t* parent,
                       const double* pos, const int32_t* path_idx, int64_t n_max,
                       const int32_t* n_dev, int l_min, int c_ray, int n_nodes,

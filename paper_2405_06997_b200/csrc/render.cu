@@ -505,10 +505,13 @@ static void carve_pass(Arena& a, const wfpg_svo* svo, const wfpg_camera* cam,
     for (int d = 0; d <= kMaxDepth; ++d) L.own_seg[d] = 0;
   }
   L.scratch_off = a.off;
-  size_t scratch = std::max(scan_ws_bytes(P + 1), partition_ws_bytes(P));
+  // the local partition stores each hit's ancestor chain above l_min for
+  // the ascent; the global one (start nodes given) does not
+  const int chain_levels = svo ? std::max(0, svo->depth - cfg->l_min) : 0;
+  size_t scratch = std::max(scan_ws_bytes(P + 1), partition_ws_bytes(P, chain_levels));
   if (multi) {
     const int64_t G = L.seg * L.world;
-    scratch = std::max(scratch, std::max(scan_ws_bytes(G + 1), partition_ws_bytes(G)));
+    scratch = std::max(scratch, std::max(scan_ws_bytes(G + 1), partition_ws_bytes(G, 0)));
     scratch = std::max(scratch, accumulate_ws_bytes(L.wire_cap * L.world) + 4096);
     scratch = std::max(scratch, 2 * align_up(4 * (G + 1)) + scan_ws_bytes(G + 1) + 4096);
   }
