@@ -424,7 +424,10 @@ __global__ void __launch_bounds__(FieldCfg<N>::kThreads, FieldCfg<N>::kMinBlocks
             tb, s.n_tris, dx, dy, dz, s.ray_eps, &bt, &bid);
       else if (TRACE == kTracePacket)
         warp_bvh_nearest(s, reinterpret_cast<int2*>(tb) + warp * kWarpBvhStack, ox, oy, oz, dx,
-                         dy, dz, s.ray_eps, &bt, &bid);
+                         dy, dz, s.ray_eps, &bt, &bid,
+                         reinterpret_cast<double*>(reinterpret_cast<int2*>(tb) +
+                                                   nwarps * kWarpBvhStack) +
+                             warp * kLeafStage * kLeafRec);
       else
         bvh_nearest(s, ox, oy, oz, dx, dy, dz, s.ray_eps, &bt, &bid);
       if (bid >= 0) {
@@ -587,7 +590,8 @@ static int launch_fields_n_(const SceneView& s, const SvoView& v, const double* 
   constexpr int T = FieldCfg<N>::kThreads;
   size_t smem = sizeof(double) * (N * FieldCfg<N>::kStride + 3 * N) +
                 (TRACE == kTraceBrute ? sizeof(TriBin) * s.n_tris
-                 : TRACE == kTracePacket ? sizeof(int2) * kWarpBvhStack * (T / 32)  // warp stacks
+                 : TRACE == kTracePacket ? (sizeof(int2) * kWarpBvhStack +  // warp stacks,
+                                            sizeof(double) * kLeafStage * kLeafRec) * (T / 32)  // leaf records
                                          : 0);
   static size_t configured = 0;
   if (smem > configured) {

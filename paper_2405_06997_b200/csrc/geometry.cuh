@@ -705,6 +705,10 @@ __device__ __forceinline__ bool brute_occluded(const TriRec* __restrict__ tris, 
 // Rays of a field tile span a few degrees, so the packet visits about the
 // nodes one ray visits, without the per-lane divergence of 32 separate walks.
 constexpr int kWarpBvhStack = 64;
+// per-warp staging of a leaf's per-(origin, triangle) Moeller-Trumbore terms
+// (the TriBin terms: n = e2 x e1, w = e2 x tvec, q = tvec x e1, ts0 = e2.q,
+// plus the triangle id): kLeafStage records of kLeafRec doubles
+constexpr int kLeafStage = 8, kLeafRec = 12;
 
 __device__ __forceinline__ bool slab32_reach(const float4* box, const RaySlab& r, float lo,
                                              float hi) {
@@ -717,7 +721,8 @@ __device__ __forceinline__ bool slab32_reach(const float4* box, const RaySlab& r
 __device__ __forceinline__ void warp_bvh_nearest(const SceneView& b, int2* __restrict__ wstack,
                                                  double ox, double oy, double oz, double dx,
                                                  double dy, double dz, double tmin,
-                                                 double* best_t, int32_t* best_tri) {
+                                                 double* best_t, int32_t* best_tri,
+                                                 double* __restrict__ wrec = nullptr) {
   const int lane = threadIdx.x & 31;
   const unsigned me = 1u << lane;
   const RaySlab rs = make_ray_slab(ox, oy, oz, dx, dy, dz);
@@ -731,7 +736,59 @@ __device__ __forceinline__ void warp_bvh_nearest(const SceneView& b, int2* __res
   while (mask) {
     const int32_t cnt = __ldg(&b.bcount[node]);
     const int32_t c0 = __ldg(&b.bleft[node]);
-    if (cnt > 0) {
+    if (cnt > 0 && wrec) {
+      // the warp's rays share one origin (a field bin): lanes build the
+      // leaf's direction-linear triangle terms once, then every lane in the
+      // mask tests its own direction with three dot products per triangle
+      for (int32_t k0 = 0; k0 < cnt; k0 += kLeafStage) {
+        const int kn = cnt - k0 < kLeafStage ? cnt - k0 : kLeafStage;
+        __syncwarp();
+        if (lane < kn) {
+          const int32_t tri = __ldg(&b.border[c0 + k0 + lane]);
+          const double* v0 = b.v0 + 3 * tri;
+          const double* e1 = b.e1 + 3 * tri;
+          const double* e2 = b.e2 + 3 * tri;
+          const double e1x = __ldg(e1), e1y = __ldg(e1 + 1), e1z = __ldg(e1 + 2);
+          const double e2x = __ldg(e2), e2y = __ldg(e2 + 1), e2z = __ldg(e2 + 2);
+          const double tx = ox - __ldg(v0), ty = oy - __ldg(v0 + 1), tz = oz - __ldg(v0 + 2);
+          double* r = wrec + lane * kLeafRec;
+          const double qx = ty * e1z - tz * e1y, qy = tz * e1x - tx * e1z, qz = tx * e1y - ty * e1x;
+          r[0] = e2y * e1z - e2z * e1y;
+          r[1] = e2z * e1x - e2x * e1z;
+          r[2] = e2x * e1y - e2y * e1x;
+          r[3] = e2y * tz - e2z * ty;
+          r[4] = e2z * tx - e2x * tz;
+          r[5] = e2x * ty - e2y * tx;
+          r[6] = qx;
+          r[7] = qy;
+          r[8] = qz;
+          r[9] = e2x * qx + e2y * qy + e2z * qz;
+          r[10] = __longlong_as_double((long long)tri);
+        }
+        __syncwarp();
+        if (mask & me) {
+          for (int k = 0; k < kn; ++k) {
+            const double* r = wrec + k * kLeafRec;
+            const double det = dx * r[0] + dy * r[1] + dz * r[2];
+            const double sg = det > 0.0 ? 1.0 : -1.0;
+            const double ad = det * sg;
+            const double us = (dx * r[3] + dy * r[4] + dz * r[5]) * sg;
+            const double vs = (dx * r[6] + dy * r[7] + dz * r[8]) * sg;
+            const double ts = r[9] * sg;
+            if ((ad > 1e-300) & (us >= 0.0) & (vs >= 0.0) & (us + vs <= ad) &
+                (ts > tmin * ad) & (ts < bt * ad)) {
+              const double h = ts / ad;
+              if (h < bt) {
+                bt = h;
+                bid = (int32_t)__double_as_longlong(r[10]);
+              }
+            }
+          }
+          hi = bt < 1e300 ? __double2float_ru(bt) * (1.0f + 1e-6f) : hi;
+        }
+      }
+      mask = 0;
+    } else if (cnt > 0) {
       if (mask & me) {
         for (int32_t k = c0; k < c0 + cnt; ++k) {
           const int32_t tri = __ldg(&b.border[k]);
