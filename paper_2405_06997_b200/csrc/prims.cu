@@ -19,6 +19,10 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_reduce(const uint32_t* __re
   __shared__ uint32_t sw[kScanBlock / 32 + 1];
   const int64_t n = dev_count(n_max, n_dev);
   const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  if (base >= n) {  // past the live count (grids are sized for n_max): uniform exit
+    if (threadIdx.x == 0) partial[blockIdx.x] = 0;
+    return;
+  }
   uint32_t s = 0;
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
@@ -53,21 +57,38 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_tiles(const uint32_t* in, u
   __shared__ uint32_t sw[kScanBlock / 32 + 1];
   const int64_t n = dev_count(n_max, n_dev);
   const int64_t base = (int64_t)blockIdx.x * kScanTile;
-  // blocked arrangement: thread t owns items base + t*ITEMS .. +ITEMS-1
+  if (base >= n) return;  // uniform: nothing live in this tile
+  // blocked arrangement: thread t owns items base + t*ITEMS .. +ITEMS-1,
+  // loaded / stored as one 16-byte vector when all four are live and the
+  // arrays are 16-byte aligned (a warp then moves 512 contiguous bytes)
+  static_assert(kScanItems == 4, "uint4 vectors");
+  const int64_t i0 = base + (int64_t)threadIdx.x * kScanItems;
+  const bool vec = i0 + kScanItems <= n &&
+                   ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
   uint32_t v[kScanItems];
-  uint32_t s = 0;
+  if (vec) {
+    const uint4 q = *reinterpret_cast<const uint4*>(in + i0);
+    v[0] = q.x;
+    v[1] = q.y;
+    v[2] = q.z;
+    v[3] = q.w;
+  } else {
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    int64_t i = base + (int64_t)threadIdx.x * kScanItems + k;
-    v[k] = i < n ? in[i] : 0;
-    s += v[k];
+    for (int k = 0; k < kScanItems; ++k) v[k] = i0 + k < n ? in[i0 + k] : 0;
   }
-  uint32_t ex = block_exclusive_scan<kScanBlock>(s, sw, nullptr) + partial[blockIdx.x];
+  const uint32_t s = v[0] + v[1] + v[2] + v[3];
+  const uint32_t ex = block_exclusive_scan<kScanBlock>(s, sw, nullptr) + partial[blockIdx.x];
+  uint32_t o[kScanItems];
+  o[0] = ex;
+  o[1] = o[0] + v[0];
+  o[2] = o[1] + v[1];
+  o[3] = o[2] + v[2];
+  if (vec) {
+    *reinterpret_cast<uint4*>(out + i0) = make_uint4(o[0], o[1], o[2], o[3]);
+  } else {
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    int64_t i = base + (int64_t)threadIdx.x * kScanItems + k;
-    if (i < n) out[i] = ex;
-    ex += v[k];
+    for (int k = 0; k < kScanItems; ++k)
+      if (i0 + k < n) out[i0 + k] = o[k];
   }
 }
 
