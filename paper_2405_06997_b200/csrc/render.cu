@@ -55,6 +55,19 @@ __global__ void k_flags_alive(const uint8_t* __restrict__ alive, int64_t n,
     flags[i] = alive[i] ? 1u : 0u;
 }
 
+// depth 1: every path was just initialised alive, so the live queue is the
+// identity (no flags / scan / scatter)
+__global__ void k_active_all(int64_t n, int32_t* __restrict__ active, int32_t* __restrict__ n_out,
+                             int32_t* __restrict__ stat) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    active[i] = (int32_t)i;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *n_out = (int32_t)n;
+    *stat = (int32_t)n;
+  }
+}
+
 __global__ void k_scatter_alive(const uint32_t* __restrict__ flags,
                                 const uint32_t* __restrict__ scan, int64_t n,
                                 int32_t* __restrict__ active, const uint32_t* __restrict__ total,
@@ -618,16 +631,21 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
 
   for (int depth = 1; depth <= cfg->max_depth; ++depth) {
     // live queue (np.nonzero(state.alive), wavefront.py:227)
-    k_flags_alive<<<grid, 256, 0, st>>>(paths->alive, P, L.flags);
-    WFPG_CHECK_LAUNCH("k_flags_alive");
-    {
-      size_t mark = scratch.off;
-      WFPG_TRY(scan_u32(L.flags, L.scan, P, nullptr, L.total, scratch, st));
-      scratch.off = mark;
+    if (depth == 1) {
+      k_active_all<<<grid, 256, 0, st>>>(P, L.active, L.n_active, &L.stats->live[depth]);
+      WFPG_CHECK_LAUNCH("k_active_all");
+    } else {
+      k_flags_alive<<<grid, 256, 0, st>>>(paths->alive, P, L.flags);
+      WFPG_CHECK_LAUNCH("k_flags_alive");
+      {
+        size_t mark = scratch.off;
+        WFPG_TRY(scan_u32(L.flags, L.scan, P, nullptr, L.total, scratch, st));
+        scratch.off = mark;
+      }
+      k_scatter_alive<<<grid, 256, 0, st>>>(L.flags, L.scan, P, L.active, L.total, L.n_active,
+                                            &L.stats->live[depth]);
+      WFPG_CHECK_LAUNCH("k_scatter_alive");
     }
-    k_scatter_alive<<<grid, 256, 0, st>>>(L.flags, L.scan, P, L.active, L.total, L.n_active,
-                                          &L.stats->live[depth]);
-    WFPG_CHECK_LAUNCH("k_scatter_alive");
     if (depth == 1 && sv.brute) {  // primary rays share the camera position
       WFPG_TRY(launch_intersect_origin(sv, cam->position, paths->ray_d, L.active, P, L.n_active,
                                        scene->ray_eps, L.hit_t, L.hit_tri, st));
