@@ -48,11 +48,31 @@ __global__ void k_bin_image(const int32_t* __restrict__ bin_slot,
   }
 }
 
-__global__ void k_flags_alive(const uint8_t* __restrict__ alive, int64_t n,
-                              uint32_t* __restrict__ flags) {
+// depth >= 2: the live queue compacted from the previous depth's queue (the
+// only paths that can still be alive), in the same path order
+__global__ void k_flags_alive_list(const uint8_t* __restrict__ alive,
+                                   const int32_t* __restrict__ prev, int64_t n_max,
+                                   const int32_t* __restrict__ n_dev, uint32_t* __restrict__ flags) {
+  const int64_t n = dev_count(n_max, n_dev);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    flags[i] = alive[i] ? 1u : 0u;
+    flags[i] = alive[prev[i]] ? 1u : 0u;
+}
+
+__global__ void k_scatter_alive_list(const uint32_t* __restrict__ flags,
+                                     const uint32_t* __restrict__ scan,
+                                     const int32_t* __restrict__ prev, int64_t n_max,
+                                     const int32_t* __restrict__ n_dev, int32_t* __restrict__ active,
+                                     const uint32_t* __restrict__ total, int32_t* __restrict__ n_out,
+                                     int32_t* __restrict__ stat) {
+  const int64_t n = dev_count(n_max, n_dev);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (flags[i]) active[scan[i]] = prev[i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *n_out = (int32_t)*total;
+    *stat = (int32_t)*total;
+  }
 }
 
 // depth 1: every path was just initialised alive, so the live queue is the
@@ -65,19 +85,6 @@ __global__ void k_active_all(int64_t n, int32_t* __restrict__ active, int32_t* _
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *n_out = (int32_t)n;
     *stat = (int32_t)n;
-  }
-}
-
-__global__ void k_scatter_alive(const uint32_t* __restrict__ flags,
-                                const uint32_t* __restrict__ scan, int64_t n,
-                                int32_t* __restrict__ active, const uint32_t* __restrict__ total,
-                                int32_t* __restrict__ n_out, int32_t* __restrict__ stat) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    if (flags[i]) active[scan[i]] = (int32_t)i;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    *n_out = (int32_t)*total;
-    *stat = (int32_t)*total;
   }
 }
 
@@ -356,10 +363,12 @@ struct PassLayout {
   int n0;
   // buffers
   int32_t* active;
+  int32_t* active2;  // live queues of odd / even depths (each compacted from the other)
   uint32_t* flags;
   uint32_t* scan;
   uint32_t* total;
   int32_t* n_active;
+  int32_t* n_active2;
   double* hit_t;
   int32_t* hit_tri;
   int32_t* lam;
@@ -442,10 +451,12 @@ static void carve_pass(Arena& a, const wfpg_svo* svo, const wfpg_camera* cam,
   L.n0 = std::max(8, cfg->field_res);
   const int64_t P = L.P;
   L.active = a.take<int32_t>(P);
+  L.active2 = a.take<int32_t>(P);
   L.flags = a.take<uint32_t>(P + 1);
   L.scan = a.take<uint32_t>(P + 1);
   L.total = a.take<uint32_t>(4);
   L.n_active = a.take<int32_t>(4);
+  L.n_active2 = a.take<int32_t>(4);
   L.hit_t = a.take<double>(P);
   L.hit_tri = a.take<int32_t>(P);
   L.stats = a.take<StatsDev>(1);
@@ -630,27 +641,32 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
   if (!svo || last_bin_depth < 1) WFPG_TRY(rec_ev(cfg->ev_rec_counters));
 
   for (int depth = 1; depth <= cfg->max_depth; ++depth) {
-    // live queue (np.nonzero(state.alive), wavefront.py:227)
+    // live queue (np.nonzero(state.alive), wavefront.py:227): the identity at
+    // depth 1, then compacted from the previous depth's queue
+    int32_t* const act = (depth & 1) ? L.active2 : L.active;
+    int32_t* const n_act = (depth & 1) ? L.n_active2 : L.n_active;
     if (depth == 1) {
-      k_active_all<<<grid, 256, 0, st>>>(P, L.active, L.n_active, &L.stats->live[depth]);
+      k_active_all<<<grid, 256, 0, st>>>(P, act, n_act, &L.stats->live[depth]);
       WFPG_CHECK_LAUNCH("k_active_all");
     } else {
-      k_flags_alive<<<grid, 256, 0, st>>>(paths->alive, P, L.flags);
-      WFPG_CHECK_LAUNCH("k_flags_alive");
+      const int32_t* prev = (depth & 1) ? L.active : L.active2;
+      const int32_t* n_prev = (depth & 1) ? L.n_active : L.n_active2;
+      k_flags_alive_list<<<grid, 256, 0, st>>>(paths->alive, prev, P, n_prev, L.flags);
+      WFPG_CHECK_LAUNCH("k_flags_alive_list");
       {
         size_t mark = scratch.off;
-        WFPG_TRY(scan_u32(L.flags, L.scan, P, nullptr, L.total, scratch, st));
+        WFPG_TRY(scan_u32(L.flags, L.scan, P, n_prev, L.total, scratch, st));
         scratch.off = mark;
       }
-      k_scatter_alive<<<grid, 256, 0, st>>>(L.flags, L.scan, P, L.active, L.total, L.n_active,
-                                            &L.stats->live[depth]);
-      WFPG_CHECK_LAUNCH("k_scatter_alive");
+      k_scatter_alive_list<<<grid, 256, 0, st>>>(L.flags, L.scan, prev, P, n_prev, act, L.total,
+                                                 n_act, &L.stats->live[depth]);
+      WFPG_CHECK_LAUNCH("k_scatter_alive_list");
     }
     if (depth == 1 && sv.brute) {  // primary rays share the camera position
-      WFPG_TRY(launch_intersect_origin(sv, cam->position, paths->ray_d, L.active, P, L.n_active,
+      WFPG_TRY(launch_intersect_origin(sv, cam->position, paths->ray_d, act, P, n_act,
                                        scene->ray_eps, L.hit_t, L.hit_tri, st));
     } else {
-      WFPG_TRY(launch_intersect(sv, paths->ray_o, paths->ray_d, L.active, P, L.n_active,
+      WFPG_TRY(launch_intersect(sv, paths->ray_o, paths->ray_d, act, P, n_act,
                                 scene->ray_eps, L.hit_t, L.hit_tri, false, st));
     }
 
@@ -659,15 +675,15 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
     const int32_t* slots = nullptr;
     if (svo && depth <= last_bin_depth &&
         (!cfg->skip_unguided_bins || depth <= cfg->guided_depths || (depth == 1 && cfg->bin_image))) {
-      k_flags_lambert<<<grid, 256, 0, st>>>(sv, L.active, L.n_active, L.hit_tri, P, L.flags,
+      k_flags_lambert<<<grid, 256, 0, st>>>(sv, act, n_act, L.hit_tri, P, L.flags,
                                             L.stats->mats[depth]);
       WFPG_CHECK_LAUNCH("k_flags_lambert");
       {
         size_t mark = scratch.off;
-        WFPG_TRY(scan_u32(L.flags, L.scan, P, L.n_active, L.total, scratch, st));
+        WFPG_TRY(scan_u32(L.flags, L.scan, P, n_act, L.total, scratch, st));
         scratch.off = mark;
       }
-      k_scatter_lambert<<<grid, 256, 0, st>>>(L.active, L.n_active, L.flags, L.scan, P,
+      k_scatter_lambert<<<grid, 256, 0, st>>>(act, n_act, L.flags, L.scan, P,
                                               paths->ray_o, paths->ray_d, L.hit_t, L.lam,
                                               L.lam_pos, L.total, L.n_lam, &L.stats->lam[depth]);
       WFPG_CHECK_LAUNCH("k_scatter_lambert");
@@ -809,7 +825,7 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
         slots = L.bin_slot;
       }
     }
-    WFPG_TRY(launch_shade(sv, gv, pv, depth, L.active, P, L.n_active, L.hit_t, L.hit_tri, slots,
+    WFPG_TRY(launch_shade(sv, gv, pv, depth, act, P, n_act, L.hit_t, L.hit_tri, slots,
                           cfg->russian_roulette != 0, cfg->rr_depth, st));
   }
 
