@@ -35,8 +35,6 @@ __global__ void k_dep_emit(SvoView v, const int32_t* __restrict__ emit_depth,
                            int32_t* __restrict__ leaf, double* __restrict__ dirs,
                            double* __restrict__ rad) {
   const double nudge = (v.size / v.resolution) * 1e-3;
-  const double tiny = v.size * 1e-12;
-  const double lo[3] = {v.lox, v.loy, v.loz};
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x) {
     if (counts[p] == 0) continue;
@@ -56,12 +54,14 @@ __global__ void k_dep_emit(SvoView v, const int32_t* __restrict__ emit_depth,
       double d[3];
       for (int c = 0; c < 3; ++c) d[c] = __dsub_rn(prev[c], pos[c]);
       double nrm = norm_axis(d[0], d[1], d[2]);
+      // the reference clamps the nudged point into [lo + tiny, lo + size -
+      // tiny] before quantising; quantise's clamp of the cell index gives the
+      // same cell for every point (truncation is monotone), so the point
+      // clamp is not repeated here
       double q[3];
       for (int c = 0; c < 3; ++c) {
         d[c] = __ddiv_rn(d[c], nrm);
-        double x = __dadd_rn(pos[c], __dmul_rn(d[c], nudge));
-        x = fmin(fmax(x, __dadd_rn(lo[c], tiny)), __dsub_rn(__dadd_rn(lo[c], v.size), tiny));
-        q[c] = x;
+        q[c] = __dadd_rn(pos[c], __dmul_rn(d[c], nudge));
         dirs[3 * (int64_t)o + c] = d[c];
       }
       int32_t qx = quantise(q[0], v.lox, v.scale, v.resolution);
