@@ -331,7 +331,6 @@ struct SvoView {
   double lox, loy, loz, size;
   double scale;        // resolution / size
   double nudge;        // (size / resolution) * 1e-3 (_kernels.pyx:676)
-  double clo[3], chi[3];  // lo + size*1e-12, (lo + size) - size*1e-12 (:677-683)
   float half_log2_s0;     // 0.5 log2(size^2): best_cone_level's estimate (fp32)
   int32_t resolution, depth;
 };
@@ -352,11 +351,6 @@ __host__ inline SvoView make_view(const wfpg_svo* s) {
   v.size = s->size;
   v.scale = (double)s->resolution / s->size;
   v.nudge = (s->size / s->resolution) * 1e-3;
-  const double tiny = s->size * 1e-12;
-  for (int a = 0; a < 3; ++a) {
-    v.clo[a] = s->lo[a] + tiny;
-    v.chi[a] = s->lo[a] + s->size - tiny;
-  }
   v.half_log2_s0 = 0.5f * log2f((float)(s->size * s->size));
   v.resolution = s->resolution;
   v.depth = s->depth;
