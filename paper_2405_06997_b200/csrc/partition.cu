@@ -209,9 +209,11 @@ __global__ void k_part_bins(const uint32_t* __restrict__ keys, const uint32_t* _
     if (bin_slot) {
       uint32_t b = scan[i] + flags[i] - 1u;  // bin of this sorted position
       const int32_t p = item_path[vals[i]];
-      if (b < cap && p >= 0) {
-        bin_slot[p] = (int32_t)b;
-        if (need) need[b] = 1;
+      if (p >= 0) {
+        // every own item gets its slot written (-1 past the capacity), so
+        // the shade kernel's reads of Lambert paths need no prior reset
+        bin_slot[p] = b < cap ? (int32_t)b : -1;
+        if (need && b < cap) need[b] = 1;
       }
     }
     if (flags[i]) {

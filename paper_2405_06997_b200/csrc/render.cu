@@ -689,9 +689,11 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
       WFPG_CHECK_LAUNCH("k_scatter_lambert");
       const bool guided_depth = depth <= cfg->guided_depths;
       const bool want_image = depth == 1 && cfg->bin_image;
-      if (guided_depth || want_image) {
-        WFPG_CUDA(cudaMemsetAsync(L.bin_slot, 0xFF, sizeof(int32_t) * P, st));
-      }
+      // the partition writes the slot of every Lambert path it bins; the
+      // shade kernel reads slots of Lambert paths only (misses, emitters and
+      // mirrors return before), so only the bin image (every pixel) needs
+      // the -1 reset
+      if (want_image) WFPG_CUDA(cudaMemsetAsync(L.bin_slot, 0xFF, sizeof(int32_t) * P, st));
       if (!counters_waited) {  // the previous pass's partitions are done with the counters
         WFPG_TRY(wait_ev(cfg->ev_wait_counters));
         counters_waited = true;
