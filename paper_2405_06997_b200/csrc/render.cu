@@ -886,9 +886,16 @@ static int enqueue_pass(const wfpg_scene* scene, wfpg_svo* svo, const wfpg_camer
                              &L.stats->deposits, scratch, st, 2, L.dirty));
   }
   if (svo) WFPG_TRY(rec_ev(cfg->ev_rec_svo));
-  k_frame<<<(int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(L.n_pix, 256), kNumSMs * 8)), 256,
-            0, st>>>(paths->radiance, L.n_pix, cfg->n_samples, frame);
-  WFPG_CHECK_LAUNCH("k_frame");
+  if (cfg->n_samples == 1) {
+    // one sample: the mean (0 + r) / 1 is r itself (radiance sums are never
+    // -0), so the frame is a plain device copy of the radiance
+    WFPG_CUDA(cudaMemcpyAsync(frame, paths->radiance, sizeof(double) * 3 * (size_t)L.n_pix,
+                              cudaMemcpyDeviceToDevice, st));
+  } else {
+    k_frame<<<(int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(L.n_pix, 256), kNumSMs * 8)),
+              256, 0, st>>>(paths->radiance, L.n_pix, cfg->n_samples, frame);
+    WFPG_CHECK_LAUNCH("k_frame");
+  }
 
   return WFPG_OK;
 }
